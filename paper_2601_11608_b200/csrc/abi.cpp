@@ -1,0 +1,89 @@
+// abi.cpp -- the extern "C" boundary declared in include/widthfold_b200.h.
+// Argument validation, plan (re)construction and dispatch to the sm_100a
+// launchers. No allocation on the conv path; every call is stream-ordered.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <string>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+#include "widthfold_b200.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int> g_num_sms{0};
+
+wf_status fail(wf_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+int wf_abi_version(void) { return 1; }
+
+const char* wf_last_error(void) { return g_last_error.c_str(); }
+
+void wf_set_num_sms(int num_sms) { g_num_sms.store(num_sms < 0 ? 0 : num_sms); }
+
+wf_status wf_plan_fold(const wf_conv_desc* desc, int64_t f, int64_t group_size, wf_dtype in_dtype,
+                       wf_fold_plan* plan) {
+  if (!desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
+  wfb::Schedule S;
+  std::string err;
+  wf_status st = wfb::make_schedule(*desc, f, group_size, in_dtype, &S, &err);
+  if (st != WF_OK) return fail(st, err);
+  *plan = S.plan;
+  return WF_OK;
+}
+
+size_t wf_packed_filter_bytes(const wf_fold_plan* plan) {
+  if (!plan || plan->status != WF_FOLD_APPLY) return 0;
+  return static_cast<size_t>(plan->packed_bytes);
+}
+
+wf_status wf_expand_filter_pack(const void* w, const float* b, const wf_conv_desc* desc, const wf_fold_plan* plan,
+                                void* w_packed, float* b_rep, void* stream) {
+  if (!w || !desc || !plan || !w_packed) return fail(WF_INVALID_ARGUMENT, "null argument");
+  wfb::Schedule S;
+  std::string err;
+  wf_status st = wfb::schedule_from_plan(*desc, *plan, &S, &err);
+  if (st != WF_OK) return fail(st, err);
+  st = wfb::launch_pack(S, *desc, w, b, w_packed, b_rep, static_cast<cudaStream_t>(stream), &err);
+  if (st != WF_OK) return fail(st, err);
+  return WF_OK;
+}
+
+wf_status wf_expand_filter_dense(const float* w, const wf_conv_desc* desc, int64_t f, float* w_dense, void* stream) {
+  if (!w || !desc || !w_dense) return fail(WF_INVALID_ARGUMENT, "null argument");
+  std::string err;
+  wf_status st = wfb::validate_desc(*desc, &err);
+  if (st != WF_OK) return fail(st, err);
+  if (f < 1) return fail(WF_INVALID_ARGUMENT, "fold factor must be >= 1");
+  if (f % desc->stride_w != 0) return fail(WF_ILLEGAL_FOLD, "fold factor must be a multiple of stride_w");
+  st = wfb::launch_expand_dense(*desc, f, w, w_dense, static_cast<cudaStream_t>(stream), &err);
+  if (st != WF_OK) return fail(st, err);
+  return WF_OK;
+}
+
+wf_status wf_conv_fold_fwd(const void* x, const void* w_packed, const float* b_rep, void* y,
+                           const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype, uint32_t epilogue,
+                           void* stream) {
+  if (!x || !w_packed || !y || !desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
+  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU))
+    return fail(WF_INVALID_ARGUMENT, "unknown epilogue flags");
+  wfb::Schedule S;
+  std::string err;
+  wf_status st = wfb::schedule_from_plan(*desc, *plan, &S, &err);
+  if (st != WF_OK) return fail(st, err);
+  st = wfb::launch_conv(S, *desc, x, w_packed, b_rep, y, out_dtype, epilogue, static_cast<cudaStream_t>(stream),
+                        g_num_sms.load(), &err);
+  if (st != WF_OK) return fail(st, err);
+  return WF_OK;
+}
+
+}  // extern "C"

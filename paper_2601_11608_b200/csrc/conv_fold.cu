@@ -1,0 +1,469 @@
+// conv_fold.cu -- K2: folded implicit-GEMM first-layer convolution for sm_100a.
+//
+// Replaces the reference hot loop widthfold::conv2d (src/refconv.cpp:57-78)
+// run on the width-folded view (src/fold.cpp:113-143, a reshape) followed by
+// bias_add (src/refconv.cpp:82-95) and reconstruct_output (src/fold.cpp:228-259,
+// a reshape). One persistent, warp-specialised CTA per SM:
+//
+//   warp 0      TMA producer: once, the CTA's packed B operand (bulk copy);
+//               per 128-row M tile, one 5-D TMA box per H-stride residue that
+//               lands the canonical K-major core-matrix layout directly
+//               (plan.hpp explains the view); OOB rows/cols are zero-filled,
+//               which implements the conv padding.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, driven by the
+//               schedule table (a_off, b_off, tmem column, accumulate) built by
+//               plan.cpp; fp32 accumulators double-buffered in TMEM.
+//   warps 2..5  epilogue: tcgen05.ld -> +bias -> ReLU -> bf16/fp16/fp32 ->
+//               64B-swizzled staging smem -> TMA tensor store of final NHWC.
+//
+// Work split: CTA c serves N-tile (c % n_tiles) and M tiles
+// local, local + ctas_per_ntile, ... -- the B operand of its N-tile stays
+// resident in shared memory for the whole launch.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "kernels.hpp"
+#include "ptx.cuh"
+
+namespace wfb {
+
+struct ConvArgs {
+  const uint8_t* packed;  // schedule table at [0, table_bytes), B operands after
+  const float* bias;      // replicated bias (r*Cout fp32) or nullptr
+  long long table_bytes;
+  int num_mtiles, ohb, OHt, Wbox, Wfo, c0;
+  int s;
+  unsigned res_mask;
+  int amin[kMaxResidues];
+  int box_bytes, region_bytes;
+  int stages, stage_bytes;
+  int n_tiles, ctas_per_ntile;
+  int nt_entry0[kMaxNTiles], nt_entries[kMaxNTiles], nt_col0[kMaxNTiles], nt_cols[kMaxNTiles];
+  int nt_bbytes[kMaxNTiles];
+  long long nt_boff[kMaxNTiles];
+  int lbo_a, lbo_b;
+  unsigned idesc;
+  unsigned acc_stride, tmem_cols;
+  int epi_flags;
+  int off_stg, off_a, off_b, off_table, off_bias, stg_bytes;
+};
+
+struct TmaMaps {
+  CUtensorMap in[kMaxResidues];
+  CUtensorMap out;
+};
+
+template <typename OutT>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <>
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int kKind, typename OutT>
+__global__ void __launch_bounds__(192, 1)
+    conv_fold_kernel(const __grid_constant__ ConvArgs a, const __grid_constant__ TmaMaps maps) {
+  using namespace ptx;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t bar_full = base;          // [stages] x 8 B
+  const uint32_t bar_empty = base + 64;    // [stages] x 8 B
+  const uint32_t bar_tfull = base + 128;   // [2] x 8 B
+  const uint32_t bar_tempty = base + 144;  // [2] x 8 B
+  const uint32_t bar_b = base + 160;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + 192);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntile = blockIdx.x % a.n_tiles;
+  const int local = blockIdx.x / a.n_tiles;
+  const int entries = a.nt_entries[ntile];
+  const int ncols = a.nt_cols[ntile];
+  const int col0 = a.nt_col0[ntile];
+
+  // Schedule table and bias slice into shared memory.
+  {
+    const uint4* gtab = reinterpret_cast<const uint4*>(a.packed) + a.nt_entry0[ntile];
+    uint4* stab = reinterpret_cast<uint4*>(gbase + a.off_table);
+    for (int i = threadIdx.x; i < entries; i += blockDim.x) stab[i] = gtab[i];
+    float* sbias = reinterpret_cast<float*>(gbase + a.off_bias);
+    const bool has_bias = (a.bias != nullptr) && (a.epi_flags & WF_EPI_BIAS);
+    for (int i = threadIdx.x; i < ncols; i += blockDim.x) sbias[i] = has_bias ? a.bias[col0 + i] : 0.0f;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.stages; ++i) {
+      mbar_init(bar_full + 8 * i, 1);
+      mbar_init(bar_empty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_tfull + 8 * i, 1);
+      mbar_init(bar_tempty + 8 * i, 128);
+    }
+    mbar_init(bar_b, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    for (int b = 0; b < a.s; ++b)
+      if ((a.res_mask >> b) & 1u) prefetch_tmap(&maps.in[b]);
+    prefetch_tmap(&maps.out);
+  }
+  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), a.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint8_t* gb = a.packed + a.table_bytes + a.nt_boff[ntile];
+      const int bb = a.nt_bbytes[ntile];
+      mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
+      for (int off = 0; off < bb; off += 32768)
+        bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
+      const uint32_t tx = static_cast<uint32_t>(a.box_bytes * __popc(a.res_mask));
+      int it = 0;
+      for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it) {
+        const int stage = it % a.stages;
+        const uint32_t round = static_cast<uint32_t>(it / a.stages);
+        mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
+        const int n = mt / a.ohb;
+        const int oh0 = (mt - n * a.ohb) * a.OHt;
+        const uint32_t dst = base + a.off_a + stage * a.stage_bytes;
+        mbar_arrive_expect_tx(bar_full + 8 * stage, tx);
+        for (int b = 0; b < a.s; ++b)
+          if ((a.res_mask >> b) & 1u)
+            tma_load_5d(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n,
+                        bar_full + 8 * stage);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      const uint4* stab = reinterpret_cast<const uint4*>(gbase + a.off_table);
+      const uint32_t b_base = base + a.off_b;
+      mbar_wait(bar_b, 0);
+      int it = 0;
+      for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it) {
+        const int stage = it % a.stages;
+        const uint32_t round = static_cast<uint32_t>(it / a.stages);
+        const int acc = it & 1;
+        const uint32_t acc_round = static_cast<uint32_t>(it >> 1);
+        mbar_wait(bar_tempty + 8 * acc, (acc_round & 1u) ^ 1u);
+        mbar_wait(bar_full + 8 * stage, round & 1u);
+        tc_fence_after();
+        const uint32_t a_base = base + a.off_a + stage * a.stage_bytes;
+        const uint32_t d_base = tmem_base + acc * a.acc_stride;
+        for (int i = 0; i < entries; ++i) {
+          const uint4 e = stab[i];
+          mma<kKind>(d_base + e.w, smem_desc(a_base + e.x, a.lbo_a, 128), smem_desc(b_base + e.y, a.lbo_b, 128),
+                     a.idesc, e.z >> 31);
+        }
+        mma_commit(bar_empty + 8 * stage);
+        mma_commit(bar_tfull + 8 * acc);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    constexpr int CC = 64 / static_cast<int>(sizeof(OutT));  // columns per 64-byte staging row
+    const int quarter = warp & 3;                              // TMEM lanes [32q, 32q+32)
+    const int m = quarter * 32 + lane;
+    const int t = m / a.Wbox;
+    const int wq = m - t * a.Wbox;
+    const bool valid = (t < a.OHt) && (wq < a.Wfo);
+    const uint32_t srow = static_cast<uint32_t>(t * a.Wfo + wq);
+    const int nchunks = ncols / CC;
+    const bool leader = (threadIdx.x == 64);
+    const bool relu = (a.epi_flags & WF_EPI_RELU) != 0;
+    const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
+    uint32_t stg_i = 0;
+    int it = 0;
+    for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_round = static_cast<uint32_t>(it >> 1);
+      const int n = mt / a.ohb;
+      const int oh0 = (mt - n * a.ohb) * a.OHt;
+      mbar_wait(bar_tfull + 8 * acc, acc_round & 1u);
+      tc_fence_after();
+      const uint32_t trow = tmem_base + acc * a.acc_stride + (static_cast<uint32_t>(quarter * 32) << 16);
+      for (int ch = 0; ch < nchunks; ++ch) {
+        float v[CC];
+        if constexpr (CC == 32) {
+          uint32_t r[32];
+          tmem_ld32(trow + ch * CC, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
+        } else {
+          uint32_t r[16];
+          tmem_ld16(trow + ch * CC, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+        }
+        if (ch == nchunks - 1) {
+          tc_fence_before();
+          mbar_arrive(bar_tempty + 8 * acc);
+        }
+#pragma unroll
+        for (int k = 0; k < CC; ++k) {
+          float x = v[k] + sbias[ch * CC + k];
+          if (relu) x = (x < 0.0f) ? 0.0f : x;
+          v[k] = x;
+        }
+        const uint32_t buf = base + a.off_stg + (stg_i & 1u) * a.stg_bytes;
+        named_bar_sync(1, 128);
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t lin = srow * 64u + q * 16u;
+            const uint32_t swz = lin ^ (((lin >> 7) & 3u) << 4);
+            uint32_t w0, w1, w2, w3;
+            if constexpr (sizeof(OutT) == 4) {
+              w0 = __float_as_uint(v[q * 4 + 0]);
+              w1 = __float_as_uint(v[q * 4 + 1]);
+              w2 = __float_as_uint(v[q * 4 + 2]);
+              w3 = __float_as_uint(v[q * 4 + 3]);
+            } else {
+              w0 = pack2<OutT>(v[q * 8 + 0], v[q * 8 + 1]);
+              w1 = pack2<OutT>(v[q * 8 + 2], v[q * 8 + 3]);
+              w2 = pack2<OutT>(v[q * 8 + 4], v[q * 8 + 5]);
+              w3 = pack2<OutT>(v[q * 8 + 6], v[q * 8 + 7]);
+            }
+            st_shared_v4(buf + swz, w0, w1, w2, w3);
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (leader) {
+          tma_store_4d(&maps.out, buf, col0 + ch * CC, 0, oh0, n);
+          bulk_commit();
+          bulk_wait_read_1();
+        }
+        ++stg_i;
+      }
+    }
+    if (leader) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, a.tmem_cols);
+  }
+}
+
+// ============================== host side ==============================
+
+namespace {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode(std::string* err) {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) *err = "cuTensorMapEncodeTiled unavailable (driver too old?)";
+  return fn;
+}
+
+CUtensorMapDataType tmap_type(wf_dtype t) {
+  switch (t) {
+    case WF_BF16: return CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    case WF_F16: return CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    default: return CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  }
+}
+
+uint32_t pow2ceil(uint32_t v) {
+  uint32_t p = 32;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+template <int kKind, typename OutT>
+cudaError_t launch_typed(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st) {
+  auto kern = conv_fold_kernel<kKind, OutT>;
+  static int configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  kern<<<grid, 192, smem, st>>>(args, maps);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, const void* packed,
+                      const float* b_rep, void* y, wf_dtype out_dtype, uint32_t epilogue, cudaStream_t st,
+                      int num_sms, std::string* err) {
+  const wf_fold_plan& p = S.plan;
+  const wf_dtype in_t = static_cast<wf_dtype>(p.in_dtype);
+  if (out_dtype != WF_F32 && out_dtype != WF_BF16 && out_dtype != WF_F16) {
+    *err = "output dtype must be f32, bf16 or f16";
+    return WF_INVALID_ARGUMENT;
+  }
+  if ((epilogue & WF_EPI_BIAS) && b_rep == nullptr) {
+    *err = "bias epilogue requested without a replicated bias";
+    return WF_INVALID_ARGUMENT;
+  }
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(packed)) & 15u) {
+    *err = "x, y and the packed filter must be 16-byte aligned";
+    return WF_INVALID_ARGUMENT;
+  }
+  const int oes = elem_bytes(out_dtype);
+  const int CC = 64 / oes;
+  for (const auto& t : S.ntiles)
+    if (t.cols % CC != 0) {
+      *err = "N-tile width not a multiple of the epilogue chunk";
+      return WF_UNSUPPORTED;
+    }
+  EncodeTiledFn encode = get_encode(err);
+  if (!encode) return WF_CUDA_ERROR;
+
+  ConvArgs a{};
+  TmaMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  a.packed = static_cast<const uint8_t*>(packed);
+  a.bias = b_rep;
+  a.table_bytes = p.table_bytes;
+  a.OHt = static_cast<int>(p.tile_rows);
+  a.Wbox = static_cast<int>(p.wbox);
+  a.Wfo = static_cast<int>(p.wfo);
+  a.c0 = static_cast<int>(p.c0);
+  a.s = S.s;
+  a.ohb = static_cast<int>(S.ohb);
+  a.num_mtiles = static_cast<int>(S.num_mtiles);
+  a.res_mask = 0;
+  for (int b = 0; b < S.s; ++b) {
+    if (S.has_res[b]) a.res_mask |= 1u << b;
+    a.amin[b] = S.amin[b];
+  }
+  const int U = S.U;
+  a.box_bytes = 2 * U * S.lbo_a;
+  a.region_bytes = S.region_bytes;
+  a.stages = S.stages;
+  a.stage_bytes = S.stage_bytes;
+  a.n_tiles = static_cast<int>(S.ntiles.size());
+  uint32_t max_cols = 0;
+  for (int i = 0; i < a.n_tiles; ++i) {
+    const NTile& t = S.ntiles[i];
+    a.nt_entry0[i] = t.entry0;
+    a.nt_entries[i] = t.entries;
+    a.nt_col0[i] = t.col0;
+    a.nt_cols[i] = t.cols;
+    a.nt_bbytes[i] = static_cast<int>(t.b_bytes);
+    a.nt_boff[i] = t.b_off;
+    max_cols = std::max<uint32_t>(max_cols, static_cast<uint32_t>(t.cols));
+  }
+  if (num_sms <= 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  a.ctas_per_ntile = std::max(1, std::min<int>(num_sms / a.n_tiles, a.num_mtiles));
+  a.lbo_a = S.lbo_a;
+  a.lbo_b = S.Ng * 16;
+  const uint32_t fmt = (in_t == WF_BF16) ? 1u : (in_t == WF_F16 ? 0u : 2u);
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((static_cast<uint32_t>(S.Ng) >> 3) << 17) |
+            ((static_cast<uint32_t>(kTileM) >> 4) << 24);
+  a.acc_stride = pow2ceil(max_cols);
+  a.tmem_cols = 2 * a.acc_stride;
+  a.epi_flags = static_cast<int>(epilogue);
+  // shared-memory carve-up (offsets from the 1024-aligned base)
+  a.stg_bytes = kStagingBytes / 2;  // 128 rows x 64 B
+  a.off_stg = 1024;
+  a.off_a = a.off_stg + 2 * a.stg_bytes;
+  a.off_b = a.off_a + a.stages * a.stage_bytes + kTileM * 16;
+  a.off_b = (a.off_b + 127) / 128 * 128;
+  a.off_table = a.off_b + S.b_smem_bytes;
+  a.off_bias = a.off_table + (S.table_smem_bytes + 127) / 128 * 128;
+  const int smem = a.off_bias + kMaxAccCols * 4 + 1024;
+  if (smem > kSmemLimit) {
+    *err = "shared-memory budget exceeded";
+    return WF_UNSUPPORTED;
+  }
+
+  // ---- tensor maps --------------------------------------------------------------
+  const int es = S.esize;
+  const cuuint64_t rowpitch = static_cast<cuuint64_t>(d.w) * d.c * es;
+  const cuuint64_t pix = static_cast<cuuint64_t>(p.f) * d.c * es;
+  for (int b = 0; b < S.s; ++b) {
+    if (!S.has_res[b]) continue;
+    const cuuint64_t rows_b = static_cast<cuuint64_t>((d.h - b + S.s - 1) / S.s);
+    cuuint64_t gdim[5] = {static_cast<cuuint64_t>(16 / es), static_cast<cuuint64_t>(p.wf), rows_b,
+                          static_cast<cuuint64_t>(2 * U), static_cast<cuuint64_t>(d.n)};
+    cuuint64_t gstr[4] = {pix, rowpitch * S.s, 16, rowpitch * d.h};
+    cuuint32_t box[5] = {static_cast<cuuint32_t>(16 / es), static_cast<cuuint32_t>(p.wbox),
+                         static_cast<cuuint32_t>(p.nrows), static_cast<cuuint32_t>(2 * U), 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    void* gaddr = const_cast<uint8_t*>(static_cast<const uint8_t*>(x) + b * rowpitch);
+    CUresult r = encode(&maps.in[b], tmap_type(in_t), 5, gaddr, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "cuTensorMapEncodeTiled(input) failed: " + std::to_string(static_cast<int>(r));
+      return WF_CUDA_ERROR;
+    }
+  }
+  {
+    const cuuint64_t cf = static_cast<cuuint64_t>(p.cout_f);
+    cuuint64_t gdim[4] = {cf, static_cast<cuuint64_t>(p.wfo), static_cast<cuuint64_t>(p.oh),
+                          static_cast<cuuint64_t>(d.n)};
+    cuuint64_t gstr[3] = {cf * oes, static_cast<cuuint64_t>(p.ow) * d.cout * oes,
+                          static_cast<cuuint64_t>(p.oh) * p.ow * d.cout * oes};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(CC), static_cast<cuuint32_t>(p.wfo),
+                         static_cast<cuuint32_t>(p.tile_rows), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(&maps.out, tmap_type(out_dtype), 4, y, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "cuTensorMapEncodeTiled(output) failed: " + std::to_string(static_cast<int>(r));
+      return WF_CUDA_ERROR;
+    }
+  }
+
+  const int grid = a.n_tiles * a.ctas_per_ntile;
+  cudaError_t e;
+  const bool tf32 = (in_t == WF_TF32);
+  if (out_dtype == WF_BF16)
+    e = tf32 ? launch_typed<1, __nv_bfloat16>(a, maps, grid, smem, st) : launch_typed<0, __nv_bfloat16>(a, maps, grid, smem, st);
+  else if (out_dtype == WF_F16)
+    e = tf32 ? launch_typed<1, __half>(a, maps, grid, smem, st) : launch_typed<0, __half>(a, maps, grid, smem, st);
+  else
+    e = tf32 ? launch_typed<1, float>(a, maps, grid, smem, st) : launch_typed<0, float>(a, maps, grid, smem, st);
+  if (e != cudaSuccess) {
+    *err = std::string("conv_fold_kernel launch failed: ") + cudaGetErrorString(e);
+    return WF_CUDA_ERROR;
+  }
+  return WF_OK;
+}
+
+}  // namespace wfb

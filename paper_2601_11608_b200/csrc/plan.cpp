@@ -1,0 +1,322 @@
+// plan.cpp -- see plan.hpp for the geometry and the schedule it produces.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <numeric>
+
+namespace wfb {
+
+namespace {
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t floor_div(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+  return q;
+}
+int64_t pos_mod(int64_t a, int64_t b) { return ((a % b) + b) % b; }
+
+wf_fold_plan fallback(wf_fold_reason reason, int64_t f) {
+  wf_fold_plan p{};
+  p.status = WF_FOLD_FALLBACK;
+  p.reason = reason;
+  p.f = f;
+  return p;
+}
+
+}  // namespace
+
+int elem_bytes(wf_dtype t) {
+  switch (t) {
+    case WF_BF16: case WF_F16: return 2;
+    case WF_TF32: case WF_F32: return 4;
+  }
+  return 0;
+}
+
+wf_status validate_desc(const wf_conv_desc& d, std::string* err) {
+  const int64_t ext[7] = {d.n, d.h, d.w, d.c, d.kh, d.kw, d.cout};
+  for (int64_t e : ext) {
+    if (e < 1) {
+      *err = "conv extents must be >= 1";
+      return WF_SHAPE_MISMATCH;
+    }
+  }
+  if (d.stride_h < 1 || d.stride_w < 1) {
+    *err = "strides must be >= 1";
+    return WF_SHAPE_MISMATCH;
+  }
+  if (d.pad_h < 0 || d.pad_w < 0) {
+    *err = "padding must be >= 0";
+    return WF_SHAPE_MISMATCH;
+  }
+  if (d.h + 2 * d.pad_h < d.kh || d.w + 2 * d.pad_w < d.kw) {
+    *err = "padded input smaller than the filter: empty output";
+    return WF_DEGENERATE_OUTPUT;
+  }
+  return WF_OK;
+}
+
+wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
+                        wf_dtype in_dtype, Schedule* out, std::string* err) {
+  wf_status st = validate_desc(d, err);
+  if (st != WF_OK) return st;
+  if (in_dtype != WF_BF16 && in_dtype != WF_F16 && in_dtype != WF_TF32) {
+    *err = "input dtype must be bf16, f16 or tf32";
+    return WF_INVALID_ARGUMENT;
+  }
+  if (f_req < 0 || gs_req < 0) {
+    *err = "fold factor / group size must be >= 0 (0 = auto)";
+    return WF_INVALID_ARGUMENT;
+  }
+  Schedule S;
+  S.esize = elem_bytes(in_dtype);
+  S.E = 32 / S.esize;
+  const int64_t sh = d.stride_h, sw = d.stride_w;
+  S.s = static_cast<int>(sh);
+  S.ph = static_cast<int>(d.pad_h);
+  S.pw = static_cast<int>(d.pad_w);
+  const int64_t OH = (d.h + 2 * d.pad_h - d.kh) / sh + 1;
+  const int64_t OW = (d.w + 2 * d.pad_w - d.kw) / sw + 1;
+
+  // ---- fold factor ------------------------------------------------------
+  int64_t f = f_req;
+  if (f == 0) {
+    // smallest f: multiple of the W stride, 32-byte folded pixel, divides W,
+    // r*Cout groupable (the auto rule of choose_fold_factor, src/fold.cpp:67-90,
+    // with the tcgen05 K-step as the alignment target).
+    const int64_t pix = d.c * S.esize;
+    const int64_t base_align = 32 / std::gcd<int64_t>(pix, 32);
+    const int64_t base = std::lcm<int64_t>(base_align, sw);
+    wf_fold_plan first{};
+    bool have = false;
+    for (int64_t cand = base; cand <= d.w; cand += base) {
+      Schedule tmp;
+      std::string e2;
+      wf_status s2 = make_schedule(d, cand, gs_req, in_dtype, &tmp, &e2);
+      if (s2 != WF_OK) {
+        *err = e2;
+        return s2;
+      }
+      if (tmp.plan.status == WF_FOLD_APPLY) {
+        *out = std::move(tmp);
+        return WF_OK;
+      }
+      if (!have) {
+        first = tmp.plan;
+        have = true;
+      }
+    }
+    S.plan = have ? first : fallback(WF_REASON_FACTOR_TOO_LARGE, base);
+    *out = std::move(S);
+    return WF_OK;
+  }
+  if (d.w % f != 0) { S.plan = fallback(WF_REASON_WIDTH_NOT_DIVISIBLE, f); *out = S; return WF_OK; }
+  if (f % sw != 0) { S.plan = fallback(WF_REASON_STRIDE_ON_FOLD_AXIS, f); *out = S; return WF_OK; }
+  if ((f * d.c * S.esize) % 32 != 0) { S.plan = fallback(WF_REASON_UNALIGNED_PIXEL, f); *out = S; return WF_OK; }
+  const int64_t r = f / sw;
+  if (OW % r != 0) { S.plan = fallback(WF_REASON_OUTPUT_TAIL, f); *out = S; return WF_OK; }
+  if (d.h < sh) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
+
+  const int64_t c0 = -ceil_div(d.pad_w, f);
+  const int64_t kwf = floor_div(f - sw - d.pad_w + d.kw - 1, f) - c0 + 1;
+  const int64_t Wf = d.w / f, Wfo = OW / r;
+  const int64_t U = f * d.c * S.esize / 32;
+  S.U = static_cast<int>(U);
+  const int64_t Wbox = Wfo + kwf - 1;
+  if (Wbox > kTileM || U * 2 > 256) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
+  int64_t OHt = std::min<int64_t>(kTileM / Wbox, OH);
+
+  // ---- residues of the H stride -----------------------------------------
+  if (sh > kMaxResidues) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
+  for (int b = 0; b < sh; ++b) { S.has_res[b] = false; S.amin[b] = 0; S.amax[b] = 0; }
+  for (int64_t kh = 0; kh < d.kh; ++kh) {
+    const int64_t delta = kh - d.pad_h;
+    const int b = static_cast<int>(pos_mod(delta, sh));
+    const int a = static_cast<int>((delta - b) / sh);
+    if (!S.has_res[b]) { S.has_res[b] = true; S.amin[b] = a; S.amax[b] = a; }
+    S.amin[b] = std::min(S.amin[b], a);
+    S.amax[b] = std::max(S.amax[b], a);
+  }
+  int64_t NR = 0;
+  for (int b = 0; b < sh; ++b)
+    if (S.has_res[b]) NR = std::max<int64_t>(NR, OHt + S.amax[b] - S.amin[b]);
+  if (NR > 256) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
+  S.lbo_a = static_cast<int>(NR * Wbox * 16);
+  S.region_bytes = static_cast<int>(((2 * U * S.lbo_a) + 127) / 128 * 128);
+  S.stage_bytes = static_cast<int>(sh) * S.region_bytes;
+
+  // ---- MMA groups ---------------------------------------------------------
+  int64_t gs = gs_req;
+  if (gs == 0) {
+    int64_t best = 0;
+    for (int64_t g = 1; g <= r; ++g) {
+      if (r % g || (g * d.cout) % 16 || g * d.cout > kMaxAccCols) continue;
+      if (best == 0 || (best * d.cout < 64)) best = g;
+      if (best * d.cout >= 64) break;
+    }
+    gs = best;
+  }
+  if (gs == 0 || r % gs || (gs * d.cout) % 16 || gs * d.cout > kMaxAccCols) {
+    S.plan = fallback(WF_REASON_UNSUPPORTED_CHANNELS, f);
+    *out = S;
+    return WF_OK;
+  }
+  const int64_t G = r / gs;
+  S.Ng = static_cast<int>(gs * d.cout);
+  std::vector<int64_t> lo(G), hi(G);
+  for (int64_t g = 0; g < G; ++g) {
+    lo[g] = INT64_MAX;
+    hi[g] = -1;
+    for (int64_t j = g * gs; j < (g + 1) * gs; ++j) {
+      const int64_t off = ((-c0) * f + j * sw - d.pad_w) * d.c;
+      lo[g] = std::min(lo[g], off / S.E);
+      hi[g] = std::max(hi[g], (off + d.kw * d.c - 1) / S.E);
+    }
+  }
+  const int64_t block_bytes = static_cast<int64_t>(S.Ng) * 32;  // 2 core cols x Ng rows x 16 B
+  auto group_b_bytes = [&](int64_t g) { return d.kh * (hi[g] - lo[g] + 1) * block_bytes; };
+
+  // ---- N-tiles and shared-memory budget ------------------------------------
+  const int ctrl_bytes = 1024;
+  const int staging = kStagingBytes;   // two 8 KB epilogue buffers
+  const int a_pad = kTileM * 16;
+  const int bias_bytes = kMaxAccCols * 4;
+  int64_t b_budget = 128 * 1024;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    S.ntiles.clear();
+    bool ok = true;
+    int64_t g = 0;
+    while (g < G) {
+      NTile t{};
+      t.g0 = static_cast<int>(g);
+      int64_t cols = 0, bytes = 0;
+      while (g < G && cols + S.Ng <= kMaxAccCols && bytes + group_b_bytes(g) <= b_budget) {
+        cols += S.Ng;
+        bytes += group_b_bytes(g);
+        ++g;
+      }
+      if (g == t.g0) { ok = false; break; }
+      t.g1 = static_cast<int>(g);
+      t.col0 = static_cast<int>(t.g0 * S.Ng);
+      t.cols = static_cast<int>(cols);
+      t.b_bytes = bytes;
+      S.ntiles.push_back(t);
+    }
+    if (!ok || S.ntiles.size() > static_cast<size_t>(kMaxNTiles)) {
+      S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
+      *out = S;
+      return WF_OK;
+    }
+    int64_t max_b = 0, max_entries = 0;
+    for (auto& t : S.ntiles) {
+      max_b = std::max(max_b, t.b_bytes);
+      int64_t e = 0;
+      for (int gg = t.g0; gg < t.g1; ++gg) e += d.kh * (hi[gg] - lo[gg] + 1);
+      max_entries = std::max(max_entries, e);
+    }
+    const int64_t table_b = max_entries * 16;
+    const int64_t fixed = ctrl_bytes + staging + a_pad + 128 + (max_b + 127) / 128 * 128 +
+                          (table_b + 127) / 128 * 128 + bias_bytes + 1024;
+    int stages = 0;
+    for (int st2 = 4; st2 >= 2; --st2)
+      if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { stages = st2; break; }
+    if (stages >= 2) {
+      S.stages = stages;
+      S.b_smem_bytes = static_cast<int>((max_b + 127) / 128 * 128);
+      S.table_smem_bytes = static_cast<int>(table_b);
+      S.smem_bytes = static_cast<int>(fixed + static_cast<int64_t>(stages) * S.stage_bytes);
+      break;
+    }
+    b_budget /= 2;
+    if (attempt == 7 || b_budget < block_bytes) {
+      S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
+      *out = S;
+      return WF_OK;
+    }
+  }
+
+  // ---- the schedule: per N-tile, kh -> group -> unit ------------------------
+  S.entries.clear();
+  int64_t b_cursor = 0;
+  for (auto& t : S.ntiles) {
+    t.entry0 = static_cast<int>(S.entries.size());
+    t.b_off = b_cursor;
+    uint32_t boff = 0;
+    for (int64_t kh = 0; kh < d.kh; ++kh) {
+      const int64_t delta = kh - d.pad_h;
+      const int b = static_cast<int>(pos_mod(delta, sh));
+      const int a = static_cast<int>((delta - b) / sh);
+      for (int gg = t.g0; gg < t.g1; ++gg) {
+        for (int64_t u = lo[gg]; u <= hi[gg]; ++u) {
+          const int64_t kp = u / U, uq = u % U;
+          MmaEntry e{};
+          e.a_off = static_cast<uint32_t>(b * S.region_bytes +
+                                          ((a - S.amin[b]) * Wbox + kp) * 16 +
+                                          2 * uq * S.lbo_a);
+          e.b_off = boff;
+          boff += static_cast<uint32_t>(block_bytes);
+          const bool acc = !(kh == 0 && u == lo[gg]);
+          e.meta = static_cast<uint32_t>(kh) | (static_cast<uint32_t>(u) << 8) |
+                   (static_cast<uint32_t>(gg) << 16) | (acc ? 0x80000000u : 0u);
+          e.tmem_col = static_cast<uint32_t>((gg - t.g0) * S.Ng);
+          S.entries.push_back(e);
+        }
+      }
+    }
+    t.entries = static_cast<int>(S.entries.size()) - t.entry0;
+    b_cursor += t.b_bytes;
+  }
+
+  // ---- plan facts -----------------------------------------------------------
+  wf_fold_plan& p = S.plan;
+  p = wf_fold_plan{};
+  p.status = WF_FOLD_APPLY;
+  p.reason = WF_REASON_NONE;
+  p.f = f;
+  p.r = r;
+  p.c0 = c0;
+  p.kw_f = kwf;
+  p.k_f = d.kh * kwf * f * d.c;
+  p.cout_f = r * d.cout;
+  p.in_dtype = in_dtype;
+  p.elem_bytes = S.esize;
+  p.oh = OH;
+  p.ow = OW;
+  p.wf = Wf;
+  p.wfo = Wfo;
+  p.units_per_px = U;
+  p.group_size = gs;
+  p.n_groups = G;
+  p.n_tiles = static_cast<int64_t>(S.ntiles.size());
+  p.tile_rows = OHt;
+  p.wbox = Wbox;
+  p.nrows = NR;
+  p.mma_entries = static_cast<int64_t>(S.entries.size());
+  p.table_bytes = (p.mma_entries * 16 + 127) / 128 * 128;
+  p.packed_bytes = p.table_bytes + b_cursor;
+  S.ohb = ceil_div(OH, OHt);
+  S.num_mtiles = d.n * S.ohb;
+  p.useful_macs = static_cast<uint64_t>(d.n) * OH * OW * d.cout * d.kh * d.kw * d.c;
+  p.issued_macs = static_cast<uint64_t>(S.num_mtiles) * p.mma_entries * kTileM * S.Ng * S.E;
+  *out = std::move(S);
+  return WF_OK;
+}
+
+wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
+                             Schedule* out, std::string* err) {
+  if (p.status != WF_FOLD_APPLY) {
+    *err = "plan is not an Apply plan";
+    return WF_INVALID_ARGUMENT;
+  }
+  wf_status st = make_schedule(d, p.f, p.group_size, static_cast<wf_dtype>(p.in_dtype), out, err);
+  if (st != WF_OK) return st;
+  if (out->plan.status != WF_FOLD_APPLY || out->plan.packed_bytes != p.packed_bytes ||
+      out->plan.mma_entries != p.mma_entries) {
+    *err = "plan does not match this conv descriptor";
+    return WF_SHAPE_MISMATCH;
+  }
+  return WF_OK;
+}
+
+}  // namespace wfb

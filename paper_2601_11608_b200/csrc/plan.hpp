@@ -1,0 +1,95 @@
+// plan.hpp -- generalized width-fold planner and tcgen05 schedule builder.
+//
+// Host-only, pure. Turns a conv problem (x NHWC, w HWIO, stride, padding) and
+// a fold factor into (a) the FoldPlan facts the reference exposes
+// (/root/reference/proj/include/widthfold/fold.hpp:28-37) and (b) the exact
+// list of tcgen05.mma instructions one 128-row M tile issues.
+//
+// Geometry (the reference stops at KW == 1,
+// src/fold.cpp:51-65):
+//   r   = f / s                     output columns per folded column
+//   c0  = -ceil(pw / f)             first folded column an output reads
+//   KW' = floor((f-s-pw+KW-1)/f) - c0 + 1
+//   folded output column w' covers ow = w'*r + j, j in [0, r); for input row
+//   kh its window is the KW*C contiguous elements starting at element
+//   off_j = (-c0*f + j*s - pw)*C of the KW'*f*C "window row".
+//
+// Shared-memory A operand (K-major, no swizzle, canonical 8x16 B core
+// matrices): for each residue b = (kh - ph) mod s a region
+//   [core column q in 0..2U)[input row i in 0..NR)[folded col w'' in 0..Wbox)[16 B]
+// loaded by ONE 5-D TMA box (non-monotonic strides, probed on B200). The M row
+// m = t*Wbox + w' of kh's operand is smem row ((a-amin_b)*Wbox + w' + kw'),
+// so every (kh, kw') view is the same buffer at a 16-byte-aligned row shift
+// (descriptor start address), i.e. each input byte is fetched once per tile.
+//
+// K is cut into 32-byte "units" (one MMA K-step: 16 bf16/fp16 or 8 tf32) that
+// never straddle a folded pixel (f*C*elem % 32 == 0). Output columns are split
+// into groups of `group_size` sub-columns j; group g issues only the units its
+// windows touch -- the tensor-core analogue of grouped_conv
+// (src/blockdiag.cpp:138-187), which skips the structural zeros of the
+// block-diagonal expansion.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "widthfold_b200.h"
+
+namespace wfb {
+
+constexpr int kTileM = 128;           // tcgen05 M (cta_group::1)
+constexpr int kMaxAccCols = 256;      // accumulator columns per N-tile (x2 buffers)
+constexpr int kMaxResidues = 8;
+constexpr int kMaxNTiles = 16;
+constexpr int kSmemLimit = 227 * 1024;
+constexpr int kStagingBytes = 16 * 1024;  // one epilogue staging buffer
+
+struct MmaEntry {          // 16 bytes, lives in the packed buffer and in smem
+  uint32_t a_off;          // byte offset of the A view inside an A stage
+  uint32_t b_off;          // byte offset of the B block inside the N-tile's B
+  uint32_t meta;           // kh | u << 8 | g << 16 | accumulate << 31
+  uint32_t tmem_col;       // accumulator column of the group
+};
+
+struct NTile {
+  int g0, g1;              // groups [g0, g1)
+  int col0, cols;          // output columns [col0, col0 + cols) of the r*Cout row
+  int entry0, entries;     // slice of the schedule
+  int64_t b_off, b_bytes;  // B region inside the packed buffer (after the table)
+};
+
+struct Schedule {
+  wf_fold_plan plan{};
+  int s = 1, ph = 0, pw = 0;
+  int esize = 2;                 // input element bytes
+  int E = 16;                    // elements per 32-byte unit
+  int U = 1;                     // units per folded pixel
+  int Ng = 64;                   // accumulator columns per group
+  int amin[kMaxResidues] = {0};
+  int amax[kMaxResidues] = {0};
+  bool has_res[kMaxResidues] = {false};
+  int region_bytes = 0, stage_bytes = 0, lbo_a = 0;
+  int stages = 2;
+  int smem_bytes = 0, b_smem_bytes = 0, table_smem_bytes = 0;
+  int64_t num_mtiles = 0, ohb = 0;
+  std::vector<MmaEntry> entries;
+  std::vector<NTile> ntiles;
+};
+
+// Validates the descriptor like ConvSpec::validate (src/refconv.cpp:5-32) plus
+// padding; throws nothing: returns a status and fills `err`.
+wf_status validate_desc(const wf_conv_desc& d, std::string* err);
+
+// Full planner. Returns WF_OK with plan.status == APPLY or FALLBACK (reason),
+// or an error status (shape problems, bad arguments).
+wf_status make_schedule(const wf_conv_desc& d, int64_t f, int64_t group_size,
+                        wf_dtype in_dtype, Schedule* out, std::string* err);
+
+// Rebuild the schedule from a plan previously returned by make_schedule.
+wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
+                             Schedule* out, std::string* err);
+
+int elem_bytes(wf_dtype t);
+
+}  // namespace wfb
