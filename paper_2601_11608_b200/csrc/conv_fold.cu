@@ -33,11 +33,12 @@
 
 namespace wfb {
 
+constexpr int kMaxTable = 384;  // schedule entries per launch (constant bank)
+
 struct ConvArgs {
-  const uint8_t* packed;  // schedule table at [0, table_bytes), B operands after
-  const float* bias;      // replicated bias (r*Cout fp32) or nullptr
-  long long table_bytes;
-  int num_mtiles, ohb, OHt, Wbox, Wfo, c0;
+  const float* bias;  // replicated bias (r*Cout fp32) or nullptr
+  uint8_t* out;       // y (n, oh, ow, cout) NHWC
+  int num_mtiles, ohb, OHt, OH, Wbox, Wfo, c0;
   int s;
   unsigned res_mask;
   int amin[kMaxResidues];
@@ -46,17 +47,19 @@ struct ConvArgs {
   int n_tiles, ctas_per_ntile;
   int nt_entry0[kMaxNTiles], nt_entries[kMaxNTiles], nt_col0[kMaxNTiles], nt_cols[kMaxNTiles];
   int nt_bbytes[kMaxNTiles];
-  long long nt_boff[kMaxNTiles];
-  int lbo_a, lbo_b;
+  long long nt_bsrc[kMaxNTiles];  // device address of the N-tile's packed B
+  long long row_bytes;            // bytes of one folded output row = r*Cout*out_elem
   unsigned idesc;
   unsigned acc_stride, tmem_cols;
   int epi_flags;
-  int off_stg, off_a, off_b, off_table, off_bias, stg_bytes;
+  int off_stg, off_a, off_b, off_bias;
+  // schedule: x = (a_off>>4) | (lbo_a>>4)<<16, y = (b_off>>4) | (lbo_b>>4)<<16,
+  // z = accumulate flag (bit 31), w = accumulator column
+  uint4 table[kMaxTable];
 };
 
 struct TmaMaps {
   CUtensorMap in[kMaxResidues];
-  CUtensorMap out;
 };
 
 template <typename OutT>
@@ -73,7 +76,7 @@ __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
 }
 
 template <int kKind, typename OutT>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     conv_fold_kernel(const __grid_constant__ ConvArgs a, const __grid_constant__ TmaMaps maps) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
@@ -87,18 +90,16 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t bar_b = base + 160;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + 192);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index via shuffle so the compiler knows it is warp-uniform (keeps the
+  // MMA issuer's operands in uniform registers)
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
   const int ntile = blockIdx.x % a.n_tiles;
   const int local = blockIdx.x / a.n_tiles;
-  const int entries = a.nt_entries[ntile];
   const int ncols = a.nt_cols[ntile];
   const int col0 = a.nt_col0[ntile];
 
-  // Schedule table and bias slice into shared memory.
-  {
-    const uint4* gtab = reinterpret_cast<const uint4*>(a.packed) + a.nt_entry0[ntile];
-    uint4* stab = reinterpret_cast<uint4*>(gbase + a.off_table);
-    for (int i = threadIdx.x; i < entries; i += blockDim.x) stab[i] = gtab[i];
+  {  // bias slice of this N-tile into shared memory
     float* sbias = reinterpret_cast<float*>(gbase + a.off_bias);
     const bool has_bias = (a.bias != nullptr) && (a.epi_flags & WF_EPI_BIAS);
     for (int i = threadIdx.x; i < ncols; i += blockDim.x) sbias[i] = has_bias ? a.bias[col0 + i] : 0.0f;
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_tfull + 8 * i, 1);
-      mbar_init(bar_tempty + 8 * i, 128);
+      mbar_init(bar_tempty + 8 * i, 256);
     }
     mbar_init(bar_b, 1);
     fence_barrier_init();
@@ -118,7 +119,6 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     for (int b = 0; b < a.s; ++b)
       if ((a.res_mask >> b) & 1u) prefetch_tmap(&maps.in[b]);
-    prefetch_tmap(&maps.out);
   }
   if (warp == 1) tmem_alloc(smem_u32(tmem_slot), a.tmem_cols);
   tc_fence_before();
@@ -127,9 +127,9 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      const uint8_t* gb = a.packed + a.table_bytes + a.nt_boff[ntile];
+    // ===================== TMA producer (one elected lane) =====================
+    if (elect_one()) {
+      const uint8_t* gb = reinterpret_cast<const uint8_t*>(a.nt_bsrc[ntile]);
       const int bb = a.nt_bbytes[ntile];
       mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
       for (int off = 0; off < bb; off += 32768)
@@ -153,45 +153,67 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
-      const uint4* stab = reinterpret_cast<const uint4*>(gbase + a.off_table);
-      const uint32_t b_base = base + a.off_b;
-      mbar_wait(bar_b, 0);
-      int it = 0;
-      for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it) {
-        const int stage = it % a.stages;
-        const uint32_t round = static_cast<uint32_t>(it / a.stages);
-        const int acc = it & 1;
-        const uint32_t acc_round = static_cast<uint32_t>(it >> 1);
-        mbar_wait(bar_tempty + 8 * acc, (acc_round & 1u) ^ 1u);
-        mbar_wait(bar_full + 8 * stage, round & 1u);
-        tc_fence_after();
-        const uint32_t a_base = base + a.off_a + stage * a.stage_bytes;
-        const uint32_t d_base = tmem_base + acc * a.acc_stride;
-        for (int i = 0; i < entries; ++i) {
-          const uint4 e = stab[i];
-          mma<kKind>(d_base + e.w, smem_desc(a_base + e.x, a.lbo_a, 128), smem_desc(b_base + e.y, a.lbo_b, 128),
-                     a.idesc, e.z >> 31);
+    // The whole warp walks the (warp-uniform) schedule so descriptors live in
+    // uniform registers straight from the constant bank; one lane issues.
+    const int e0 = a.nt_entry0[ntile];
+    const int entries = a.nt_entries[ntile];
+    const bool skip_mma = (a.epi_flags & 0x100) != 0;  // profiling switch
+    const uint32_t b_lo = (base + a.off_b) >> 4;
+    const bool leader = elect_one();
+    mbar_wait(bar_b, 0);
+    int it = 0;
+    for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it) {
+      const int stage = it % a.stages;
+      const uint32_t round = static_cast<uint32_t>(it / a.stages);
+      const int acc = it & 1;
+      const uint32_t acc_round = static_cast<uint32_t>(it >> 1);
+      mbar_wait(bar_tempty + 8 * acc, (acc_round & 1u) ^ 1u);
+      mbar_wait(bar_full + 8 * stage, round & 1u);
+      tc_fence_after();
+      const uint32_t a_lo = (base + a.off_a + stage * a.stage_bytes) >> 4;
+      const uint32_t d_base = tmem_base + acc * a.acc_stride;
+      if (!skip_mma) {
+        int i = 0;
+        for (; i + 8 <= entries; i += 8) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 e = a.table[e0 + i + j];
+            const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
+            const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
+            if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, a.idesc, e.z >> 31);
+          }
         }
+        for (; i < entries; ++i) {
+          const uint4 e = a.table[e0 + i];
+          const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
+          const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
+          if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, a.idesc, e.z >> 31);
+        }
+      }
+      if (leader) {
         mma_commit(bar_empty + 8 * stage);
         mma_commit(bar_tfull + 8 * acc);
       }
+      __syncwarp();
     }
-    __syncwarp();
   } else {
-    // ===================== epilogue (warps 2..5) =====================
-    constexpr int CC = 64 / static_cast<int>(sizeof(OutT));  // columns per 64-byte staging row
-    const int quarter = warp & 3;                              // TMEM lanes [32q, 32q+32)
+    // ===================== epilogue (warps 2..9) =====================
+    // Warp w owns TMEM lanes [32q, 32q+32), q = w % 4 -- M rows m = 32q + lane,
+    // one output row segment per thread -- and every other 64-byte column chunk
+    // (half = 0 for warps 2..5, 1 for warps 6..9). Per chunk: tcgen05.ld ->
+    // +bias -> ReLU -> convert -> two 256-bit stores (full 32-byte sectors)
+    // straight to the final NHWC row; no shared-memory staging.
+    constexpr int CC = 64 / static_cast<int>(sizeof(OutT));  // columns per chunk
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int nchunks = ncols / CC;
+    const bool relu = (a.epi_flags & WF_EPI_RELU) != 0;
+    const bool dbg_skip_epi = (a.epi_flags & 0x200) != 0;
+    const bool dbg_skip_store = (a.epi_flags & 0x400) != 0;
+    const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
     const int m = quarter * 32 + lane;
     const int t = m / a.Wbox;
     const int wq = m - t * a.Wbox;
-    const bool valid = (t < a.OHt) && (wq < a.Wfo);
-    const uint32_t srow = static_cast<uint32_t>(t * a.Wfo + wq);
-    const int nchunks = ncols / CC;
-    const bool leader = (threadIdx.x == 64);
-    const bool relu = (a.epi_flags & WF_EPI_RELU) != 0;
-    const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
-    uint32_t stg_i = 0;
     int it = 0;
     for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it) {
       const int acc = it & 1;
@@ -200,65 +222,57 @@ __global__ void __launch_bounds__(192, 1)
       const int oh0 = (mt - n * a.ohb) * a.OHt;
       mbar_wait(bar_tfull + 8 * acc, acc_round & 1u);
       tc_fence_after();
+      if (dbg_skip_epi || half >= nchunks) {
+        tc_fence_before();
+        mbar_arrive(bar_tempty + 8 * acc);
+        continue;
+      }
+      const int oh = oh0 + t;
+      const bool valid = (wq < a.Wfo) && (t < a.OHt) && (oh < a.OH) && !dbg_skip_store;
+      uint8_t* grow = a.out + ((static_cast<long long>(n) * a.OH + oh) * a.Wfo + wq) * a.row_bytes +
+                      static_cast<long long>(col0) * sizeof(OutT);
       const uint32_t trow = tmem_base + acc * a.acc_stride + (static_cast<uint32_t>(quarter * 32) << 16);
-      for (int ch = 0; ch < nchunks; ++ch) {
-        float v[CC];
-        if constexpr (CC == 32) {
-          uint32_t r[32];
-          tmem_ld32(trow + ch * CC, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
-        } else {
-          uint32_t r[16];
-          tmem_ld16(trow + ch * CC, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
-        }
-        if (ch == nchunks - 1) {
-          tc_fence_before();
-          mbar_arrive(bar_tempty + 8 * acc);
-        }
-#pragma unroll
-        for (int k = 0; k < CC; ++k) {
-          float x = v[k] + sbias[ch * CC + k];
-          if (relu) x = (x < 0.0f) ? 0.0f : x;
-          v[k] = x;
-        }
-        const uint32_t buf = base + a.off_stg + (stg_i & 1u) * a.stg_bytes;
-        named_bar_sync(1, 128);
-        if (valid) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t lin = srow * 64u + q * 16u;
-            const uint32_t swz = lin ^ (((lin >> 7) & 3u) << 4);
-            uint32_t w0, w1, w2, w3;
-            if constexpr (sizeof(OutT) == 4) {
-              w0 = __float_as_uint(v[q * 4 + 0]);
-              w1 = __float_as_uint(v[q * 4 + 1]);
-              w2 = __float_as_uint(v[q * 4 + 2]);
-              w3 = __float_as_uint(v[q * 4 + 3]);
-            } else {
-              w0 = pack2<OutT>(v[q * 8 + 0], v[q * 8 + 1]);
-              w1 = pack2<OutT>(v[q * 8 + 2], v[q * 8 + 3]);
-              w2 = pack2<OutT>(v[q * 8 + 4], v[q * 8 + 5]);
-              w3 = pack2<OutT>(v[q * 8 + 6], v[q * 8 + 7]);
-            }
-            st_shared_v4(buf + swz, w0, w1, w2, w3);
+      uint32_t r[2][CC];
+      if constexpr (CC == 32) tmem_ld32(trow + half * CC, r[0]); else tmem_ld16(trow + half * CC, r[0]);
+      tmem_ld_wait();
+      reg_fence<CC>(r[0]);
+      int cur = 0;
+#pragma unroll 1
+      for (int ch = half; ch < nchunks; ch += 2) {
+        const int nxt = ch + 2;
+        if (nxt < nchunks) {  // prefetch this warp's next chunk
+          if (cur == 0) {
+            if constexpr (CC == 32) tmem_ld32(trow + nxt * CC, r[1]); else tmem_ld16(trow + nxt * CC, r[1]);
+          } else {
+            if constexpr (CC == 32) tmem_ld32(trow + nxt * CC, r[0]); else tmem_ld16(trow + nxt * CC, r[0]);
           }
         }
-        fence_proxy_async_smem();
-        named_bar_sync(1, 128);
-        if (leader) {
-          tma_store_4d(&maps.out, buf, col0 + ch * CC, 0, oh0, n);
-          bulk_commit();
-          bulk_wait_read_1();
+        uint32_t pk[16];
+#pragma unroll
+        for (int k = 0; k < CC; k += (sizeof(OutT) == 4 ? 1 : 2)) {
+          float x0 = __uint_as_float(cur == 0 ? r[0][k] : r[1][k]) + sbias[ch * CC + k];
+          if (relu) x0 = (x0 < 0.0f) ? 0.0f : x0;
+          if constexpr (sizeof(OutT) == 4) {
+            pk[k] = __float_as_uint(x0);
+          } else {
+            float x1 = __uint_as_float(cur == 0 ? r[0][k + 1] : r[1][k + 1]) + sbias[ch * CC + k + 1];
+            if (relu) x1 = (x1 < 0.0f) ? 0.0f : x1;
+            pk[k / 2] = pack2<OutT>(x0, x1);
+          }
         }
-        ++stg_i;
+        if (valid) {
+          st_global_v8(grow + ch * 64, pk);
+          st_global_v8(grow + ch * 64 + 32, pk + 8);
+        }
+        tmem_ld_wait();
+        if (nxt < nchunks) {
+          if (cur == 0) reg_fence<CC>(r[1]); else reg_fence<CC>(r[0]);
+        }
+        cur ^= 1;
       }
+      tc_fence_before();
+      mbar_arrive(bar_tempty + 8 * acc);
     }
-    if (leader) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -314,7 +328,7 @@ cudaError_t launch_typed(const ConvArgs& args, const TmaMaps& maps, int grid, in
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  kern<<<grid, 192, smem, st>>>(args, maps);
+  kern<<<grid, 320, smem, st>>>(args, maps);
   return cudaGetLastError();
 }
 
@@ -333,8 +347,9 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     *err = "bias epilogue requested without a replicated bias";
     return WF_INVALID_ARGUMENT;
   }
-  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(packed)) & 15u) {
-    *err = "x, y and the packed filter must be 16-byte aligned";
+  if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(packed)) & 15u) ||
+      (reinterpret_cast<uintptr_t>(y) & 31u)) {
+    *err = "x and the packed filter must be 16-byte aligned, y 32-byte aligned";
     return WF_INVALID_ARGUMENT;
   }
   const int oes = elem_bytes(out_dtype);
@@ -347,13 +362,18 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   EncodeTiledFn encode = get_encode(err);
   if (!encode) return WF_CUDA_ERROR;
 
-  ConvArgs a{};
+  if (S.entries.size() > static_cast<size_t>(kMaxTable)) {
+    *err = "schedule too long for the constant bank";
+    return WF_UNSUPPORTED;
+  }
+  ConvArgs a;
+  std::memset(&a, 0, sizeof(a));
   TmaMaps maps;
   std::memset(&maps, 0, sizeof(maps));
-  a.packed = static_cast<const uint8_t*>(packed);
   a.bias = b_rep;
-  a.table_bytes = p.table_bytes;
+  a.out = static_cast<uint8_t*>(y);
   a.OHt = static_cast<int>(p.tile_rows);
+  a.OH = static_cast<int>(p.oh);
   a.Wbox = static_cast<int>(p.wbox);
   a.Wfo = static_cast<int>(p.wfo);
   a.c0 = static_cast<int>(p.c0);
@@ -372,6 +392,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   a.stage_bytes = S.stage_bytes;
   a.n_tiles = static_cast<int>(S.ntiles.size());
   uint32_t max_cols = 0;
+  const uint8_t* packed_b = static_cast<const uint8_t*>(packed) + p.table_bytes;
   for (int i = 0; i < a.n_tiles; ++i) {
     const NTile& t = S.ntiles[i];
     a.nt_entry0[i] = t.entry0;
@@ -379,8 +400,16 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     a.nt_col0[i] = t.col0;
     a.nt_cols[i] = t.cols;
     a.nt_bbytes[i] = static_cast<int>(t.b_bytes);
-    a.nt_boff[i] = t.b_off;
+    a.nt_bsrc[i] = reinterpret_cast<long long>(packed_b + t.b_off);
     max_cols = std::max<uint32_t>(max_cols, static_cast<uint32_t>(t.cols));
+  }
+  const uint32_t lbo_b = static_cast<uint32_t>(S.Ng) * 16u;
+  for (size_t i = 0; i < S.entries.size(); ++i) {
+    const MmaEntry& e = S.entries[i];
+    a.table[i].x = (e.a_off >> 4) | ((static_cast<uint32_t>(S.lbo_a) >> 4) << 16);
+    a.table[i].y = (e.b_off >> 4) | ((lbo_b >> 4) << 16);
+    a.table[i].z = e.meta;
+    a.table[i].w = e.tmem_col;
   }
   if (num_sms <= 0) {
     int dev = 0;
@@ -388,8 +417,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   a.ctas_per_ntile = std::max(1, std::min<int>(num_sms / a.n_tiles, a.num_mtiles));
-  a.lbo_a = S.lbo_a;
-  a.lbo_b = S.Ng * 16;
+  a.row_bytes = p.cout_f * oes;
   const uint32_t fmt = (in_t == WF_BF16) ? 1u : (in_t == WF_F16 ? 0u : 2u);
   a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((static_cast<uint32_t>(S.Ng) >> 3) << 17) |
             ((static_cast<uint32_t>(kTileM) >> 4) << 24);
@@ -397,20 +425,18 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   a.tmem_cols = 2 * a.acc_stride;
   a.epi_flags = static_cast<int>(epilogue);
   // shared-memory carve-up (offsets from the 1024-aligned base)
-  a.stg_bytes = kStagingBytes / 2;  // 128 rows x 64 B
-  a.off_stg = 1024;
-  a.off_a = a.off_stg + 2 * a.stg_bytes;
+  a.off_stg = 1024;                      // 8 epilogue warps x 2 KB staging
+  a.off_a = a.off_stg + kStagingBytes;
   a.off_b = a.off_a + a.stages * a.stage_bytes + kTileM * 16;
   a.off_b = (a.off_b + 127) / 128 * 128;
-  a.off_table = a.off_b + S.b_smem_bytes;
-  a.off_bias = a.off_table + (S.table_smem_bytes + 127) / 128 * 128;
+  a.off_bias = a.off_b + S.b_smem_bytes;
   const int smem = a.off_bias + kMaxAccCols * 4 + 1024;
   if (smem > kSmemLimit) {
     *err = "shared-memory budget exceeded";
     return WF_UNSUPPORTED;
   }
 
-  // ---- tensor maps --------------------------------------------------------------
+  // ---- input tensor maps (one 5-D view per H-stride residue) --------------------
   const int es = S.esize;
   const cuuint64_t rowpitch = static_cast<cuuint64_t>(d.w) * d.c * es;
   const cuuint64_t pix = static_cast<cuuint64_t>(p.f) * d.c * es;
@@ -429,23 +455,6 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       *err = "cuTensorMapEncodeTiled(input) failed: " + std::to_string(static_cast<int>(r));
-      return WF_CUDA_ERROR;
-    }
-  }
-  {
-    const cuuint64_t cf = static_cast<cuuint64_t>(p.cout_f);
-    cuuint64_t gdim[4] = {cf, static_cast<cuuint64_t>(p.wfo), static_cast<cuuint64_t>(p.oh),
-                          static_cast<cuuint64_t>(d.n)};
-    cuuint64_t gstr[3] = {cf * oes, static_cast<cuuint64_t>(p.ow) * d.cout * oes,
-                          static_cast<cuuint64_t>(p.oh) * p.ow * d.cout * oes};
-    cuuint32_t box[4] = {static_cast<cuuint32_t>(CC), static_cast<cuuint32_t>(p.wfo),
-                         static_cast<cuuint32_t>(p.tile_rows), 1};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = encode(&maps.out, tmap_type(out_dtype), 4, y, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      *err = "cuTensorMapEncodeTiled(output) failed: " + std::to_string(static_cast<int>(r));
       return WF_CUDA_ERROR;
     }
   }

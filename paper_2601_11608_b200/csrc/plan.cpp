@@ -123,9 +123,14 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   const int64_t Wf = d.w / f, Wfo = OW / r;
   const int64_t U = f * d.c * S.esize / 32;
   S.U = static_cast<int>(U);
-  const int64_t Wbox = Wfo + kwf - 1;
+  // Folded columns per output row in the A layout: >= Wfo + KW' - 1 and a
+  // divisor or multiple of 32, so each epilogue warp (32 TMEM lanes) owns whole
+  // output rows (Wbox <= 32) or a 32-column slice of one (Wbox >= 32).
+  int64_t Wbox = 1;
+  while (Wbox < Wfo + kwf - 1) Wbox *= 2;
   if (Wbox > kTileM || U * 2 > 256) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
-  int64_t OHt = std::min<int64_t>(kTileM / Wbox, OH);
+  // Never shrunk to OH: rows past OH are zero-filled on load and clipped on store.
+  const int64_t OHt = kTileM / Wbox;
 
   // ---- residues of the H stride -----------------------------------------
   if (sh > kMaxResidues) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
@@ -179,7 +184,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
 
   // ---- N-tiles and shared-memory budget ------------------------------------
   const int ctrl_bytes = 1024;
-  const int staging = kStagingBytes;   // two 8 KB epilogue buffers
+  const int staging = kStagingBytes;   // 4 epilogue warps x 2 x 2 KB
   const int a_pad = kTileM * 16;
   const int bias_bytes = kMaxAccCols * 4;
   int64_t b_budget = 128 * 1024;
@@ -216,8 +221,8 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
       max_entries = std::max(max_entries, e);
     }
     const int64_t table_b = max_entries * 16;
-    const int64_t fixed = ctrl_bytes + staging + a_pad + 128 + (max_b + 127) / 128 * 128 +
-                          (table_b + 127) / 128 * 128 + bias_bytes + 1024;
+    (void)table_b;  // the schedule lives in the kernel's constant bank
+    const int64_t fixed = ctrl_bytes + staging + a_pad + 128 + (max_b + 127) / 128 * 128 + bias_bytes + 1024;
     int stages = 0;
     for (int st2 = 4; st2 >= 2; --st2)
       if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { stages = st2; break; }
@@ -247,8 +252,15 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
       const int64_t delta = kh - d.pad_h;
       const int b = static_cast<int>(pos_mod(delta, sh));
       const int a = static_cast<int>((delta - b) / sh);
+      // Interleave groups: consecutive MMAs accumulate into different TMEM
+      // columns, so they pipeline instead of serialising on one accumulator.
+      int64_t steps = 0;
+      for (int gg = t.g0; gg < t.g1; ++gg) steps = std::max<int64_t>(steps, hi[gg] - lo[gg] + 1);
+      for (int64_t step = 0; step < steps; ++step)
       for (int gg = t.g0; gg < t.g1; ++gg) {
-        for (int64_t u = lo[gg]; u <= hi[gg]; ++u) {
+        if (step > hi[gg] - lo[gg]) continue;
+        {
+          const int64_t u = lo[gg] + step;
           const int64_t kp = u / U, uq = u % U;
           MmaEntry e{};
           e.a_off = static_cast<uint32_t>(b * S.region_bytes +

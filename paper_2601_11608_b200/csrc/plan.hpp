@@ -43,7 +43,7 @@ constexpr int kMaxAccCols = 256;      // accumulator columns per N-tile (x2 buff
 constexpr int kMaxResidues = 8;
 constexpr int kMaxNTiles = 16;
 constexpr int kSmemLimit = 227 * 1024;
-constexpr int kStagingBytes = 16 * 1024;  // one epilogue staging buffer
+constexpr int kStagingBytes = 0;  // epilogue writes straight from registers (no staging)
 
 struct MmaEntry {          // 16 bytes, lives in the packed buffer and in smem
   uint32_t a_off;          // byte offset of the A view inside an A stage

@@ -71,6 +71,33 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b32 r;\n"
+      "elect.sync r|p, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void st_global_v4(void* ptr, uint4 v) {
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+// 256-bit global store (sm_100+: STG.E.ENL2.256): one full 32-byte sector.
+__device__ __forceinline__ void st_global_v8(void* ptr, const uint32_t* v) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(ptr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
 // ---- named barriers ----------------------------------------------------------
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -120,6 +147,31 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t adesc, uint64_t bd
         : "memory");
   }
 }
+// Same MMA with an A-collector hint: 1 = fill (keep A for the next MMA),
+// 2 = use (reuse the kept A and keep it), 3 = lastuse (reuse, then drop).
+// Consecutive MMAs that share an A view then read it from shared memory once.
+template <int kKind>
+__device__ __forceinline__ void mma_coll(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate, uint32_t coll) {
+#define WFB_MMA_COLL(KIND, COLL)                                                                  \
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"                                      \
+               "tcgen05.mma.cta_group::1.kind::" KIND COLL " [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d), \
+               "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)                                 \
+               : "memory")
+  if constexpr (kKind == 0) {
+    if (coll == 1) WFB_MMA_COLL("f16", ".collector::a::fill");
+    else if (coll == 2) WFB_MMA_COLL("f16", ".collector::a::use");
+    else if (coll == 3) WFB_MMA_COLL("f16", ".collector::a::lastuse");
+    else WFB_MMA_COLL("f16", "");
+  } else {
+    if (coll == 1) WFB_MMA_COLL("tf32", ".collector::a::fill");
+    else if (coll == 2) WFB_MMA_COLL("tf32", ".collector::a::use");
+    else if (coll == 3) WFB_MMA_COLL("tf32", ".collector::a::lastuse");
+    else WFB_MMA_COLL("tf32", "");
+  }
+#undef WFB_MMA_COLL
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -148,6 +200,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Ties registers written by an asynchronous tcgen05.ld to a point after the
+// matching wait::ld, so the compiler cannot hoist their consumers above it.
+template <int N>
+__device__ __forceinline__ void reg_fence(uint32_t (&r)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i])::"memory");
+}
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)

@@ -83,8 +83,13 @@ def prepare_filter(w: torch.Tensor, b: torch.Tensor | None, x_shape, stride=(1, 
 
 
 def conv_folded(x: torch.Tensor, ff: FoldedFilter, *, relu: bool = False, bias: bool = True,
-                out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None) -> torch.Tensor:
-    """y = ReLU?(conv(x, w) + b) through the folded tcgen05 kernel (NHWC in, NHWC out)."""
+                out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
+                _profile_flags: int = 0) -> torch.Tensor:
+    """y = ReLU?(conv(x, w) + b) through the folded tcgen05 kernel (NHWC in, NHWC out).
+
+    ``_profile_flags`` (0x100 skip MMAs, 0x200 skip epilogue, 0x400 skip stores) exist
+    only to decompose the kernel's time in profiling runs; results are garbage with them.
+    """
     _require_cuda(x)
     if x.dtype != ff.in_dtype:
         raise ValueError(f"x dtype {x.dtype} != packed filter dtype {ff.in_dtype}")
@@ -103,6 +108,7 @@ def conv_folded(x: torch.Tensor, ff: FoldedFilter, *, relu: bool = False, bias: 
         epi |= A.WF_EPI_BIAS
     if relu:
         epi |= A.WF_EPI_RELU
+    epi |= _profile_flags & 0x700
     A.check(A.lib().wf_conv_fold_fwd(_ptr(x), _ptr(ff.packed), _ptr(ff.bias_rep) if epi & A.WF_EPI_BIAS else None,
                                      _ptr(out), d, ff.plan, _OUT_TO_WF[out_dtype], epi, _stream_ptr(x.device)))
     return out

@@ -1,0 +1,36 @@
+"""Summarise an ncu report: key throughput metrics + top SASS stall sites (dev aid)."""
+import csv, subprocess, sys, io
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return dict(zip(rows[0], rows[2])), dict(zip(rows[0], rows[1]))
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
+        "l1tex__data_pipe_tc_wavefronts_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_uniform.sum", "smsp__inst_executed.sum", "sm__cycles_elapsed.avg",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum",
+        "lts__t_sectors_srcunit_tex_op_write.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
+
+def main(rep, top=20):
+    v, u = raw(rep)
+    for k in KEYS:
+        if k in v:
+            print(f"{k:80s} {v[k]:>16s} {u.get(k,'')}")
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[1]; data = rows[2:]
+    iS = hdr.index("Warp Stall Sampling (All Samples)")
+    cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+    tot = sum(float(r[iS] or 0) for r in data) or 1
+    print("top stall sites (% of samples):")
+    for r in sorted(data, key=lambda r: -float(r[iS] or 0))[:top]:
+        st = sorted(((float(r[i] or 0), hdr[i][6:]) for i in cols), reverse=True)[:2]
+        print(f"{float(r[iS])/tot*100:5.1f}% {r[0][-5:]} {r[1].strip()[:64]:64s} {[(int(a), b) for a, b in st]}")
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 20)
