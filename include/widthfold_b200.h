@@ -144,6 +144,25 @@ wf_status wf_conv_fold_fwd(const void* x, const void* w_packed,
                            const wf_conv_desc* desc, const wf_fold_plan* plan,
                            wf_dtype out_dtype, uint32_t epilogue, void* stream);
 
+/* Exact-order fp32 direct convolution on CUDA cores: widthfold::conv2d
+ * (src/refconv.cpp:34-80) bit-for-bit (kh -> kw -> ci, no FMA) plus explicit
+ * zero padding. The reference-semantics path for shapes/precisions the folded
+ * tcgen05 kernel does not cover, and the engine of grouped_conv. */
+wf_status wf_conv_direct_fwd(const float* x, const float* w, float* y, const wf_conv_desc* desc, void* stream);
+
+/* out = ReLU?(y + b[i % c]) -- widthfold::bias_add (src/refconv.cpp:82-95). */
+wf_status wf_bias_add(const float* y, const float* b, float* out, int64_t n, int64_t c, int32_t relu, void* stream);
+
+/* out[j*cout + co] = b[co], j < r -- widthfold::replicate_bias (src/fold.cpp:213-226). */
+wf_status wf_replicate_bias(const float* b, int64_t cout, int64_t r, float* out, void* stream);
+
+/* Strict-zero block-diagonal check of a dense (kh,kw,cif,cof) fp32 filter for
+ * `groups` blocks (src/blockdiag.cpp:24-84). scratch: 8 bytes of device
+ * memory. *first_bad = flat index of the first offending entry or -1.
+ * Synchronizes `stream`. Returns WF_NOT_BLOCK_DIAGONAL when one is found. */
+wf_status wf_check_block_diagonal(const float* w_dense, int64_t kh, int64_t kw, int64_t cif, int64_t cof,
+                                  int64_t groups, void* scratch, int64_t* first_bad, void* stream);
+
 /* Number of SMs the conv kernel assumes (persistent grid); 0 = device value. */
 void wf_set_num_sms(int num_sms);
 

@@ -86,4 +86,51 @@ wf_status wf_conv_fold_fwd(const void* x, const void* w_packed, const float* b_r
   return WF_OK;
 }
 
+wf_status wf_conv_direct_fwd(const float* x, const float* w, float* y, const wf_conv_desc* desc, void* stream) {
+  if (!x || !w || !y || !desc) return fail(WF_INVALID_ARGUMENT, "null argument");
+  std::string err;
+  wf_status st = wfb::validate_desc(*desc, &err);
+  if (st != WF_OK) return fail(st, err);
+  st = wfb::launch_conv_direct(*desc, x, w, y, static_cast<cudaStream_t>(stream), &err);
+  if (st != WF_OK) return fail(st, err);
+  return WF_OK;
+}
+
+wf_status wf_bias_add(const float* y, const float* b, float* out, int64_t n, int64_t c, int32_t relu, void* stream) {
+  if (!y || !b || !out) return fail(WF_INVALID_ARGUMENT, "null argument");
+  if (c < 1 || n < 0 || n % c != 0) return fail(WF_SHAPE_MISMATCH, "bias length does not divide the output");
+  std::string err;
+  wf_status st = wfb::launch_bias_add(y, b, out, n, static_cast<int>(c), relu, static_cast<cudaStream_t>(stream), &err);
+  if (st != WF_OK) return fail(st, err);
+  return WF_OK;
+}
+
+wf_status wf_replicate_bias(const float* b, int64_t cout, int64_t r, float* out, void* stream) {
+  if (!b || !out) return fail(WF_INVALID_ARGUMENT, "null argument");
+  if (r < 1) return fail(WF_INVALID_ARGUMENT, "fold factor must be >= 1");
+  if (cout < 1) return fail(WF_SHAPE_MISMATCH, "bias must be non-empty");
+  std::string err;
+  wf_status st = wfb::launch_replicate_bias(b, static_cast<int>(cout), static_cast<int>(r), out,
+                                            static_cast<cudaStream_t>(stream), &err);
+  if (st != WF_OK) return fail(st, err);
+  return WF_OK;
+}
+
+wf_status wf_check_block_diagonal(const float* w_dense, int64_t kh, int64_t kw, int64_t cif, int64_t cof,
+                                  int64_t groups, void* scratch, int64_t* first_bad, void* stream) {
+  if (!w_dense || !scratch || !first_bad) return fail(WF_INVALID_ARGUMENT, "null argument");
+  if (groups < 1 || cif % groups != 0 || cof % groups != 0)
+    return fail(WF_SHAPE_MISMATCH, "channel extents not divisible into the requested blocks");
+  std::string err;
+  long long bad = -1;
+  wf_status st = wfb::launch_blockdiag_check(w_dense, static_cast<int>(kh), static_cast<int>(kw),
+                                             static_cast<int>(cif), static_cast<int>(cof), static_cast<int>(groups),
+                                             static_cast<unsigned long long*>(scratch), &bad,
+                                             static_cast<cudaStream_t>(stream), &err);
+  if (st != WF_OK) return fail(st, err);
+  *first_bad = bad;
+  if (bad >= 0) return fail(WF_NOT_BLOCK_DIAGONAL, "off-diagonal entry at flat index " + std::to_string(bad) + " is nonzero");
+  return WF_OK;
+}
+
 }  // extern "C"

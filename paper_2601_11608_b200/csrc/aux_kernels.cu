@@ -1,0 +1,123 @@
+// aux_kernels.cu -- the non-hot-path device operations behind the reference API.
+//
+//   conv_direct_kernel   widthfold::conv2d (src/refconv.cpp:34-80) bit-for-bit:
+//                        fp32, per output element kh -> kw -> ci, separately
+//                        rounded multiply and add (no FMA), accumulator +0.0f,
+//                        plus explicit zero padding. Used for the reference's
+//                        exact-fp32 semantics (precision="exact") and for
+//                        grouped_conv (src/blockdiag.cpp:138-187), which the
+//                        reference guarantees bitwise equal to the dense conv.
+//   bias_add_kernel      widthfold::bias_add (src/refconv.cpp:82-95) (+ReLU).
+//   blockdiag_check      BlockDiagFilter::from_expanded's strict-zero check
+//                        (src/blockdiag.cpp:24-84): any off-diagonal entry that
+//                        is not +-0.0f is an error.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "kernels.hpp"
+
+namespace wfb {
+
+__global__ void conv_direct_kernel(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y,
+                                   int B, int H, int W, int C, int KH, int KW, int Co, int sh, int sw, int ph,
+                                   int pw, int OH, int OW) {
+  const long long total = (long long)B * OH * OW * Co;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long t = idx;
+    const int oc = static_cast<int>(t % Co); t /= Co;
+    const int ow = static_cast<int>(t % OW); t /= OW;
+    const int oh = static_cast<int>(t % OH); t /= OH;
+    const int b = static_cast<int>(t);
+    float acc = 0.0f;
+    for (int kh = 0; kh < KH; ++kh) {
+      const int ih = oh * sh - ph + kh;
+      for (int kw = 0; kw < KW; ++kw) {
+        const int iw = ow * sw - pw + kw;
+        const bool in = (ih >= 0 && ih < H && iw >= 0 && iw < W);
+        const float* xr = x + (((long long)b * H + (in ? ih : 0)) * W + (in ? iw : 0)) * C;
+        const float* wr = w + ((long long)(kh * KW + kw) * C) * Co + oc;
+        for (int ci = 0; ci < C; ++ci) {
+          const float xv = in ? xr[ci] : 0.0f;
+          acc = __fadd_rn(acc, __fmul_rn(xv, wr[(long long)ci * Co]));
+        }
+      }
+    }
+    y[idx] = acc;
+  }
+}
+
+__global__ void bias_add_kernel(const float* __restrict__ y, const float* __restrict__ b, float* __restrict__ out,
+                                long long n, int C, int relu) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float v = __fadd_rn(y[i], b[i % C]);
+    if (relu && v < 0.0f) v = 0.0f;
+    out[i] = v;
+  }
+}
+
+__global__ void blockdiag_check_kernel(const float* __restrict__ wd, int KH, int KW, int Cif, int Cof, int groups,
+                                       unsigned long long* __restrict__ first_bad) {
+  const long long total = (long long)KH * KW * Cif * Cof;
+  const int Cib = Cif / groups, Cob = Cof / groups;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int co = static_cast<int>(i % Cof);
+    const int ci = static_cast<int>((i / Cof) % Cif);
+    if (co / Cob != ci / Cib && wd[i] != 0.0f) atomicMin(first_bad, static_cast<unsigned long long>(i));
+  }
+}
+
+static int grid_for(long long total) {
+  const long long g = (total + 255) / 256;
+  return static_cast<int>(g < 1 ? 1 : (g > 65535 ? 65535 : g));
+}
+
+wf_status launch_conv_direct(const wf_conv_desc& d, const float* x, const float* w, float* y, cudaStream_t st,
+                             std::string* err) {
+  const int64_t OH = (d.h + 2 * d.pad_h - d.kh) / d.stride_h + 1;
+  const int64_t OW = (d.w + 2 * d.pad_w - d.kw) / d.stride_w + 1;
+  const long long total = (long long)d.n * OH * OW * d.cout;
+  conv_direct_kernel<<<grid_for(total), 256, 0, st>>>(x, w, y, (int)d.n, (int)d.h, (int)d.w, (int)d.c, (int)d.kh,
+                                                      (int)d.kw, (int)d.cout, (int)d.stride_h, (int)d.stride_w,
+                                                      (int)d.pad_h, (int)d.pad_w, (int)OH, (int)OW);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("conv_direct_kernel: ") + cudaGetErrorString(e);
+    return WF_CUDA_ERROR;
+  }
+  return WF_OK;
+}
+
+wf_status launch_bias_add(const float* y, const float* b, float* out, long long n, int C, int relu, cudaStream_t st,
+                          std::string* err) {
+  bias_add_kernel<<<grid_for(n), 256, 0, st>>>(y, b, out, n, C, relu);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("bias_add_kernel: ") + cudaGetErrorString(e);
+    return WF_CUDA_ERROR;
+  }
+  return WF_OK;
+}
+
+wf_status launch_blockdiag_check(const float* wd, int KH, int KW, int Cif, int Cof, int groups,
+                                 unsigned long long* scratch, long long* first_bad, cudaStream_t st, std::string* err) {
+  const unsigned long long init = ~0ull;
+  cudaError_t e = cudaMemcpyAsync(scratch, &init, sizeof(init), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    const long long total = (long long)KH * KW * Cif * Cof;
+    blockdiag_check_kernel<<<grid_for(total), 256, 0, st>>>(wd, KH, KW, Cif, Cof, groups, scratch);
+    e = cudaGetLastError();
+  }
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, scratch, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    *err = std::string("blockdiag check: ") + cudaGetErrorString(e);
+    return WF_CUDA_ERROR;
+  }
+  *first_bad = (h == ~0ull) ? -1 : static_cast<long long>(h);
+  return WF_OK;
+}
+
+}  // namespace wfb

@@ -1,0 +1,212 @@
+// bindings.cpp -- pybind11 module `paper_2601_11608_b200._core`.
+//
+// Mirrors the reference binding (/root/reference/proj/python/bindings.cpp:48-207):
+// same function names, keyword arguments, plan_dict keys and exception types
+// (ShapeMismatchError / IllegalFoldError / DegenerateOutputError are ValueError
+// subclasses, bindings.cpp:51-56). Device data crosses as integer pointers plus
+// shapes and a cudaStream_t; the Python layer (api.py) maps torch/numpy onto it.
+// The GIL is released around every device call.
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cstdint>
+
+#include "widthfold.hpp"
+
+namespace py = pybind11;
+namespace wf = widthfold;
+
+namespace {
+
+void* P(std::uintptr_t v) { return reinterpret_cast<void*>(v); }
+const float* F(std::uintptr_t v) { return reinterpret_cast<const float*>(v); }
+
+wf::Dtype dtype_of(const std::string& s) {
+  if (s == "bf16") return wf::Dtype::BF16;
+  if (s == "f16" || s == "fp16") return wf::Dtype::F16;
+  if (s == "tf32") return wf::Dtype::TF32;
+  if (s == "f32" || s == "fp32") return wf::Dtype::F32;
+  throw std::invalid_argument("unknown dtype '" + s + "'");
+}
+
+py::dict plan_dict(const wf::FoldPlan& plan) {
+  py::dict d;
+  d["status"] = plan.ok() ? "apply" : "fallback";
+  d["reason"] = wf::to_string(plan.reason);
+  d["factor"] = plan.factor;
+  d["folded_input_shape"] = plan.folded_input_shape;
+  d["expanded_filter_shape"] = plan.expanded_filter_shape;
+  return d;
+}
+
+py::dict raw_dict(const wf_fold_plan& p) {
+  py::dict d;
+  d["f"] = p.f; d["r"] = p.r; d["c0"] = p.c0; d["kw_f"] = p.kw_f; d["k_f"] = p.k_f; d["cout_f"] = p.cout_f;
+  d["oh"] = p.oh; d["ow"] = p.ow; d["wf"] = p.wf; d["wfo"] = p.wfo; d["units_per_px"] = p.units_per_px;
+  d["group_size"] = p.group_size; d["n_groups"] = p.n_groups; d["n_tiles"] = p.n_tiles;
+  d["tile_rows"] = p.tile_rows; d["wbox"] = p.wbox; d["nrows"] = p.nrows; d["mma_entries"] = p.mma_entries;
+  d["packed_bytes"] = p.packed_bytes; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
+  return d;
+}
+
+wf::ConvSpec spec_of(const wf::Shape& in, const wf::Shape& filt, std::int64_t sh, std::int64_t sw, std::int64_t ph,
+                     std::int64_t pw) {
+  return wf::ConvSpec{in, filt, sh, sw, ph, pw};
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_core, m) {
+  m.doc() = "widthfold-b200: B200-native width folding for first-layer convolutions";
+
+  py::register_exception<wf::ShapeMismatch>(m, "ShapeMismatchError", PyExc_ValueError);
+  py::register_exception<wf::IllegalFold>(m, "IllegalFoldError", PyExc_ValueError);
+  py::register_exception<wf::DegenerateOutput>(m, "DegenerateOutputError", PyExc_ValueError);
+  py::register_exception<wf::NotBlockDiagonal>(m, "NotBlockDiagonalError", PyExc_RuntimeError);
+  py::register_exception<wf::Unsupported>(m, "UnsupportedError", PyExc_RuntimeError);
+  py::register_exception<wf::CudaError>(m, "CudaError", PyExc_RuntimeError);
+
+  m.def("abi_version", &wf_abi_version);
+
+  m.def(
+      "check_legality",
+      [](const wf::Shape& in, const wf::Shape& filt, std::int64_t factor, std::int64_t align, std::int64_t sh,
+         std::int64_t sw) { return plan_dict(wf::check_legality(spec_of(in, filt, sh, sw, 0, 0), factor, align)); },
+      py::arg("input_shape"), py::arg("filter_shape"), py::arg("factor"), py::arg("align") = 8,
+      py::arg("stride_h") = 1, py::arg("stride_w") = 1,
+      "Reference fold legality: Apply iff W % F == 0, KW == 1 and stride_w == 1.");
+
+  m.def(
+      "choose_fold_factor",
+      [](const wf::Shape& in, const wf::Shape& filt, std::int64_t align, std::int64_t sh, std::int64_t sw) {
+        return plan_dict(wf::choose_fold_factor(spec_of(in, filt, sh, sw, 0, 0), align));
+      },
+      py::arg("input_shape"), py::arg("filter_shape"), py::arg("align") = 8, py::arg("stride_h") = 1,
+      py::arg("stride_w") = 1, "Smallest factor whose folded channels meet the alignment target.");
+
+  m.def(
+      "count_macs",
+      [](const wf::Shape& in, const wf::Shape& filt, std::int64_t sh, std::int64_t sw, std::int64_t ph,
+         std::int64_t pw) { return wf::count_macs(spec_of(in, filt, sh, sw, ph, pw)); },
+      py::arg("input_shape"), py::arg("filter_shape"), py::arg("stride_h") = 1, py::arg("stride_w") = 1,
+      py::arg("pad_h") = 0, py::arg("pad_w") = 0);
+
+  m.def(
+      "mac_report",
+      [](const wf::Shape& in, const wf::Shape& filt, std::int64_t factor, std::int64_t align) {
+        const wf::ConvSpec spec = spec_of(in, filt, 1, 1, 0, 0);
+        const wf::MacReport r = wf::mac_report(spec, wf::check_legality(spec, factor, align), align);
+        py::dict d;
+        d["original"] = r.original;
+        d["dense_folded"] = r.dense_folded;
+        d["grouped_folded"] = r.grouped_folded;
+        d["zero_padded"] = r.zero_padded;
+        d["factor"] = r.factor;
+        return d;
+      },
+      py::arg("input_shape"), py::arg("filter_shape"), py::arg("factor"), py::arg("align") = 8);
+
+  m.def(
+      "plan_fold",
+      [](const wf::Shape& in, const wf::Shape& filt, std::int64_t sh, std::int64_t sw, std::int64_t ph,
+         std::int64_t pw, std::int64_t factor, std::int64_t group_size, const std::string& dtype) {
+        const wf::DevicePlan dp =
+            wf::plan_device_fold(spec_of(in, filt, sh, sw, ph, pw), factor, group_size, dtype_of(dtype));
+        py::dict d = plan_dict(dp.plan);
+        if (dp.plan.ok()) d["device"] = raw_dict(dp.raw);
+        return d;
+      },
+      py::arg("input_shape"), py::arg("filter_shape"), py::arg("stride_h") = 1, py::arg("stride_w") = 1,
+      py::arg("pad_h") = 0, py::arg("pad_w") = 0, py::arg("factor") = 0, py::arg("group_size") = 0,
+      py::arg("dtype") = "bf16", "Generalized device fold plan (KW > 1, stride, padding).");
+
+  m.def("folded_filter_shape", &wf::folded_filter_shape, py::arg("filter_shape"), py::arg("factor"),
+        py::arg("stride_w") = 1, py::arg("pad_w") = 0);
+
+  m.def(
+      "conv2d_exact",
+      [](std::uintptr_t x, std::uintptr_t w, std::uintptr_t y, const wf::Shape& in, const wf::Shape& filt,
+         std::int64_t sh, std::int64_t sw, std::int64_t ph, std::int64_t pw, std::uintptr_t stream) {
+        const wf::ConvSpec spec = spec_of(in, filt, sh, sw, ph, pw);
+        py::gil_scoped_release nogil;
+        wf::conv2d_exact(F(x), F(w), static_cast<float*>(P(y)), spec, P(stream));
+      },
+      py::arg("x"), py::arg("w"), py::arg("y"), py::arg("input_shape"), py::arg("filter_shape"),
+      py::arg("stride_h"), py::arg("stride_w"), py::arg("pad_h"), py::arg("pad_w"), py::arg("stream"));
+
+  m.def(
+      "bias_add",
+      [](std::uintptr_t y, std::uintptr_t b, std::uintptr_t out, std::int64_t n, std::int64_t c, bool relu,
+         std::uintptr_t stream) {
+        py::gil_scoped_release nogil;
+        wf::bias_add(F(y), F(b), static_cast<float*>(P(out)), n, c, relu, P(stream));
+      },
+      py::arg("y"), py::arg("b"), py::arg("out"), py::arg("n"), py::arg("c"), py::arg("relu"), py::arg("stream"));
+
+  m.def(
+      "replicate_bias",
+      [](std::uintptr_t b, std::int64_t cout, std::int64_t factor, std::uintptr_t out, std::uintptr_t stream) {
+        py::gil_scoped_release nogil;
+        wf::replicate_bias(F(b), cout, factor, static_cast<float*>(P(out)), P(stream));
+      },
+      py::arg("b"), py::arg("cout"), py::arg("factor"), py::arg("out"), py::arg("stream"));
+
+  m.def(
+      "expand_filter_general",
+      [](std::uintptr_t w, const wf::Shape& fs, std::int64_t factor, std::uintptr_t out, std::uintptr_t stream) {
+        py::gil_scoped_release nogil;
+        wf::expand_filter_general(F(w), fs, factor, static_cast<float*>(P(out)), P(stream));
+      },
+      py::arg("w"), py::arg("filter_shape"), py::arg("factor"), py::arg("out"), py::arg("stream"));
+
+  m.def(
+      "expand_filter_folded",
+      [](std::uintptr_t w, const wf::Shape& fs, std::int64_t factor, std::int64_t sw, std::int64_t pw,
+         std::uintptr_t out, std::uintptr_t stream) {
+        py::gil_scoped_release nogil;
+        wf::expand_filter_folded(F(w), fs, factor, sw, pw, static_cast<float*>(P(out)), P(stream));
+      },
+      py::arg("w"), py::arg("filter_shape"), py::arg("factor"), py::arg("stride_w"), py::arg("pad_w"),
+      py::arg("out"), py::arg("stream"));
+
+  m.def(
+      "check_block_diagonal",
+      [](std::uintptr_t w, const wf::Shape& s, std::int64_t groups, std::uintptr_t scratch, std::uintptr_t stream) {
+        py::gil_scoped_release nogil;
+        wf::check_block_diagonal(F(w), s, groups, P(scratch), P(stream));
+      },
+      py::arg("w"), py::arg("dense_shape"), py::arg("groups"), py::arg("scratch"), py::arg("stream"));
+
+  py::class_<wf::FoldedConv>(m, "FoldedConv")
+      .def(py::init([](const wf::Shape& in, const wf::Shape& filt, std::int64_t sh, std::int64_t sw,
+                       std::int64_t ph, std::int64_t pw, const std::string& dtype, std::int64_t factor,
+                       std::int64_t group_size) {
+             return wf::FoldedConv(spec_of(in, filt, sh, sw, ph, pw), dtype_of(dtype), factor, group_size);
+           }),
+           py::arg("input_shape"), py::arg("filter_shape"), py::arg("stride_h") = 1, py::arg("stride_w") = 1,
+           py::arg("pad_h") = 0, py::arg("pad_w") = 0, py::arg("dtype") = "bf16", py::arg("factor") = 0,
+           py::arg("group_size") = 0)
+      .def_property_readonly("packed_bytes", &wf::FoldedConv::packed_bytes)
+      .def_property_readonly("cout_f", &wf::FoldedConv::cout_f)
+      .def_property_readonly("plan", [](const wf::FoldedConv& c) { return plan_dict(c.plan()); })
+      .def_property_readonly("device", [](const wf::FoldedConv& c) { return raw_dict(c.raw()); })
+      .def_property_readonly("output_shape", [](const wf::FoldedConv& c) { return c.spec().output_shape(); })
+      .def(
+          "pack",
+          [](const wf::FoldedConv& c, std::uintptr_t w, std::uintptr_t b, std::uintptr_t packed, std::uintptr_t brep,
+             std::uintptr_t stream) {
+            py::gil_scoped_release nogil;
+            c.pack(P(w), b ? F(b) : nullptr, P(packed), brep ? static_cast<float*>(P(brep)) : nullptr, P(stream));
+          },
+          py::arg("w"), py::arg("b"), py::arg("packed"), py::arg("b_rep"), py::arg("stream"))
+      .def(
+          "forward",
+          [](const wf::FoldedConv& c, std::uintptr_t x, std::uintptr_t packed, std::uintptr_t brep, std::uintptr_t y,
+             const std::string& out_dtype, bool bias, bool relu, std::uintptr_t stream, std::uint32_t flags) {
+            const wf::Dtype od = dtype_of(out_dtype);
+            py::gil_scoped_release nogil;
+            c.forward(P(x), P(packed), brep ? F(brep) : nullptr, P(y), od, bias, relu, P(stream), flags);
+          },
+          py::arg("x"), py::arg("packed"), py::arg("b_rep"), py::arg("y"), py::arg("out_dtype"), py::arg("bias"),
+          py::arg("relu"), py::arg("stream"), py::arg("profile_flags") = 0);
+}

@@ -23,4 +23,13 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
                       const float* b_rep, void* y, wf_dtype out_dtype, uint32_t epilogue,
                       cudaStream_t st, int num_sms, std::string* err);
 
+// Exact-order fp32 direct conv (reference conv2d semantics, with padding).
+wf_status launch_conv_direct(const wf_conv_desc& d, const float* x, const float* w, float* y, cudaStream_t st,
+                             std::string* err);
+wf_status launch_bias_add(const float* y, const float* b, float* out, long long n, int C, int relu, cudaStream_t st,
+                          std::string* err);
+wf_status launch_blockdiag_check(const float* wd, int KH, int KW, int Cif, int Cof, int groups,
+                                 unsigned long long* scratch, long long* first_bad, cudaStream_t st, std::string* err);
+wf_status launch_replicate_bias(const float* b, int cout, int r, float* out, cudaStream_t st, std::string* err);
+
 }  // namespace wfb

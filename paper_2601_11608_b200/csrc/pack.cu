@@ -165,6 +165,16 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
   return WF_OK;
 }
 
+wf_status launch_replicate_bias(const float* b, int cout, int r, float* out, cudaStream_t st, std::string* err) {
+  replicate_bias_kernel<<<(cout * r + 255) / 256, 256, 0, st>>>(b, out, cout, r);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("replicate_bias_kernel: ") + cudaGetErrorString(e);
+    return WF_CUDA_ERROR;
+  }
+  return WF_OK;
+}
+
 wf_status launch_expand_dense(const wf_conv_desc& d, int64_t f, const float* w, float* out, cudaStream_t st,
                               std::string* err) {
   const int64_t s = d.stride_w;

@@ -1,0 +1,241 @@
+"""GPU parity: the sm_100a kernels vs the pinned oracle / reference goldens.
+
+Tolerances (north star): integer-valued data exact; bf16/fp16 normwise
+max|y - y_ref| / max|y_ref| <= 1e-2; TF32 <= 1e-3; the exact-fp32 CUDA-core
+path and all index transforms bit-exact. Inputs are device-representable
+(quantised) values, so differences isolate accumulation order and output
+rounding.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_11608_b200 as wf
+from tests.test_oracle import CONFIG_GEOM
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"bf16": 1e-2, "f16": 1e-2, "f32": 1e-3}
+TDT = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}
+
+
+def normrel(y, ref):
+    y = np.asarray(y, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+def cuda(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(dtype)
+
+
+def test_exact_conv_matches_reference_bitwise(golden_conv):
+    tags = sorted({k.rsplit("_", 1)[0] for k in golden_conv if k.endswith("_x")})
+    for tag in tags:
+        g = {k[len(tag) + 1:]: v for k, v in golden_conv.items() if k.startswith(tag + "_")}
+        sh, sw = (int(v) for v in g["stride"])
+        y = wf.conv2d(g["x"], g["w"], sh, sw)  # numpy in -> reference semantics (exact fp32)
+        assert isinstance(y, np.ndarray)
+        np.testing.assert_array_equal(y.view(np.uint32), g["y"].view(np.uint32), err_msg=tag)
+        yb = wf.bias_add(y, g["b"])
+        np.testing.assert_array_equal(yb.view(np.uint32), g["yb"].view(np.uint32), err_msg=tag)
+        yb2 = wf.conv2d(g["x"], g["w"], sh, sw, bias=g["b"])
+        np.testing.assert_array_equal(yb2.view(np.uint32), g["yb"].view(np.uint32), err_msg=tag)
+
+
+def test_appendix_a_on_device(golden_appendix):
+    for kind in ("float", "int"):
+        g = {k[len(kind) + 1:]: v for k, v in golden_appendix.items() if k.startswith(kind + "_")}
+        plan, x_f, w_f, b_f = wf.apply_width_fold(g["x"], g["w"], g["b"], 8)
+        assert plan["status"] == "apply" and plan["folded_input_shape"] == [1, 32, 8, 8]
+        np.testing.assert_array_equal(x_f, g["x_f"])
+        np.testing.assert_array_equal(w_f, g["w_f"])
+        np.testing.assert_array_equal(b_f, g["b_f"])
+        y = wf.reconstruct_output(wf.bias_add(wf.conv2d(x_f, w_f), b_f), 8)
+        np.testing.assert_array_equal(y, g["y_folded"])
+
+
+def test_fallback_keeps_inputs():
+    x = np.zeros((1, 4, 7, 1), np.float32)
+    plan, x2, w2, b2 = wf.apply_width_fold(x, np.zeros((3, 1, 1, 1), np.float32), np.zeros(1, np.float32), 8)
+    assert plan["status"] == "fallback" and plan["reason"] == "WidthNotDivisible"
+    np.testing.assert_array_equal(x2, x)
+    with pytest.raises(ValueError):
+        wf.fold_input(np.zeros((1, 2, 7, 1), np.float32), 2)
+
+
+def test_fold_views_are_zero_copy():
+    x = torch.randn(2, 8, 32, 3, device="cuda")
+    xf = wf.fold_input_general(x, 16)
+    assert xf.data_ptr() == x.data_ptr() and tuple(xf.shape) == (2, 8, 2, 48)
+    back = wf.unfold_input_general(xf, 16)
+    assert back.data_ptr() == x.data_ptr() and torch.equal(back, x)
+    y = torch.randn(2, 5, 14, 512, device="cuda")
+    r = wf.reconstruct_output(y, 8)
+    assert r.data_ptr() == y.data_ptr() and tuple(r.shape) == (2, 5, 112, 64)
+
+
+def test_expand_filters_bitwise(golden_kats, golden_configs, oracle):
+    np.testing.assert_array_equal(wf.expand_filter_general(golden_kats["expand_general_in"], 4),
+                                  golden_kats["expand_general_out_f4"])
+    np.testing.assert_array_equal(wf.expand_filter(golden_kats["expand_in"], 2), golden_kats["expand_out"])
+    np.testing.assert_array_equal(wf.replicate_bias(np.array([1, 2], np.float32), 3), golden_kats["replicate"])
+    for name, f in CONFIG_GEOM.items():
+        KH, KW, C, Co, s, p, relu = (int(v) for v in golden_configs[f"{name}_geom"])
+        w = golden_configs[f"{name}_w"]
+        np.testing.assert_array_equal(wf.expand_filter_folded(w, f, s, p), oracle.expand_filter_folded(w, f, s, p),
+                                      err_msg=name)
+    with pytest.raises(wf.IllegalFoldError):
+        wf.expand_filter_general(np.zeros((3, 3, 1, 1), np.float32), 2)
+
+
+def _config_run(golden_configs, name, suffix, out_dtype=None):
+    KH, KW, C, Co, s, p, relu = (int(v) for v in golden_configs[f"{name}_geom"])
+    dt = str(golden_configs[f"{name}_dtype"])
+    x, w, b = (golden_configs[f"{name}_{k}{suffix}"] for k in ("x", "w", "b"))
+    tdt = TDT[dt]
+    conv = wf.FoldedConv2d(cuda(w, tdt), cuda(b), x.shape, stride=s, padding=p, dtype=tdt)
+    y = conv(cuda(x, tdt), relu=bool(relu), out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy(), golden_configs[f"{name}_y{suffix}"], dt, conv
+
+
+@pytest.mark.parametrize("name", [n for n in CONFIG_GEOM if n != "alexnet"])
+def test_tensor_core_conv_configs_within_tolerance(golden_configs, name):
+    y, ref, dt, conv = _config_run(golden_configs, name, "")
+    assert y.shape == ref.shape
+    err = normrel(y, ref)
+    assert err <= TOL[dt], f"{name}: normwise rel {err:.3e} > {TOL[dt]} (plan {conv.device_plan})"
+
+
+@pytest.mark.parametrize("name", [n for n in CONFIG_GEOM if n != "alexnet"])
+def test_tensor_core_conv_integer_data_exact(golden_configs, name):
+    y, ref, dt, _ = _config_run(golden_configs, name, "i", out_dtype=torch.float32)
+    np.testing.assert_array_equal(y, ref, err_msg=name)
+
+
+def test_packed_operand_unpacks_to_the_expansion(oracle):
+    """The once-packed tcgen05 B operand holds exactly W'(kh, kw', fi*C+c, j*Co+co)."""
+    rng = np.random.default_rng(5)
+    KH, KW, C, Co, s, p = 7, 7, 3, 64, 2, 3
+    w = rng.integers(-8, 9, (KH, KW, C, Co)).astype(np.float32)
+    conv = wf.FoldedConv2d(cuda(w, torch.bfloat16), None, (2, 64, 64, 3), stride=s, padding=p,
+                           dtype=torch.bfloat16)
+    d = conv.device_plan
+    f, gs = d["f"], d["group_size"]
+    wexp = oracle.expand_filter_folded(w, f, s, p)  # (KH, KW', f*C, r*Co)
+    raw = conv.packed.cpu().numpy()
+    n_ent = d["mma_entries"]
+    table = raw[: n_ent * 16].view(np.uint32).reshape(n_ent, 4)
+    table_bytes = (n_ent * 16 + 127) // 128 * 128
+    Ng = gs * Co
+    block = Ng * 32
+    E = 16
+    base = table_bytes
+    last_end = 0
+    checked = 0
+    for i, (a_off, b_off, meta, col) in enumerate(table):
+        if i > 0 and b_off == 0:  # B offsets restart at each N-tile
+            base += last_end
+        last_end = int(b_off) + block
+        kh, u, g = meta & 0xFF, (meta >> 8) & 0xFF, (meta >> 16) & 0x7FFF
+        blk = raw[base + b_off: base + b_off + block].view(np.uint16).reshape(2, Ng, 8)
+        vals = (blk.astype(np.uint32) << 16).view(np.float32)
+        for cc in range(2):
+            widx = u * E + cc * 8 + np.arange(8)
+            kp, k = widx // (f * C), widx % (f * C)
+            for nrow in range(0, Ng, 7):
+                n = g * Ng + nrow
+                np.testing.assert_array_equal(vals[cc, nrow], wexp[kh, kp, k, n])
+                checked += 1
+    assert checked > 100
+
+
+@pytest.mark.parametrize("batch,h,w", [(3, 36, 48), (1, 224, 224), (5, 20, 32), (2, 9, 16)])
+def test_partial_tiles_and_odd_shapes(oracle, batch, h, w):
+    """OH not a multiple of the 8-row M tile, tiny images, batch tails: exact on integers."""
+    rng = np.random.default_rng(batch * 100 + h)
+    x = rng.integers(-4, 5, (batch, h, w, 3)).astype(np.float32)
+    wt = rng.integers(-4, 5, (7, 7, 3, 64)).astype(np.float32)
+    b = rng.integers(-4, 5, (64,)).astype(np.float32)
+    conv = wf.FoldedConv2d(cuda(wt, torch.bfloat16), cuda(b), x.shape, stride=2, padding=3, dtype=torch.bfloat16)
+    y = conv(cuda(x, torch.bfloat16), out_dtype=torch.float32).cpu().numpy()
+    ref = oracle.conv_padded(x, wt, b, 2, 3)
+    np.testing.assert_array_equal(y, ref)
+
+
+def test_epilogue_variants(oracle):
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1, 1, (2, 32, 32, 3)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (3, 3, 3, 32)) / 5).astype(np.float32)
+    b = rng.uniform(-1, 1, (32,)).astype(np.float32)
+    xq = cuda(x, torch.float16)
+    wq = cuda(w, torch.float16)
+    xs, ws = xq.float().cpu().numpy(), wq.float().cpu().numpy()
+    conv = wf.FoldedConv2d(wq, cuda(b), x.shape, stride=2, padding=1, dtype=torch.float16)
+    for relu in (False, True):
+        for bias in (False, True):
+            for od in (torch.float16, torch.float32, torch.bfloat16):
+                y = conv(xq, relu=relu, bias=bias, out_dtype=od).float().cpu().numpy()
+                ref = oracle.conv_padded(xs, ws, b if bias else None, 2, 1, relu)
+                assert normrel(y, ref) <= 1e-2, (relu, bias, od)
+
+
+def test_full_size_sampled_images(oracle):
+    """Full 224x224 geometry, batch 6: compare two sampled images with the oracle."""
+    rng = np.random.default_rng(1234)
+    for (KH, Co, s, p, dt) in ((7, 64, 2, 3, torch.bfloat16), (3, 64, 1, 1, torch.bfloat16),
+                               (3, 32, 2, 1, torch.float16)):
+        x = torch.from_numpy(rng.uniform(-1, 1, (6, 224, 224, 3)).astype(np.float32)).cuda().to(dt)
+        w = torch.from_numpy((rng.uniform(-1, 1, (KH, KH, 3, Co)) / KH / 2).astype(np.float32)).cuda().to(dt)
+        b = torch.from_numpy(rng.uniform(-1, 1, (Co,)).astype(np.float32)).cuda()
+        conv = wf.FoldedConv2d(w, b, x.shape, stride=s, padding=p, dtype=dt)
+        y = conv(x).float().cpu().numpy()
+        for i in (0, 5):
+            ref = oracle.conv_padded(x[i:i + 1].float().cpu().numpy(), w.float().cpu().numpy(), b.cpu().numpy(), s, p)
+            assert normrel(y[i:i + 1], ref) <= 1e-2
+
+
+def test_tf32_path_within_1e3(golden_configs):
+    y, ref, dt, conv = _config_run(golden_configs, "r50_b1", "")
+    assert dt == "f32" and conv.device_plan["f"] == 8
+    assert normrel(y, ref) <= 1e-3
+    y2 = wf.conv2d(golden_configs["r50_b1_x"], golden_configs["r50_b1_w"], 2, 2, padding=3,
+                   bias=golden_configs["r50_b1_b"], precision="tf32")
+    assert normrel(y2, ref) <= 1e-3
+
+
+def test_grouped_conv_and_block_diagonal_check(oracle):
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((1, 10, 8, 1)).astype(np.float32)
+    w = rng.standard_normal((3, 1, 1, 1)).astype(np.float32)
+    x_f = wf.fold_input(x, 8)
+    w_f = wf.expand_filter(w, 8)
+    np.testing.assert_array_equal(wf.grouped_conv(x_f, w_f, 8), wf.conv2d(x_f, w_f))
+    np.testing.assert_array_equal(wf.grouped_conv(x_f, w_f, 8), oracle.grouped_conv(x_f, w_f, 8))
+    bad = w_f.copy()
+    bad[0, 0, 0, 3] = 1e-30
+    with pytest.raises(wf.NotBlockDiagonalError):
+        wf.grouped_conv(x_f, bad, 8)
+
+
+def test_conv1d_and_gemm_routes(oracle):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((12, 9, 1)).astype(np.float32)
+    k = rng.standard_normal(4).astype(np.float32)
+    y = wf.conv1d_h(x, k, 0.5)
+    ref = oracle.bias_add(oracle.conv2d(x.reshape(1, 12, 9, 1), k.reshape(4, 1, 1, 1)),
+                          np.array([0.5], np.float32)).reshape(9, 9, 1)
+    np.testing.assert_array_equal(y, ref)
+    a = rng.integers(-4, 5, (16, 3)).astype(np.float32)
+    bm = rng.integers(-4, 5, (3, 4)).astype(np.float32)
+    want = (a.astype(np.float64) @ bm.astype(np.float64)).astype(np.float32)
+    np.testing.assert_array_equal(wf.gemm_ref(a, bm), want)
+    np.testing.assert_array_equal(wf.gemm_as_conv1x1(a, bm), want)
+    np.testing.assert_array_equal(wf.fold_tall_skinny(a, bm, 8), want)
+
+
+def test_no_cpu_fallback_on_cpu_tensors():
+    conv = wf.FoldedConv2d(torch.randn(3, 3, 3, 16, device="cuda").bfloat16(), None, (1, 32, 32, 3), padding=1)
+    with pytest.raises(ValueError):
+        conv(torch.randn(1, 32, 32, 3).bfloat16())

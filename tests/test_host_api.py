@@ -1,0 +1,114 @@
+"""CPU: the C++ host layer (_core, namespace widthfold) reproduces the
+reference's host-side API: legality, auto factor, MAC accounting, errors."""
+import ast
+
+import numpy as np
+import pytest
+
+import paper_2601_11608_b200 as wf
+from paper_2601_11608_b200 import _core
+
+
+def test_reference_names_exported():
+    ref_names = ["apply_width_fold", "apply_width_fold_general", "bias_add", "check_legality",
+                 "choose_fold_factor", "conv1d_h", "conv2d", "count_macs", "expand_filter",
+                 "expand_filter_general", "fold_input", "fold_input_general", "fold_tall_skinny",
+                 "gemm_as_conv1x1", "gemm_ref", "grouped_conv", "mac_report", "reconstruct_output",
+                 "replicate_bias", "unfold_input_general"]  # /root/reference/proj/python/widthfold/__init__.py:27-48
+    for n in ref_names:
+        assert callable(getattr(wf, n)), n
+        assert n in wf.__all__
+
+
+def test_exception_hierarchy():
+    assert issubclass(wf.ShapeMismatchError, ValueError)
+    assert issubclass(wf.IllegalFoldError, ValueError)
+    assert issubclass(wf.DegenerateOutputError, ValueError)
+    assert issubclass(wf.NotBlockDiagonalError, RuntimeError)
+
+
+def test_legality_table_matches_reference(golden_kats):
+    for row in golden_kats["legality"]:
+        shape, filt, f, status, reason, fis, efs = ast.literal_eval(str(row))
+        p = wf.check_legality(shape, filt, f)
+        assert (p["status"], p["reason"], p["folded_input_shape"], p["expanded_filter_shape"]) == \
+            (status, reason, fis, efs), row
+
+
+def test_choose_table_matches_reference(golden_kats):
+    for row in golden_kats["choose"]:
+        shape, filt, status, reason, factor, fis, efs = ast.literal_eval(str(row))
+        p = wf.choose_fold_factor(shape, filt)
+        assert (p["status"], p["reason"], p["factor"], p["folded_input_shape"], p["expanded_filter_shape"]) == \
+            (status, reason, factor, fis, efs), row
+
+
+def test_mac_report_and_count_macs(golden_kats):
+    r = wf.mac_report([1, 32, 64, 1], [5, 1, 1, 1], 8)
+    assert [r["original"], r["dense_folded"], r["grouped_folded"], r["zero_padded"]] == \
+        list(golden_kats["mac_report"])
+    r = wf.mac_report([1, 16, 16, 3], [3, 1, 3, 4], 8)
+    assert [r["original"], r["dense_folded"], r["grouped_folded"], r["zero_padded"]] == \
+        list(golden_kats["mac_report_rgb"])
+    assert wf.count_macs([1, 32, 64, 1], [5, 1, 1, 1]) == golden_kats["count_macs"][0]
+    assert wf.count_macs([2, 9, 11, 3], [3, 2, 3, 5], 2, 3) == golden_kats["count_macs"][1]
+    with pytest.raises(ValueError):
+        wf.mac_report([1, 4, 7, 1], [3, 1, 1, 1], 8)  # fallback plan -> invalid_argument
+
+
+def test_errors_match_reference():
+    with pytest.raises(wf.ShapeMismatchError):
+        wf.check_legality([1, 8, 8], [3, 1, 1, 1], 2)
+    with pytest.raises(wf.DegenerateOutputError):
+        wf.check_legality([1, 2, 8, 1], [3, 1, 1, 1], 2)
+    with pytest.raises(ValueError):
+        wf.check_legality([1, 8, 8, 1], [3, 1, 1, 1], 0)
+    with pytest.raises(ValueError):
+        wf.choose_fold_factor([1, 8, 8, 1], [3, 1, 1, 1], align=0)
+
+
+CONFIGS = {  # name: (input, filter, stride, pad, dtype) -- BASELINE.json configs
+    "r50_b1": ([1, 224, 224, 3], [7, 7, 3, 64], 2, 3, "tf32"),
+    "vgg16": ([256, 224, 224, 3], [3, 3, 3, 64], 1, 1, "bf16"),
+    "mnv2": ([1024, 224, 224, 3], [3, 3, 3, 32], 2, 1, "f16"),
+    "r50_b8192": ([8192, 224, 224, 3], [7, 7, 3, 64], 2, 3, "bf16"),
+}
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_device_plans_for_configs(name, oracle):
+    shape, filt, s, p, dt = CONFIGS[name]
+    plan = wf.plan_fold(shape, filt, s, s, p, p, dtype=dt)
+    assert plan["status"] == "apply", plan
+    d = plan["device"]
+    esize = 4 if dt == "tf32" else 2
+    assert d["f"] % s == 0 and (d["f"] * 3 * esize) % 32 == 0
+    r, c0, kwf = oracle.fold_geometry(d["f"], s, p, filt[1])
+    assert (d["r"], d["c0"], d["kw_f"]) == (r, c0, kwf)
+    assert plan["expanded_filter_shape"] == [filt[0], kwf, d["f"] * 3, r * filt[3]]
+    oh = (shape[1] + 2 * p - filt[0]) // s + 1
+    assert d["useful_macs"] == wf.count_macs(shape, filt, s, s, p, p)
+    assert d["useful_macs"] == shape[0] * oh * oh * filt[3] * filt[0] * filt[1] * 3
+    assert d["issued_macs"] >= d["useful_macs"]
+
+
+def test_alexnet_plan_reports_reason():
+    # W = 227 is prime: no pure-reshape fold exists (the reference also says WidthNotDivisible)
+    plan = wf.plan_fold([512, 227, 227, 3], [11, 11, 3, 96], 4, 4, 0, 0, dtype="bf16")
+    assert plan["status"] == "fallback"
+    assert plan["reason"] in ("WidthNotDivisible", "FactorTooLarge")
+
+
+def test_generalized_legality_reasons():
+    assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=16)["reason"] == "WidthNotDivisible"
+    assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], 2, 3, factor=16)["reason"] == "StrideOnFoldAxis"
+    assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], factor=8)["reason"] == "UnalignedPixel"
+    with pytest.raises(wf.ShapeMismatchError):
+        wf.plan_fold([1, 32, 32, 3], [3, 3, 4, 16])
+
+
+def test_folded_filter_shape():
+    assert _core.folded_filter_shape([7, 7, 3, 64], 16, 2, 3) == [7, 3, 48, 512]
+    assert _core.folded_filter_shape([5, 1, 1, 1], 8) == [5, 1, 8, 8]
+    with pytest.raises(wf.IllegalFoldError):
+        _core.folded_filter_shape([7, 7, 3, 64], 3, 2, 3)
