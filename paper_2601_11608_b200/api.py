@@ -113,6 +113,7 @@ class FoldedConv2d:
             self.b_rep = torch.empty(self.core.cout_f, dtype=torch.float32, device=dev)
         self.core.pack(w.data_ptr(), _ptr(bf), self.packed.data_ptr(), _ptr(self.b_rep), _stream(dev))
         self._keep = (w, bf)
+        self._geom = (sh, sw, ph, pw)
         self.output_shape = tuple(self.core.output_shape)
 
     @property
@@ -141,6 +142,56 @@ class FoldedConv2d:
         self.core.forward(x.data_ptr(), self.packed.data_ptr(), _ptr(self.b_rep) if use_bias else 0,
                           out.data_ptr(), _OUT_NAME[out_dtype], use_bias, relu, _stream(x.device), _profile_flags)
         return out
+
+
+    def with_batch(self, n: int) -> "FoldedConv2d":
+        """Same filter for batch ``n`` -- shares the packed operand (the pack is batch-independent)."""
+        other = object.__new__(FoldedConv2d)
+        other.__dict__.update(self.__dict__)
+        shape = (int(n),) + self.input_shape[1:]
+        sh, sw, ph, pw = self._geom
+        w = self._keep[0]
+        other.core = _core.FoldedConv(list(shape), list(w.shape), sh, sw, ph, pw, _DT_NAME[self.dtype],
+                                      self.core.device["f"], self.core.device["group_size"])
+        if other.core.packed_bytes != self.core.packed_bytes:
+            raise UnsupportedError("batch-specific plan changed the packed operand")
+        other.input_shape = shape
+        other.output_shape = tuple(other.core.output_shape)
+        return other
+
+    def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor, *, chunk: int = 512, relu: bool = False,
+                 bias: bool = True) -> torch.Tensor:
+        """End to end from host memory: pinned x_host (N,H,W,C) -> y_host (N,OH,OW,Cout).
+
+        Chunks of ``chunk`` images alternate over two streams, so the H2D copy of
+        one chunk, the folded conv of another and the D2H copy of a third overlap.
+        """
+        if x_host.is_cuda or y_host.is_cuda:
+            raise ValueError("run_host takes host tensors (pinned for overlap)")
+        n = x_host.shape[0]
+        dev = self.packed.device
+        chunk = max(1, min(chunk, n))
+        convs = {}
+        streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        cur = torch.cuda.current_stream(dev)
+        for s in streams:
+            s.wait_stream(cur)
+        xbufs = [torch.empty((chunk,) + self.input_shape[1:], dtype=self.dtype, device=dev) for _ in range(2)]
+        ybufs = [torch.empty((chunk,) + self.output_shape[1:], dtype=y_host.dtype, device=dev) for _ in range(2)]
+        for i, start in enumerate(range(0, n, chunk)):
+            m = min(chunk, n - start)
+            k = i & 1
+            with torch.cuda.stream(streams[k]):
+                conv = convs.get(m)
+                if conv is None:
+                    conv = convs[m] = self.with_batch(m) if m != self.input_shape[0] else self
+                xd, yd = xbufs[k][:m], ybufs[k][:m]
+                xd.copy_(x_host[start:start + m], non_blocking=True)
+                conv(xd, relu=relu, bias=bias, out=yd, out_dtype=y_host.dtype)
+                y_host[start:start + m].copy_(yd, non_blocking=True)
+        for s in streams:
+            cur.wait_stream(s)
+        return y_host
 
 
 _FOLD_CACHE: dict[Any, tuple[Any, FoldedConv2d]] = {}
