@@ -74,7 +74,7 @@ wf_status wf_conv_fold_fwd(const void* x, const void* w_packed, const float* b_r
                            const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype, uint32_t epilogue,
                            void* stream) {
   if (!x || !w_packed || !y || !desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
-  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0x700))  // 0x700: profiling switches
+  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0x1F00))  // 0x1F00: profiling / epilogue-mode switches
     return fail(WF_INVALID_ARGUMENT, "unknown epilogue flags");
   wfb::Schedule S;
   std::string err;

@@ -42,7 +42,7 @@ struct ConvArgs {
   int s;
   unsigned res_mask;
   int amin[kMaxResidues];
-  int box_bytes, region_bytes;
+  int box_bytes, shift_box_bytes, region_bytes, shift_off;
   int stages, stage_bytes;
   int n_tiles, ctas_per_ntile;
   int nt_entry0[kMaxNTiles], nt_entries[kMaxNTiles], nt_col0[kMaxNTiles], nt_cols[kMaxNTiles];
@@ -60,6 +60,8 @@ struct ConvArgs {
 
 struct TmaMaps {
   CUtensorMap in[kMaxResidues];
+  CUtensorMap in_shift[kMaxResidues];  // core column 0 one folded column further (region Q)
+  CUtensorMap out;  // per-warp store box (TMA-store epilogue)
 };
 
 template <typename OutT>
@@ -73,6 +75,77 @@ template <>
 __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
   __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int CC>
+__device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&r)[CC], bool skip = false) {
+  if (skip) {
+#pragma unroll
+    for (int k = 0; k < CC; ++k) r[k] = taddr + k;  // profiling: no TMEM traffic
+    return;
+  }
+  if constexpr (CC == 32) ptx::tmem_ld32(taddr, r); else ptx::tmem_ld16(taddr, r);
+}
+
+// +bias (vectorised broadcast loads from smem) -> ReLU -> convert -> two 256-bit
+// stores of this thread's 64-byte row segment.
+template <typename OutT, int CC>
+__device__ __forceinline__ void epi_store_chunk(const uint32_t (&r)[CC], const float* sb, bool relu, bool valid,
+                                                uint8_t* dst) {
+  float v[CC];
+#pragma unroll
+  for (int k = 0; k < CC; k += 4) {
+    const float4 bb = *reinterpret_cast<const float4*>(sb + k);
+    v[k + 0] = __uint_as_float(r[k + 0]) + bb.x;
+    v[k + 1] = __uint_as_float(r[k + 1]) + bb.y;
+    v[k + 2] = __uint_as_float(r[k + 2]) + bb.z;
+    v[k + 3] = __uint_as_float(r[k + 3]) + bb.w;
+  }
+  if (relu) {
+#pragma unroll
+    for (int k = 0; k < CC; ++k) v[k] = (v[k] < 0.0f) ? 0.0f : v[k];
+  }
+  uint32_t pk[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if constexpr (sizeof(OutT) == 4) pk[k] = __float_as_uint(v[k]);
+    else pk[k] = pack2<OutT>(v[2 * k], v[2 * k + 1]);
+  }
+  if (valid) {
+    ptx::st_global_v8(dst, pk);
+    ptx::st_global_v8(dst + 32, pk + 8);
+  }
+}
+
+// Same math, but the 64-byte row segment goes to this warp's 64B-swizzled
+// staging buffer (row = lane); the warp then TMA-stores the whole box.
+template <typename OutT, int CC>
+__device__ __forceinline__ void epi_stage_chunk(const uint32_t (&r)[CC], const float* sb, bool relu, uint32_t stg,
+                                                uint32_t lane) {
+  float v[CC];
+#pragma unroll
+  for (int k = 0; k < CC; k += 4) {
+    const float4 bb = *reinterpret_cast<const float4*>(sb + k);
+    v[k + 0] = __uint_as_float(r[k + 0]) + bb.x;
+    v[k + 1] = __uint_as_float(r[k + 1]) + bb.y;
+    v[k + 2] = __uint_as_float(r[k + 2]) + bb.z;
+    v[k + 3] = __uint_as_float(r[k + 3]) + bb.w;
+  }
+  if (relu) {
+#pragma unroll
+    for (int k = 0; k < CC; ++k) v[k] = (v[k] < 0.0f) ? 0.0f : v[k];
+  }
+  uint32_t pk[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if constexpr (sizeof(OutT) == 4) pk[k] = __float_as_uint(v[k]);
+    else pk[k] = pack2<OutT>(v[2 * k], v[2 * k + 1]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t lin = lane * 64u + q * 16u;
+    ptx::st_shared_v4(stg + (lin ^ (((lin >> 7) & 3u) << 4)), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  }
 }
 
 template <int kKind, typename OutT>
@@ -118,7 +191,10 @@ __global__ void __launch_bounds__(320, 1)
   }
   if (warp == 0 && lane == 0) {
     for (int b = 0; b < a.s; ++b)
-      if ((a.res_mask >> b) & 1u) prefetch_tmap(&maps.in[b]);
+      if ((a.res_mask >> b) & 1u) {
+        prefetch_tmap(&maps.in[b]);
+        if (a.shift_box_bytes) prefetch_tmap(&maps.in_shift[b]);
+      }
   }
   if (warp == 1) tmem_alloc(smem_u32(tmem_slot), a.tmem_cols);
   tc_fence_before();
@@ -134,7 +210,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
       for (int off = 0; off < bb; off += 32768)
         bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
-      const uint32_t tx = static_cast<uint32_t>(a.box_bytes * __popc(a.res_mask));
+      const uint32_t tx = static_cast<uint32_t>((a.box_bytes + a.shift_box_bytes) * __popc(a.res_mask));
       int it = 0;
       for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it) {
         const int stage = it % a.stages;
@@ -144,10 +220,13 @@ __global__ void __launch_bounds__(320, 1)
         const int oh0 = (mt - n * a.ohb) * a.OHt;
         const uint32_t dst = base + a.off_a + stage * a.stage_bytes;
         mbar_arrive_expect_tx(bar_full + 8 * stage, tx);
-        for (int b = 0; b < a.s; ++b)
-          if ((a.res_mask >> b) & 1u)
-            tma_load_5d(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n,
+        for (int b = 0; b < a.s; ++b) {
+          if (!((a.res_mask >> b) & 1u)) continue;
+          tma_load_5d(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, bar_full + 8 * stage);
+          if (a.shift_box_bytes)
+            tma_load_5d(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1, oh0 + a.amin[b], 0, n,
                         bar_full + 8 * stage);
+        }
       }
     }
     __syncwarp();
@@ -210,6 +289,11 @@ __global__ void __launch_bounds__(320, 1)
     const bool relu = (a.epi_flags & WF_EPI_RELU) != 0;
     const bool dbg_skip_epi = (a.epi_flags & 0x200) != 0;
     const bool dbg_skip_store = (a.epi_flags & 0x400) != 0;
+    const bool skip_ld = (a.epi_flags & 0x800) != 0;
+    const bool tma_store = (a.epi_flags & 0x1000) != 0;
+    const uint32_t stg = base + a.off_stg + static_cast<uint32_t>(warp - 2) * 2048u;
+    const int t_first = (a.Wbox <= 32) ? (quarter * 32) / a.Wbox : (quarter * 32) / a.Wbox;
+    const int w_first = (a.Wbox <= 32) ? 0 : (quarter * 32) % a.Wbox;
     const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
     const int m = quarter * 32 + lane;
     const int t = m / a.Wbox;
@@ -232,47 +316,45 @@ __global__ void __launch_bounds__(320, 1)
       uint8_t* grow = a.out + ((static_cast<long long>(n) * a.OH + oh) * a.Wfo + wq) * a.row_bytes +
                       static_cast<long long>(col0) * sizeof(OutT);
       const uint32_t trow = tmem_base + acc * a.acc_stride + (static_cast<uint32_t>(quarter * 32) << 16);
-      uint32_t r[2][CC];
-      if constexpr (CC == 32) tmem_ld32(trow + half * CC, r[0]); else tmem_ld16(trow + half * CC, r[0]);
+      // Two register sets so the TMEM load of the next chunk overlaps this
+      // chunk's convert + store; the loop is unrolled by two so the set
+      // selection is static.
+      uint32_t r0[CC], r1[CC];
+      tmem_ld_chunk<CC>(trow + half * CC, r0, skip_ld);
       tmem_ld_wait();
-      reg_fence<CC>(r[0]);
-      int cur = 0;
+      reg_fence<CC>(r0);
+      // chunk store: direct 256-bit st.global (default) or per-warp TMA box store
+      auto emit = [&](const uint32_t (&rr)[CC], int c) {
+        if (tma_store) {
+          if (lane == 0) bulk_wait_read_0();  // staging buffer free again
+          __syncwarp();
+          epi_stage_chunk<OutT, CC>(rr, sbias + c * CC, relu, stg, static_cast<uint32_t>(lane));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && !dbg_skip_store) {
+            tma_store_4d(&maps.out, stg, col0 + c * CC, w_first, oh0 + t_first, n);
+            bulk_commit();
+          }
+        } else {
+          epi_store_chunk<OutT, CC>(rr, sbias + c * CC, relu, valid, grow + c * 64);
+        }
+      };
 #pragma unroll 1
-      for (int ch = half; ch < nchunks; ch += 2) {
-        const int nxt = ch + 2;
-        if (nxt < nchunks) {  // prefetch this warp's next chunk
-          if (cur == 0) {
-            if constexpr (CC == 32) tmem_ld32(trow + nxt * CC, r[1]); else tmem_ld16(trow + nxt * CC, r[1]);
-          } else {
-            if constexpr (CC == 32) tmem_ld32(trow + nxt * CC, r[0]); else tmem_ld16(trow + nxt * CC, r[0]);
-          }
-        }
-        uint32_t pk[16];
-#pragma unroll
-        for (int k = 0; k < CC; k += (sizeof(OutT) == 4 ? 1 : 2)) {
-          float x0 = __uint_as_float(cur == 0 ? r[0][k] : r[1][k]) + sbias[ch * CC + k];
-          if (relu) x0 = (x0 < 0.0f) ? 0.0f : x0;
-          if constexpr (sizeof(OutT) == 4) {
-            pk[k] = __float_as_uint(x0);
-          } else {
-            float x1 = __uint_as_float(cur == 0 ? r[0][k + 1] : r[1][k + 1]) + sbias[ch * CC + k + 1];
-            if (relu) x1 = (x1 < 0.0f) ? 0.0f : x1;
-            pk[k / 2] = pack2<OutT>(x0, x1);
-          }
-        }
-        if (valid) {
-          st_global_v8(grow + ch * 64, pk);
-          st_global_v8(grow + ch * 64 + 32, pk + 8);
-        }
+      for (int ch = half; ch < nchunks; ch += 4) {
+        if (ch + 2 < nchunks) tmem_ld_chunk<CC>(trow + (ch + 2) * CC, r1, skip_ld);
+        emit(r0, ch);
         tmem_ld_wait();
-        if (nxt < nchunks) {
-          if (cur == 0) reg_fence<CC>(r[1]); else reg_fence<CC>(r[0]);
-        }
-        cur ^= 1;
+        if (ch + 2 >= nchunks) break;
+        reg_fence<CC>(r1);
+        if (ch + 4 < nchunks) tmem_ld_chunk<CC>(trow + (ch + 4) * CC, r0, skip_ld);
+        emit(r1, ch + 2);
+        tmem_ld_wait();
+        if (ch + 4 < nchunks) reg_fence<CC>(r0);
       }
       tc_fence_before();
       mbar_arrive(bar_tempty + 8 * acc);
     }
+    if (tma_store && lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -385,8 +467,10 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     if (S.has_res[b]) a.res_mask |= 1u << b;
     a.amin[b] = S.amin[b];
   }
-  const int U = S.U;
-  a.box_bytes = 2 * U * S.lbo_a;
+  const int Q = S.Q;
+  a.box_bytes = Q * S.lbo_a;
+  a.shift_box_bytes = S.need_shift ? S.lbo_a : 0;
+  a.shift_off = Q * S.lbo_a;
   a.region_bytes = S.region_bytes;
   a.stages = S.stages;
   a.stage_bytes = S.stage_bytes;
@@ -425,8 +509,8 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   a.tmem_cols = 2 * a.acc_stride;
   a.epi_flags = static_cast<int>(epilogue);
   // shared-memory carve-up (offsets from the 1024-aligned base)
-  a.off_stg = 1024;                      // 8 epilogue warps x 2 KB staging
-  a.off_a = a.off_stg + kStagingBytes;
+  a.off_stg = 1024;                      // 8 epilogue warps x 2 KB staging (TMA-store epilogue)
+  a.off_a = a.off_stg + ((epilogue & 0x1000u) ? 8 * 2048 : 0);
   a.off_b = a.off_a + a.stages * a.stage_bytes + kTileM * 16;
   a.off_b = (a.off_b + 127) / 128 * 128;
   a.off_bias = a.off_b + S.b_smem_bytes;
@@ -444,21 +528,44 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     if (!S.has_res[b]) continue;
     const cuuint64_t rows_b = static_cast<cuuint64_t>((d.h - b + S.s - 1) / S.s);
     cuuint64_t gdim[5] = {static_cast<cuuint64_t>(16 / es), static_cast<cuuint64_t>(p.wf), rows_b,
-                          static_cast<cuuint64_t>(2 * U), static_cast<cuuint64_t>(d.n)};
+                          static_cast<cuuint64_t>(Q), static_cast<cuuint64_t>(d.n)};
     cuuint64_t gstr[4] = {pix, rowpitch * S.s, 16, rowpitch * d.h};
     cuuint32_t box[5] = {static_cast<cuuint32_t>(16 / es), static_cast<cuuint32_t>(p.wbox),
-                         static_cast<cuuint32_t>(p.nrows), static_cast<cuuint32_t>(2 * U), 1};
+                         static_cast<cuuint32_t>(p.nrows), static_cast<cuuint32_t>(Q), 1};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     void* gaddr = const_cast<uint8_t*>(static_cast<const uint8_t*>(x) + b * rowpitch);
     CUresult r = encode(&maps.in[b], tmap_type(in_t), 5, gaddr, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS && S.need_shift) {
+      box[3] = 1;  // core column 0 only
+      r = encode(&maps.in_shift[b], tmap_type(in_t), 5, gaddr, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (r != CUDA_SUCCESS) {
       *err = "cuTensorMapEncodeTiled(input) failed: " + std::to_string(static_cast<int>(r));
       return WF_CUDA_ERROR;
     }
   }
 
+  if (epilogue & 0x1000u) {
+    // per-warp store box: 32 M rows = (32/Wbox output rows) x Wbox folded columns,
+    // columns >= Wfo and rows >= OH clipped by the tensor extent
+    const cuuint64_t cf = static_cast<cuuint64_t>(p.cout_f);
+    cuuint64_t gdim[4] = {cf, static_cast<cuuint64_t>(p.wfo), static_cast<cuuint64_t>(p.oh),
+                          static_cast<cuuint64_t>(d.n)};
+    cuuint64_t gstr[3] = {cf * oes, static_cast<cuuint64_t>(p.wfo) * cf * oes,
+                          static_cast<cuuint64_t>(p.oh) * p.wfo * cf * oes};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(CC), static_cast<cuuint32_t>(p.wbox <= 32 ? p.wbox : 32),
+                         static_cast<cuuint32_t>(p.wbox <= 32 ? 32 / p.wbox : 1), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(&maps.out, tmap_type(out_dtype), 4, y, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "cuTensorMapEncodeTiled(output) failed: " + std::to_string(static_cast<int>(r));
+      return WF_CUDA_ERROR;
+    }
+  }
   const int grid = a.n_tiles * a.ctas_per_ntile;
   cudaError_t e;
   const bool tf32 = (in_t == WF_TF32);

@@ -54,11 +54,11 @@ __global__ void pack_b_kernel(const T* __restrict__ w, uint8_t* __restrict__ pac
     const int e8 = rem - nrow * half;
     const uint4 e = reinterpret_cast<const uint4*>(packed)[ei];
     const int kh = e.z & 0xff;
-    const int u = (e.z >> 8) & 0xff;
+    const int c0col = (e.z >> 8) & 0xff;  // first core column of the pair
     const int g = (e.z >> 16) & 0x7fff;
     int nt = 0;
     while (nt + 1 < a.n_tiles && ei >= a.nt_entry0[nt + 1]) ++nt;
-    const int widx = u * a.E + cc * half + e8;  // element of the KW'*f*C window row
+    const int widx = (c0col + cc) * half + e8;  // element of the KW'*f*C window row
     const int kp = widx / (a.f * a.C);
     const int r2 = widx - kp * a.f * a.C;
     const int fi = r2 / a.C;

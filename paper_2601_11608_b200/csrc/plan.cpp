@@ -82,11 +82,11 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   // ---- fold factor ------------------------------------------------------
   int64_t f = f_req;
   if (f == 0) {
-    // smallest f: multiple of the W stride, 32-byte folded pixel, divides W,
+    // smallest f: multiple of the W stride, 16-byte folded pixel, divides W,
     // r*Cout groupable (the auto rule of choose_fold_factor, src/fold.cpp:67-90,
     // with the tcgen05 K-step as the alignment target).
     const int64_t pix = d.c * S.esize;
-    const int64_t base_align = 32 / std::gcd<int64_t>(pix, 32);
+    const int64_t base_align = 16 / std::gcd<int64_t>(pix, 16);
     const int64_t base = std::lcm<int64_t>(base_align, sw);
     wf_fold_plan first{};
     bool have = false;
@@ -113,7 +113,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   }
   if (d.w % f != 0) { S.plan = fallback(WF_REASON_WIDTH_NOT_DIVISIBLE, f); *out = S; return WF_OK; }
   if (f % sw != 0) { S.plan = fallback(WF_REASON_STRIDE_ON_FOLD_AXIS, f); *out = S; return WF_OK; }
-  if ((f * d.c * S.esize) % 32 != 0) { S.plan = fallback(WF_REASON_UNALIGNED_PIXEL, f); *out = S; return WF_OK; }
+  if ((f * d.c * S.esize) % 16 != 0) { S.plan = fallback(WF_REASON_UNALIGNED_PIXEL, f); *out = S; return WF_OK; }
   const int64_t r = f / sw;
   if (OW % r != 0) { S.plan = fallback(WF_REASON_OUTPUT_TAIL, f); *out = S; return WF_OK; }
   if (d.h < sh) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
@@ -121,14 +121,15 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   const int64_t c0 = -ceil_div(d.pad_w, f);
   const int64_t kwf = floor_div(f - sw - d.pad_w + d.kw - 1, f) - c0 + 1;
   const int64_t Wf = d.w / f, Wfo = OW / r;
-  const int64_t U = f * d.c * S.esize / 32;
-  S.U = static_cast<int>(U);
+  const int64_t Q = f * d.c * S.esize / 16;  // core columns per folded pixel
+  S.Q = static_cast<int>(Q);
+  const int64_t E2 = S.E / 2;                  // elements per core column
   // Folded columns per output row in the A layout: >= Wfo + KW' - 1 and a
   // divisor or multiple of 32, so each epilogue warp (32 TMEM lanes) owns whole
   // output rows (Wbox <= 32) or a 32-column slice of one (Wbox >= 32).
   int64_t Wbox = 1;
   while (Wbox < Wfo + kwf - 1) Wbox *= 2;
-  if (Wbox > kTileM || U * 2 > 256) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
+  if (Wbox > kTileM || Q + 1 > 256) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
   // Never shrunk to OH: rows past OH are zero-filled on load and clipped on store.
   const int64_t OHt = kTileM / Wbox;
 
@@ -146,10 +147,10 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   int64_t NR = 0;
   for (int b = 0; b < sh; ++b)
     if (S.has_res[b]) NR = std::max<int64_t>(NR, OHt + S.amax[b] - S.amin[b]);
+  // every core-column region (and the shifted one) must start 128-byte aligned
+  // for the TMA destination: pad rows so NR*Wbox*16 % 128 == 0
+  while ((NR * Wbox) % 8 != 0) ++NR;
   if (NR > 256) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
-  S.lbo_a = static_cast<int>(NR * Wbox * 16);
-  S.region_bytes = static_cast<int>(((2 * U * S.lbo_a) + 127) / 128 * 128);
-  S.stage_bytes = static_cast<int>(sh) * S.region_bytes;
 
   // ---- MMA groups ---------------------------------------------------------
   int64_t gs = gs_req;
@@ -175,12 +176,21 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
     hi[g] = -1;
     for (int64_t j = g * gs; j < (g + 1) * gs; ++j) {
       const int64_t off = ((-c0) * f + j * sw - d.pad_w) * d.c;
-      lo[g] = std::min(lo[g], off / S.E);
-      hi[g] = std::max(hi[g], (off + d.kw * d.c - 1) / S.E);
+      lo[g] = std::min(lo[g], off / E2);
+      hi[g] = std::max(hi[g], (off + d.kw * d.c - 1) / E2);
     }
   }
+  // units of group g start at core columns lo, lo+2, ... (pairs (c, c+1))
+  auto n_units = [&](int64_t g) { return (hi[g] - lo[g] + 2) / 2; };
+  S.need_shift = false;
+  for (int64_t g = 0; g < G; ++g)
+    for (int64_t i = 0; i < n_units(g); ++i)
+      if ((lo[g] + 2 * i) % Q == Q - 1) S.need_shift = true;
+  S.lbo_a = static_cast<int>(NR * Wbox * 16);
+  S.region_bytes = static_cast<int>((((Q + (S.need_shift ? 1 : 0)) * S.lbo_a) + 127) / 128 * 128);
+  S.stage_bytes = static_cast<int>(sh) * S.region_bytes;
   const int64_t block_bytes = static_cast<int64_t>(S.Ng) * 32;  // 2 core cols x Ng rows x 16 B
-  auto group_b_bytes = [&](int64_t g) { return d.kh * (hi[g] - lo[g] + 1) * block_bytes; };
+  auto group_b_bytes = [&](int64_t g) { return d.kh * n_units(g) * block_bytes; };
 
   // ---- N-tiles and shared-memory budget ------------------------------------
   const int ctrl_bytes = 1024;
@@ -217,7 +227,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
     for (auto& t : S.ntiles) {
       max_b = std::max(max_b, t.b_bytes);
       int64_t e = 0;
-      for (int gg = t.g0; gg < t.g1; ++gg) e += d.kh * (hi[gg] - lo[gg] + 1);
+      for (int gg = t.g0; gg < t.g1; ++gg) e += d.kh * n_units(gg);
       max_entries = std::max(max_entries, e);
     }
     const int64_t table_b = max_entries * 16;
@@ -255,17 +265,17 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
       // Interleave groups: consecutive MMAs accumulate into different TMEM
       // columns, so they pipeline instead of serialising on one accumulator.
       int64_t steps = 0;
-      for (int gg = t.g0; gg < t.g1; ++gg) steps = std::max<int64_t>(steps, hi[gg] - lo[gg] + 1);
+      for (int gg = t.g0; gg < t.g1; ++gg) steps = std::max<int64_t>(steps, n_units(gg));
       for (int64_t step = 0; step < steps; ++step)
       for (int gg = t.g0; gg < t.g1; ++gg) {
-        if (step > hi[gg] - lo[gg]) continue;
+        if (step >= n_units(gg)) continue;
         {
-          const int64_t u = lo[gg] + step;
-          const int64_t kp = u / U, uq = u % U;
+          const int64_t u = lo[gg] + 2 * step;  // first core column of the pair
+          const int64_t kp = u / Q, q = u % Q;
           MmaEntry e{};
           e.a_off = static_cast<uint32_t>(b * S.region_bytes +
                                           ((a - S.amin[b]) * Wbox + kp) * 16 +
-                                          2 * uq * S.lbo_a);
+                                          q * S.lbo_a);
           e.b_off = boff;
           boff += static_cast<uint32_t>(block_bytes);
           const bool acc = !(kh == 0 && u == lo[gg]);
@@ -297,7 +307,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   p.ow = OW;
   p.wf = Wf;
   p.wfo = Wfo;
-  p.units_per_px = U;
+  p.units_per_px = Q;
   p.group_size = gs;
   p.n_groups = G;
   p.n_tiles = static_cast<int64_t>(S.ntiles.size());

@@ -22,10 +22,14 @@
 // so every (kh, kw') view is the same buffer at a 16-byte-aligned row shift
 // (descriptor start address), i.e. each input byte is fetched once per tile.
 //
-// K is cut into 32-byte "units" (one MMA K-step: 16 bf16/fp16 or 8 tf32) that
-// never straddle a folded pixel (f*C*elem % 32 == 0). Output columns are split
-// into groups of `group_size` sub-columns j; group g issues only the units its
-// windows touch -- the tensor-core analogue of grouped_conv
+// K is cut into 32-byte MMA K-steps ("units": 16 bf16/fp16 or 8 tf32) made of
+// two 16-byte core columns; a unit may start at ANY core column c of the
+// window row (pixel kp = c / Q, column q = c % Q, Q = f*C*elem/16). The pair
+// (Q-1, Q) straddles into the next folded pixel: region Q of the A tile is a
+// second TMA box holding core column 0 loaded one folded column further, so
+// every pair is (region q, region q+1) at the same row shift. Output columns
+// are split into groups of `group_size` sub-columns j; group g issues only the
+// units its windows touch -- the tensor-core analogue of grouped_conv
 // (src/blockdiag.cpp:138-187), which skips the structural zeros of the
 // block-diagonal expansion.
 #pragma once
@@ -48,7 +52,7 @@ constexpr int kStagingBytes = 0;  // epilogue writes straight from registers (no
 struct MmaEntry {          // 16 bytes, lives in the packed buffer and in smem
   uint32_t a_off;          // byte offset of the A view inside an A stage
   uint32_t b_off;          // byte offset of the B block inside the N-tile's B
-  uint32_t meta;           // kh | u << 8 | g << 16 | accumulate << 31
+  uint32_t meta;           // kh | c << 8 | g << 16 | accumulate << 31 (c: first core column)
   uint32_t tmem_col;       // accumulator column of the group
 };
 
@@ -64,7 +68,8 @@ struct Schedule {
   int s = 1, ph = 0, pw = 0;
   int esize = 2;                 // input element bytes
   int E = 16;                    // elements per 32-byte unit
-  int U = 1;                     // units per folded pixel
+  int Q = 2;                     // 16-byte core columns per folded pixel
+  bool need_shift = false;       // some unit pairs (Q-1, next pixel's 0)
   int Ng = 64;                   // accumulator columns per group
   int amin[kMaxResidues] = {0};
   int amax[kMaxResidues] = {0};

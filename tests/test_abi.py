@@ -45,7 +45,7 @@ def test_plan_is_deterministic_and_packed_size_positive():
     p1 = A.plan_fold(d, 0, 0, A.WF_BF16)
     p2 = A.plan_fold(d, 0, 0, A.WF_BF16)
     assert bytes(p1) == bytes(p2)
-    assert p1.status == A.WF_FOLD_APPLY and p1.f == 16 and p1.r == 8
+    assert p1.status == A.WF_FOLD_APPLY and p1.f == 8 and p1.r == 4
     assert A.lib().wf_packed_filter_bytes(p1) == p1.packed_bytes > 0
     assert p1.table_bytes % 128 == 0
 

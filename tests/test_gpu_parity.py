@@ -130,7 +130,6 @@ def test_packed_operand_unpacks_to_the_expansion(oracle):
     table_bytes = (n_ent * 16 + 127) // 128 * 128
     Ng = gs * Co
     block = Ng * 32
-    E = 16
     base = table_bytes
     last_end = 0
     checked = 0
@@ -138,11 +137,11 @@ def test_packed_operand_unpacks_to_the_expansion(oracle):
         if i > 0 and b_off == 0:  # B offsets restart at each N-tile
             base += last_end
         last_end = int(b_off) + block
-        kh, u, g = meta & 0xFF, (meta >> 8) & 0xFF, (meta >> 16) & 0x7FFF
+        kh, c, g = meta & 0xFF, (meta >> 8) & 0xFF, (meta >> 16) & 0x7FFF  # c: first 16-byte core column
         blk = raw[base + b_off: base + b_off + block].view(np.uint16).reshape(2, Ng, 8)
         vals = (blk.astype(np.uint32) << 16).view(np.float32)
         for cc in range(2):
-            widx = u * E + cc * 8 + np.arange(8)
+            widx = (c + cc) * 8 + np.arange(8)
             kp, k = widx // (f * C), widx % (f * C)
             for nrow in range(0, Ng, 7):
                 n = g * Ng + nrow
@@ -198,7 +197,7 @@ def test_full_size_sampled_images(oracle):
 
 def test_tf32_path_within_1e3(golden_configs):
     y, ref, dt, conv = _config_run(golden_configs, "r50_b1", "")
-    assert dt == "f32" and conv.device_plan["f"] == 8
+    assert dt == "f32" and conv.device_plan["f"] % 2 == 0  # fold factor multiple of the stride
     assert normrel(y, ref) <= 1e-3
     y2 = wf.conv2d(golden_configs["r50_b1_x"], golden_configs["r50_b1_w"], 2, 2, padding=3,
                    bias=golden_configs["r50_b1_b"], precision="tf32")

@@ -82,7 +82,7 @@ def test_device_plans_for_configs(name, oracle):
     assert plan["status"] == "apply", plan
     d = plan["device"]
     esize = 4 if dt == "tf32" else 2
-    assert d["f"] % s == 0 and (d["f"] * 3 * esize) % 32 == 0
+    assert d["f"] % s == 0 and (d["f"] * 3 * esize) % 16 == 0
     r, c0, kwf = oracle.fold_geometry(d["f"], s, p, filt[1])
     assert (d["r"], d["c0"], d["kw_f"]) == (r, c0, kwf)
     assert plan["expanded_filter_shape"] == [filt[0], kwf, d["f"] * 3, r * filt[3]]
@@ -102,7 +102,7 @@ def test_alexnet_plan_reports_reason():
 def test_generalized_legality_reasons():
     assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=16)["reason"] == "WidthNotDivisible"
     assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], 2, 3, factor=16)["reason"] == "StrideOnFoldAxis"
-    assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], factor=8)["reason"] == "UnalignedPixel"
+    assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], factor=4)["reason"] == "UnalignedPixel"
     with pytest.raises(wf.ShapeMismatchError):
         wf.plan_fold([1, 32, 32, 3], [3, 3, 4, 16])
 

@@ -14,7 +14,7 @@ import pytest
 from tests.conftest import ROOT
 
 CONFIG_GEOM = {  # name -> fold factor the device uses (f % stride == 0, 32-byte folded pixel)
-    "r50_b1": 8, "vgg16": 16, "alexnet": 16, "mnv2": 16, "r50_b8192": 16,
+    "r50_b1": 4, "vgg16": 8, "alexnet": 8, "mnv2": 8, "r50_b8192": 8,
 }
 
 

@@ -2,7 +2,7 @@
 import sys
 import torch
 sys.path.insert(0, ".")
-from paper_2601_11608_b200 import ops
+import paper_2601_11608_b200 as wf
 
 CFG = {  # n, h, w, c, kh, kw, cout, s, p, dtype, relu
     "r50": (8192, 224, 224, 3, 7, 7, 64, 2, 3, torch.bfloat16, False),
@@ -18,15 +18,15 @@ gs = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 x = torch.randn(n, h, w_, c, device="cuda").to(dt)
 w = (torch.randn(kh, kw, c, cout, device="cuda") * 0.1).to(dt)
 b = torch.randn(cout, device="cuda")
-ff = ops.prepare_filter(w, b, x.shape, (s, s), (p, p), fold=f, group_size=gs)
-y = ops.conv_folded(x, ff, relu=relu)
+ff = wf.FoldedConv2d(w, b, x.shape, stride=s, padding=p, fold=f, group_size=gs)
+y = ff(x, relu=relu)
 iters = int(sys.argv[5]) if len(sys.argv) > 5 else 3
 flags = int(sys.argv[6], 0) if len(sys.argv) > 6 else 0
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize(); e0.record()
 for _ in range(iters):
-    ops.conv_folded(x, ff, relu=relu, out=y, _profile_flags=flags)
+    ff(x, relu=relu, out=y, _profile_flags=flags)
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / iters
-print(f"{name} flags={flags:#x} n={n} f={ff.plan.f} gs={ff.plan.group_size} nt={ff.plan.n_tiles}: {ms:.3f} ms {n/ms*1e3:.0f} img/s "
+print(f"{name} flags={flags:#x} n={n} f={ff.device_plan["f"]} gs={ff.device_plan["group_size"]} nt={ff.device_plan["n_tiles"]}: {ms:.3f} ms {n/ms*1e3:.0f} img/s "
       f"{(x.numel()*x.element_size()+y.numel()*y.element_size())/ms/1e6:.0f} GB/s")
