@@ -105,6 +105,9 @@ typedef struct {
   int64_t mma_entries;     /* tcgen05.mma instructions per M tile (all N-tiles) */
   int64_t table_bytes;     /* schedule table size inside the packed buffer */
   int64_t packed_bytes;    /* = wf_packed_filter_bytes */
+  int64_t epi_chunk;       /* accumulator columns per epilogue chunk: the period
+                              of the output-column permutation baked into the
+                              packed filter (coalesced 16x256b TMEM reads) */
   uint64_t useful_macs;    /* count_macs of the original conv */
   uint64_t issued_macs;    /* MACs the tensor cores execute (128-row tiles) */
 } wf_fold_plan;

@@ -24,7 +24,7 @@ wf_status fail(wf_status st, const std::string& msg) {
 
 extern "C" {
 
-int wf_abi_version(void) { return 1; }
+int wf_abi_version(void) { return 2; }
 
 const char* wf_last_error(void) { return g_last_error.c_str(); }
 
@@ -74,7 +74,7 @@ wf_status wf_conv_fold_fwd(const void* x, const void* w_packed, const float* b_r
                            const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype, uint32_t epilogue,
                            void* stream) {
   if (!x || !w_packed || !y || !desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
-  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0x1F00))  // 0x1F00: profiling / epilogue-mode switches
+  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0x3F00))  // 0x3F00: profiling / epilogue-mode switches
     return fail(WF_INVALID_ARGUMENT, "unknown epilogue flags");
   wfb::Schedule S;
   std::string err;

@@ -52,7 +52,7 @@ struct ConvArgs {
   unsigned idesc;
   unsigned acc_stride, tmem_cols;
   int epi_flags;
-  int off_stg, off_a, off_b, off_bias;
+  int off_a, off_b, off_bias;
   // schedule: x = (a_off>>4) | (lbo_a>>4)<<16, y = (b_off>>4) | (lbo_b>>4)<<16,
   // z = accumulate flag (bit 31), w = accumulator column
   uint4 table[kMaxTable];
@@ -61,7 +61,6 @@ struct ConvArgs {
 struct TmaMaps {
   CUtensorMap in[kMaxResidues];
   CUtensorMap in_shift[kMaxResidues];  // core column 0 one folded column further (region Q)
-  CUtensorMap out;  // per-warp store box (TMA-store epilogue)
 };
 
 template <typename OutT>
@@ -77,78 +76,42 @@ __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int CC>
-__device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, uint32_t (&r)[CC], bool skip = false) {
+// tcgen05.ld.16x256b with NREG/4 repetitions: 16 TMEM lanes x (NREG/2) columns.
+template <int NREG>
+__device__ __forceinline__ void tmem_ld_16x256b(uint32_t taddr, uint32_t (&r)[NREG], bool skip = false) {
   if (skip) {
 #pragma unroll
-    for (int k = 0; k < CC; ++k) r[k] = taddr + k;  // profiling: no TMEM traffic
+    for (int k = 0; k < NREG; ++k) r[k] = taddr + k;  // profiling: no TMEM traffic
     return;
   }
-  if constexpr (CC == 32) ptx::tmem_ld32(taddr, r); else ptx::tmem_ld16(taddr, r);
+  if constexpr (NREG == 32) ptx::tmem_ld_16x256b_x8(taddr, r); else ptx::tmem_ld_16x256b_x4(taddr, r);
 }
 
-// +bias (vectorised broadcast loads from smem) -> ReLU -> convert -> two 256-bit
-// stores of this thread's 64-byte row segment.
-template <typename OutT, int CC>
-__device__ __forceinline__ void epi_store_chunk(const uint32_t (&r)[CC], const float* sb, bool relu, bool valid,
-                                                uint8_t* dst) {
-  float v[CC];
+// VPT consecutive output channels of one row -> global, 32-byte stores.
+template <typename OutT, int VPT>
+__device__ __forceinline__ void store_row(uint8_t* dst, const float (&v)[VPT]) {
+  if constexpr (sizeof(OutT) == 4) {
+    static_assert(VPT % 8 == 0, "fp32 rows are stored 8 values at a time");
 #pragma unroll
-  for (int k = 0; k < CC; k += 4) {
-    const float4 bb = *reinterpret_cast<const float4*>(sb + k);
-    v[k + 0] = __uint_as_float(r[k + 0]) + bb.x;
-    v[k + 1] = __uint_as_float(r[k + 1]) + bb.y;
-    v[k + 2] = __uint_as_float(r[k + 2]) + bb.z;
-    v[k + 3] = __uint_as_float(r[k + 3]) + bb.w;
-  }
-  if (relu) {
+    for (int q = 0; q < VPT / 8; ++q) {
+      uint32_t pk[8];
 #pragma unroll
-    for (int k = 0; k < CC; ++k) v[k] = (v[k] < 0.0f) ? 0.0f : v[k];
-  }
-  uint32_t pk[16];
+      for (int k = 0; k < 8; ++k) pk[k] = __float_as_uint(v[8 * q + k]);
+      ptx::st_global_v8(dst + 32 * q, pk);
+    }
+  } else if constexpr (VPT == 16) {
+    uint32_t pk[8];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    if constexpr (sizeof(OutT) == 4) pk[k] = __float_as_uint(v[k]);
-    else pk[k] = pack2<OutT>(v[2 * k], v[2 * k + 1]);
-  }
-  if (valid) {
+    for (int k = 0; k < 8; ++k) pk[k] = pack2<OutT>(v[2 * k], v[2 * k + 1]);
     ptx::st_global_v8(dst, pk);
-    ptx::st_global_v8(dst + 32, pk + 8);
+  } else {
+    static_assert(VPT == 8, "2-byte rows are 8 or 16 values");
+    ptx::st_global_v4(dst, make_uint4(pack2<OutT>(v[0], v[1]), pack2<OutT>(v[2], v[3]), pack2<OutT>(v[4], v[5]),
+                                      pack2<OutT>(v[6], v[7])));
   }
 }
 
-// Same math, but the 64-byte row segment goes to this warp's 64B-swizzled
-// staging buffer (row = lane); the warp then TMA-stores the whole box.
-template <typename OutT, int CC>
-__device__ __forceinline__ void epi_stage_chunk(const uint32_t (&r)[CC], const float* sb, bool relu, uint32_t stg,
-                                                uint32_t lane) {
-  float v[CC];
-#pragma unroll
-  for (int k = 0; k < CC; k += 4) {
-    const float4 bb = *reinterpret_cast<const float4*>(sb + k);
-    v[k + 0] = __uint_as_float(r[k + 0]) + bb.x;
-    v[k + 1] = __uint_as_float(r[k + 1]) + bb.y;
-    v[k + 2] = __uint_as_float(r[k + 2]) + bb.z;
-    v[k + 3] = __uint_as_float(r[k + 3]) + bb.w;
-  }
-  if (relu) {
-#pragma unroll
-    for (int k = 0; k < CC; ++k) v[k] = (v[k] < 0.0f) ? 0.0f : v[k];
-  }
-  uint32_t pk[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    if constexpr (sizeof(OutT) == 4) pk[k] = __float_as_uint(v[k]);
-    else pk[k] = pack2<OutT>(v[2 * k], v[2 * k + 1]);
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint32_t lin = lane * 64u + q * 16u;
-    ptx::st_shared_v4(stg + (lin ^ (((lin >> 7) & 3u) << 4)), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-  }
-}
-
-template <int kKind, typename OutT>
+template <int kKind, typename OutT, int CH>
 __global__ void __launch_bounds__(320, 1)
     conv_fold_kernel(const __grid_constant__ ConvArgs a, const __grid_constant__ TmaMaps maps) {
   using namespace ptx;
@@ -277,84 +240,104 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else {
     // ===================== epilogue (warps 2..9) =====================
-    // Warp w owns TMEM lanes [32q, 32q+32), q = w % 4 -- M rows m = 32q + lane,
-    // one output row segment per thread -- and every other 64-byte column chunk
-    // (half = 0 for warps 2..5, 1 for warps 6..9). Per chunk: tcgen05.ld ->
-    // +bias -> ReLU -> convert -> two 256-bit stores (full 32-byte sectors)
-    // straight to the final NHWC row; no shared-memory staging.
-    constexpr int CC = 64 / static_cast<int>(sizeof(OutT));  // columns per chunk
+    // Warp w owns TMEM lanes [32q, 32q+32), q = w % 4, and every other
+    // CH-column chunk (half = 0 for warps 2..5, 1 for warps 6..9). Per chunk
+    // and 16-lane half: tcgen05.ld.16x256b -> +bias (registers) -> ReLU ->
+    // convert -> one 32-byte store per row. The packed filter permuted the
+    // accumulator columns (chunk_perm, plan.hpp) so thread t holds CH/4
+    // consecutive output channels of rows t/4 and t/4+8: the 4 threads of a
+    // row write whole 128-byte lines, 8 rows per store instruction.
+    constexpr int VPT = CH / 4;    // consecutive output channels per thread and row
+    constexpr int NREG = CH / 2;   // registers per 16x256b load (two rows)
+    constexpr int CPW = 128 / CH;  // chunks per warp at the maximum N-tile width (256)
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
-    const int nchunks = ncols / CC;
+    const int nchunks = ncols / CH;
+    const int nc_w = (nchunks > half) ? (nchunks - half + 1) / 2 : 0;  // this warp's chunks
+    const int n_it = 2 * nc_w;                                          // x two 16-lane halves
+    const int k4 = lane & 3;
     const bool relu = (a.epi_flags & WF_EPI_RELU) != 0;
     const bool dbg_skip_epi = (a.epi_flags & 0x200) != 0;
     const bool dbg_skip_store = (a.epi_flags & 0x400) != 0;
     const bool skip_ld = (a.epi_flags & 0x800) != 0;
-    const bool tma_store = (a.epi_flags & 0x1000) != 0;
-    const uint32_t stg = base + a.off_stg + static_cast<uint32_t>(warp - 2) * 2048u;
-    const int t_first = (a.Wbox <= 32) ? (quarter * 32) / a.Wbox : (quarter * 32) / a.Wbox;
-    const int w_first = (a.Wbox <= 32) ? 0 : (quarter * 32) % a.Wbox;
     const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
-    const int m = quarter * 32 + lane;
-    const int t = m / a.Wbox;
-    const int wq = m - t * a.Wbox;
-    int it = 0;
-    for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_round = static_cast<uint32_t>(it >> 1);
+    float breg[CPW][VPT];
+#pragma unroll
+    for (int cc = 0; cc < CPW; ++cc) {
+      const int c = half + 2 * cc;
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) breg[cc][v] = (c < nchunks) ? sbias[c * CH + VPT * k4 + v] : 0.0f;
+    }
+    // the four M rows this thread stores: (16-lane half h16, row group r8)
+    int row_t[2][2], row_w[2][2];
+#pragma unroll
+    for (int h16 = 0; h16 < 2; ++h16)
+#pragma unroll
+      for (int r8 = 0; r8 < 2; ++r8) {
+        const int m = quarter * 32 + h16 * 16 + r8 * 8 + (lane >> 2);
+        row_t[h16][r8] = m / a.Wbox;
+        row_w[h16][r8] = m - row_t[h16][r8] * a.Wbox;
+      }
+    const long long col_bytes = static_cast<long long>(col0 + VPT * k4) * sizeof(OutT);
+    int it_tile = 0;
+    for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it_tile) {
+      const int acc = it_tile & 1;
+      const uint32_t acc_round = static_cast<uint32_t>(it_tile >> 1);
       const int n = mt / a.ohb;
       const int oh0 = (mt - n * a.ohb) * a.OHt;
       mbar_wait(bar_tfull + 8 * acc, acc_round & 1u);
       tc_fence_after();
-      if (dbg_skip_epi || half >= nchunks) {
+      if (dbg_skip_epi || n_it == 0) {
         tc_fence_before();
         mbar_arrive(bar_tempty + 8 * acc);
         continue;
       }
-      const int oh = oh0 + t;
-      const bool valid = (wq < a.Wfo) && (t < a.OHt) && (oh < a.OH) && !dbg_skip_store;
-      uint8_t* grow = a.out + ((static_cast<long long>(n) * a.OH + oh) * a.Wfo + wq) * a.row_bytes +
-                      static_cast<long long>(col0) * sizeof(OutT);
-      const uint32_t trow = tmem_base + acc * a.acc_stride + (static_cast<uint32_t>(quarter * 32) << 16);
-      // Two register sets so the TMEM load of the next chunk overlaps this
-      // chunk's convert + store; the loop is unrolled by two so the set
-      // selection is static.
-      uint32_t r0[CC], r1[CC];
-      tmem_ld_chunk<CC>(trow + half * CC, r0, skip_ld);
-      tmem_ld_wait();
-      reg_fence<CC>(r0);
-      // chunk store: direct 256-bit st.global (default) or per-warp TMA box store
-      auto emit = [&](const uint32_t (&rr)[CC], int c) {
-        if (tma_store) {
-          if (lane == 0) bulk_wait_read_0();  // staging buffer free again
-          __syncwarp();
-          epi_stage_chunk<OutT, CC>(rr, sbias + c * CC, relu, stg, static_cast<uint32_t>(lane));
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0 && !dbg_skip_store) {
-            tma_store_4d(&maps.out, stg, col0 + c * CC, w_first, oh0 + t_first, n);
-            bulk_commit();
-          }
-        } else {
-          epi_store_chunk<OutT, CC>(rr, sbias + c * CC, relu, valid, grow + c * 64);
+      uint8_t* rowp[2][2];
+      bool rowv[2][2];
+#pragma unroll
+      for (int h16 = 0; h16 < 2; ++h16)
+#pragma unroll
+        for (int r8 = 0; r8 < 2; ++r8) {
+          const int t = row_t[h16][r8], wq = row_w[h16][r8];
+          const int oh = oh0 + t;
+          rowv[h16][r8] = (wq < a.Wfo) && (t < a.OHt) && (oh < a.OH) && !dbg_skip_store;
+          rowp[h16][r8] = a.out + ((static_cast<long long>(n) * a.OH + oh) * a.Wfo + wq) * a.row_bytes + col_bytes;
         }
+      const uint32_t tq = tmem_base + acc * a.acc_stride + (static_cast<uint32_t>(quarter * 32) << 16);
+      // iteration it: chunk cc = it / 2 (c = half + 2cc), 16-lane half h16 = it % 2
+      auto taddr = [&](int it) {
+        return tq + (static_cast<uint32_t>((it & 1) * 16) << 16) + static_cast<uint32_t>((half + 2 * (it >> 1)) * CH);
       };
-#pragma unroll 1
-      for (int ch = half; ch < nchunks; ch += 4) {
-        if (ch + 2 < nchunks) tmem_ld_chunk<CC>(trow + (ch + 2) * CC, r1, skip_ld);
-        emit(r0, ch);
+      uint32_t buf[2][NREG];
+      tmem_ld_16x256b<NREG>(taddr(0), buf[0], skip_ld);
+#pragma unroll
+      for (int it = 0; it < 2 * CPW; ++it) {
+        if (it >= n_it) break;
         tmem_ld_wait();
-        if (ch + 2 >= nchunks) break;
-        reg_fence<CC>(r1);
-        if (ch + 4 < nchunks) tmem_ld_chunk<CC>(trow + (ch + 4) * CC, r0, skip_ld);
-        emit(r1, ch + 2);
-        tmem_ld_wait();
-        if (ch + 4 < nchunks) reg_fence<CC>(r0);
+        reg_fence<NREG>(buf[it & 1]);
+        if (it + 1 < n_it) tmem_ld_16x256b<NREG>(taddr(it + 1), buf[(it + 1) & 1], skip_ld);
+        const int cc = it >> 1, h16 = it & 1;
+        const uint32_t(&r)[NREG] = buf[it & 1];
+        const long long coff = static_cast<long long>(2 * cc) * CH * sizeof(OutT);  // chunk c - half, in bytes
+        const long long hoff = static_cast<long long>(half) * CH * sizeof(OutT);
+#pragma unroll
+        for (int r8 = 0; r8 < 2; ++r8) {
+          float v[VPT];
+#pragma unroll
+          for (int i = 0; i < CH / 8; ++i) {
+            v[2 * i] = __uint_as_float(r[4 * i + 2 * r8]) + breg[cc][2 * i];
+            v[2 * i + 1] = __uint_as_float(r[4 * i + 2 * r8 + 1]) + breg[cc][2 * i + 1];
+          }
+          if (relu) {
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) v[k] = (v[k] < 0.0f) ? 0.0f : v[k];
+          }
+          if (rowv[h16][r8]) store_row<OutT, VPT>(rowp[h16][r8] + hoff + coff, v);
+        }
       }
       tc_fence_before();
       mbar_arrive(bar_tempty + 8 * acc);
     }
-    if (tma_store && lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -401,9 +384,9 @@ uint32_t pow2ceil(uint32_t v) {
   return p;
 }
 
-template <int kKind, typename OutT>
+template <int kKind, typename OutT, int CH>
 cudaError_t launch_typed(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st) {
-  auto kern = conv_fold_kernel<kKind, OutT>;
+  auto kern = conv_fold_kernel<kKind, OutT, CH>;
   static int configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -435,9 +418,8 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     return WF_INVALID_ARGUMENT;
   }
   const int oes = elem_bytes(out_dtype);
-  const int CC = 64 / oes;
   for (const auto& t : S.ntiles)
-    if (t.cols % CC != 0) {
+    if (t.cols % S.CH != 0) {
       *err = "N-tile width not a multiple of the epilogue chunk";
       return WF_UNSUPPORTED;
     }
@@ -509,8 +491,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   a.tmem_cols = 2 * a.acc_stride;
   a.epi_flags = static_cast<int>(epilogue);
   // shared-memory carve-up (offsets from the 1024-aligned base)
-  a.off_stg = 1024;                      // 8 epilogue warps x 2 KB staging (TMA-store epilogue)
-  a.off_a = a.off_stg + ((epilogue & 0x1000u) ? 8 * 2048 : 0);
+  a.off_a = 1024;
   a.off_b = a.off_a + a.stages * a.stage_bytes + kTileM * 16;
   a.off_b = (a.off_b + 127) / 128 * 128;
   a.off_bias = a.off_b + S.b_smem_bytes;
@@ -548,33 +529,25 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     }
   }
 
-  if (epilogue & 0x1000u) {
-    // per-warp store box: 32 M rows = (32/Wbox output rows) x Wbox folded columns,
-    // columns >= Wfo and rows >= OH clipped by the tensor extent
-    const cuuint64_t cf = static_cast<cuuint64_t>(p.cout_f);
-    cuuint64_t gdim[4] = {cf, static_cast<cuuint64_t>(p.wfo), static_cast<cuuint64_t>(p.oh),
-                          static_cast<cuuint64_t>(d.n)};
-    cuuint64_t gstr[3] = {cf * oes, static_cast<cuuint64_t>(p.wfo) * cf * oes,
-                          static_cast<cuuint64_t>(p.oh) * p.wfo * cf * oes};
-    cuuint32_t box[4] = {static_cast<cuuint32_t>(CC), static_cast<cuuint32_t>(p.wbox <= 32 ? p.wbox : 32),
-                         static_cast<cuuint32_t>(p.wbox <= 32 ? 32 / p.wbox : 1), 1};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = encode(&maps.out, tmap_type(out_dtype), 4, y, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      *err = "cuTensorMapEncodeTiled(output) failed: " + std::to_string(static_cast<int>(r));
-      return WF_CUDA_ERROR;
-    }
-  }
   const int grid = a.n_tiles * a.ctas_per_ntile;
   cudaError_t e;
   const bool tf32 = (in_t == WF_TF32);
+  if (tf32 && S.CH != 32) {
+    *err = "tf32 plans use 32-column epilogue chunks";
+    return WF_UNSUPPORTED;
+  }
   if (out_dtype == WF_BF16)
-    e = tf32 ? launch_typed<1, __nv_bfloat16>(a, maps, grid, smem, st) : launch_typed<0, __nv_bfloat16>(a, maps, grid, smem, st);
+    e = tf32 ? launch_typed<1, __nv_bfloat16, 32>(a, maps, grid, smem, st)
+             : (S.CH == 64 ? launch_typed<0, __nv_bfloat16, 64>(a, maps, grid, smem, st)
+                           : launch_typed<0, __nv_bfloat16, 32>(a, maps, grid, smem, st));
   else if (out_dtype == WF_F16)
-    e = tf32 ? launch_typed<1, __half>(a, maps, grid, smem, st) : launch_typed<0, __half>(a, maps, grid, smem, st);
+    e = tf32 ? launch_typed<1, __half, 32>(a, maps, grid, smem, st)
+             : (S.CH == 64 ? launch_typed<0, __half, 64>(a, maps, grid, smem, st)
+                           : launch_typed<0, __half, 32>(a, maps, grid, smem, st));
   else
-    e = tf32 ? launch_typed<1, float>(a, maps, grid, smem, st) : launch_typed<0, float>(a, maps, grid, smem, st);
+    e = tf32 ? launch_typed<1, float, 32>(a, maps, grid, smem, st)
+             : (S.CH == 64 ? launch_typed<0, float, 64>(a, maps, grid, smem, st)
+                           : launch_typed<0, float, 32>(a, maps, grid, smem, st));
   if (e != cudaSuccess) {
     *err = std::string("conv_fold_kernel launch failed: ") + cudaGetErrorString(e);
     return WF_CUDA_ERROR;

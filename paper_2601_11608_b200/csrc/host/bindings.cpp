@@ -45,7 +45,7 @@ py::dict raw_dict(const wf_fold_plan& p) {
   d["oh"] = p.oh; d["ow"] = p.ow; d["wf"] = p.wf; d["wfo"] = p.wfo; d["units_per_px"] = p.units_per_px;
   d["group_size"] = p.group_size; d["n_groups"] = p.n_groups; d["n_tiles"] = p.n_tiles;
   d["tile_rows"] = p.tile_rows; d["wbox"] = p.wbox; d["nrows"] = p.nrows; d["mma_entries"] = p.mma_entries;
-  d["packed_bytes"] = p.packed_bytes; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
+  d["packed_bytes"] = p.packed_bytes; d["epi_chunk"] = p.epi_chunk; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
   return d;
 }
 

@@ -23,7 +23,7 @@
 namespace wfb {
 
 struct PackArgs {
-  int KH, KW, C, Cout, f, s, pw, c0, gs, Ng, E, esize;
+  int KH, KW, C, Cout, f, s, pw, c0, gs, Ng, E, esize, CH;
   int entries;
   int n_tiles;
   int nt_entry0[kMaxNTiles];
@@ -63,8 +63,11 @@ __global__ void pack_b_kernel(const T* __restrict__ w, uint8_t* __restrict__ pac
     const int r2 = widx - kp * a.f * a.C;
     const int fi = r2 / a.C;
     const int c = r2 - fi * a.C;
-    const int j = g * a.gs + nrow / a.Cout;
-    const int co = nrow - (nrow / a.Cout) * a.Cout;
+    // accumulator column nrow of the group holds output column perm(nrow)
+    // (groups start on chunk boundaries, so the permutation stays inside)
+    const int ncol = chunk_perm(nrow, a.CH);
+    const int j = g * a.gs + ncol / a.Cout;
+    const int co = ncol - (ncol / a.Cout) * a.Cout;
     const int kw = (a.c0 + kp) * a.f + fi - j * a.s + a.pw;
     T val = T(0.0f);
     if (kw >= 0 && kw < a.KW) val = w[((static_cast<long long>(kh) * a.KW + kw) * a.C + c) * a.Cout + co];
@@ -130,6 +133,7 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
   a.Ng = S.Ng;
   a.E = S.E;
   a.esize = S.esize;
+  a.CH = S.CH;
   a.entries = static_cast<int>(S.entries.size());
   a.n_tiles = static_cast<int>(S.ntiles.size());
   for (int i = 0; i < a.n_tiles; ++i) {

@@ -157,19 +157,22 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   if (gs == 0) {
     int64_t best = 0;
     for (int64_t g = 1; g <= r; ++g) {
-      if (r % g || (g * d.cout) % 16 || g * d.cout > kMaxAccCols) continue;
+      if (r % g || (g * d.cout) % 32 || g * d.cout > kMaxAccCols) continue;
       if (best == 0 || (best * d.cout < 64)) best = g;
       if (best * d.cout >= 64) break;
     }
     gs = best;
   }
-  if (gs == 0 || r % gs || (gs * d.cout) % 16 || gs * d.cout > kMaxAccCols) {
+  if (gs == 0 || r % gs || (gs * d.cout) % 32 || gs * d.cout > kMaxAccCols) {
     S.plan = fallback(WF_REASON_UNSUPPORTED_CHANNELS, f);
     *out = S;
     return WF_OK;
   }
   const int64_t G = r / gs;
   S.Ng = static_cast<int>(gs * d.cout);
+  // 2-byte outputs: 64-column chunks (16 bf16 = 32 B per thread and row);
+  // tf32 (fp32 outputs): 32-column chunks (8 fp32 = 32 B).
+  S.CH = (in_dtype != WF_TF32 && S.Ng % 64 == 0) ? 64 : 32;
   std::vector<int64_t> lo(G), hi(G);
   for (int64_t g = 0; g < G; ++g) {
     lo[g] = INT64_MAX;
@@ -317,6 +320,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   p.mma_entries = static_cast<int64_t>(S.entries.size());
   p.table_bytes = (p.mma_entries * 16 + 127) / 128 * 128;
   p.packed_bytes = p.table_bytes + b_cursor;
+  p.epi_chunk = S.CH;
   S.ohb = ceil_div(OH, OHt);
   S.num_mtiles = d.n * S.ohb;
   p.useful_macs = static_cast<uint64_t>(d.n) * OH * OW * d.cout * d.kh * d.kw * d.c;

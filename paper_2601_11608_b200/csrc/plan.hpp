@@ -49,6 +49,22 @@ constexpr int kMaxNTiles = 16;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kStagingBytes = 0;  // epilogue writes straight from registers (no staging)
 
+// Output-column permutation inside an epilogue chunk of CH accumulator
+// columns. tcgen05.ld.16x256b hands thread t of a warp the columns
+// 8i + 2(t%4) + {0,1} (i = 0..CH/8-1) of TMEM lanes t/4 and t/4+8; the packed
+// filter puts output column (CH/4)*(t%4) + 2i + e of the chunk there, so each
+// thread holds CH/4 CONSECUTIVE output channels and the 4 threads of a row
+// cover CH contiguous channels: one full 128-byte line per row per store.
+#ifdef __CUDACC__
+#define WFB_HD __host__ __device__
+#else
+#define WFB_HD
+#endif
+WFB_HD inline int chunk_perm(int col, int CH) {
+  const int c = col / CH, w = col % CH;
+  return c * CH + (CH / 4) * ((w % 8) / 2) + 2 * (w / 8) + (w % 2);
+}
+
 struct MmaEntry {          // 16 bytes, lives in the packed buffer and in smem
   uint32_t a_off;          // byte offset of the A view inside an A stage
   uint32_t b_off;          // byte offset of the B block inside the N-tile's B
@@ -71,6 +87,7 @@ struct Schedule {
   int Q = 2;                     // 16-byte core columns per folded pixel
   bool need_shift = false;       // some unit pairs (Q-1, next pixel's 0)
   int Ng = 64;                   // accumulator columns per group
+  int CH = 64;                   // epilogue chunk (columns per 16x256b TMEM read)
   int amin[kMaxResidues] = {0};
   int amax[kMaxResidues] = {0};
   bool has_res[kMaxResidues] = {false};

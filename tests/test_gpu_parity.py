@@ -25,6 +25,12 @@ def normrel(y, ref):
     return float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30))
 
 
+def chunk_perm(col, ch):
+    """Accumulator column -> output column inside an epilogue chunk (plan.hpp chunk_perm)."""
+    c, w = divmod(col, ch)
+    return c * ch + (ch // 4) * ((w % 8) // 2) + 2 * (w // 8) + (w % 2)
+
+
 def cuda(a, dtype=torch.float32):
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(dtype)
 
@@ -144,7 +150,7 @@ def test_packed_operand_unpacks_to_the_expansion(oracle):
             widx = (c + cc) * 8 + np.arange(8)
             kp, k = widx // (f * C), widx % (f * C)
             for nrow in range(0, Ng, 7):
-                n = g * Ng + nrow
+                n = g * Ng + chunk_perm(nrow, d["epi_chunk"])
                 np.testing.assert_array_equal(vals[cc, nrow], wexp[kh, kp, k, n])
                 checked += 1
     assert checked > 100

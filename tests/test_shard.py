@@ -1,0 +1,73 @@
+"""Batch sharding on CPU: the partition, and the two
+out-of-band collectives (max of per-rank device time, verification gather)
+exercised with world_size 2 over gloo."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2601_11608_b200 import shard
+
+
+@pytest.mark.parametrize("n,world", [(8192, 1), (8192, 2), (8192, 8), (7, 3), (3, 8), (0, 2), (1000003, 8)])
+def test_shard_range_partitions_the_batch(n, world):
+    spans = [shard.shard_range(n, r, world) for r in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == n
+    for (a, b), (c, _) in zip(spans, spans[1:]):
+        assert b == c  # contiguous, no gap, no overlap
+    sizes = [b - a for a, b in spans]
+    assert max(sizes) - min(sizes) <= 1 and sum(sizes) == n
+
+
+def test_shard_range_rejects_bad_ranks():
+    for rank, world in ((0, 0), (2, 2), (-1, 4)):
+        with pytest.raises(ValueError):
+            shard.shard_range(16, rank, world)
+
+
+def test_single_process_collectives_are_identity():
+    assert shard.max_over_ranks(3.5) == 3.5
+    assert shard.gather_scalars([1.0, 2.0]) == [[1.0, 2.0]]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import torch.distributed as dist
+    r, local, w = shard.dist_env()
+    shard.init("gloo")
+    try:
+        lo, hi = shard.shard_range(8192, r, w)
+        ms = 10.0 + r  # per-rank "device time"
+        mx = shard.max_over_ranks(ms)
+        got = shard.gather_scalars([float(lo), float(hi), ms])
+        q.put((r, local, w, lo, hi, mx, got))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_shard_and_reduce():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    spans = [(lo, hi) for (_, _, _, lo, hi, _, _) in res]
+    assert spans == [(0, 4096), (4096, 8192)]
+    for (r, local, w, _, _, mx, got) in res:
+        assert w == 2 and local == r
+        assert mx == 11.0  # max over ranks, as bench.py times multi-GPU runs
+        assert got == [[0.0, 4096.0, 10.0], [4096.0, 8192.0, 11.0]]

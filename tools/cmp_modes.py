@@ -12,7 +12,8 @@ for (n, h, w, kh, co, s, p, dt, relu) in [(5, 224, 224, 7, 64, 2, 3, torch.bfloa
     b = torch.randn(co, device="cuda")
     conv = wf.FoldedConv2d(wt, b, x.shape, stride=s, padding=p, dtype=dt)
     y0 = conv(x, relu=relu)
-    y1 = torch.full_like(y0, float("nan"))
-    conv(x, relu=relu, out=y1, _profile_flags=0x1000)
-    torch.cuda.synchronize()
-    print(tuple(x.shape), dt, "identical" if torch.equal(y0, y1) else f"DIFF max {(y0.float()-y1.float()).abs().max().item()}")
+    for fl in (0x1000, 0x2000):
+        y1 = torch.full_like(y0, float("nan"))
+        conv(x, relu=relu, out=y1, _profile_flags=fl)
+        torch.cuda.synchronize()
+        print(tuple(x.shape), dt, hex(fl), "identical" if torch.equal(y0, y1) else f"DIFF max {(y0.float()-y1.float()).abs().max().item()}")
