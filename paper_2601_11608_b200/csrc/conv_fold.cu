@@ -49,7 +49,7 @@ struct ConvArgs {
   int nt_bbytes[kMaxNTiles];
   long long nt_bsrc[kMaxNTiles];  // device address of the N-tile's packed B
   long long row_bytes;            // bytes of one folded output row = r*Cout*out_elem
-  unsigned idesc;
+  int chunk_col[kMaxNTiles][kMaxAccCols / 32];  // output column of each epilogue chunk
   unsigned acc_stride, tmem_cols;
   int epi_flags;
   int off_a, off_b, off_bias;
@@ -182,6 +182,10 @@ __global__ void __launch_bounds__(320, 1)
         const int n = mt / a.ohb;
         const int oh0 = (mt - n * a.ohb) * a.OHt;
         const uint32_t dst = base + a.off_a + stage * a.stage_bytes;
+        if (a.epi_flags & 0x1000) {  // profiling: no A loads (stage contents stale)
+          mbar_arrive(bar_full + 8 * stage);
+          continue;
+        }
         mbar_arrive_expect_tx(bar_full + 8 * stage, tx);
         for (int b = 0; b < a.s; ++b) {
           if (!((a.res_mask >> b) & 1u)) continue;
@@ -222,14 +226,14 @@ __global__ void __launch_bounds__(320, 1)
             const uint4 e = a.table[e0 + i + j];
             const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
             const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
-            if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, a.idesc, e.z >> 31);
+            if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
           }
         }
         for (; i < entries; ++i) {
           const uint4 e = a.table[e0 + i];
           const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
           const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
-          if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, a.idesc, e.z >> 31);
+          if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
         }
       }
       if (leader) {
@@ -261,12 +265,15 @@ __global__ void __launch_bounds__(320, 1)
     const bool dbg_skip_store = (a.epi_flags & 0x400) != 0;
     const bool skip_ld = (a.epi_flags & 0x800) != 0;
     const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
-    float breg[CPW][VPT];
+    float breg[CPW][VPT];   // bias of this thread's channels in each of its chunks
+    long long coff[CPW];    // byte offset of each chunk's first output column in a row
 #pragma unroll
     for (int cc = 0; cc < CPW; ++cc) {
       const int c = half + 2 * cc;
+      const int ocol = (c < nchunks) ? a.chunk_col[ntile][c] : col0;  // slot order -> output column
+      coff[cc] = static_cast<long long>(ocol) * sizeof(OutT);
 #pragma unroll
-      for (int v = 0; v < VPT; ++v) breg[cc][v] = (c < nchunks) ? sbias[c * CH + VPT * k4 + v] : 0.0f;
+      for (int v = 0; v < VPT; ++v) breg[cc][v] = (c < nchunks) ? sbias[ocol - col0 + VPT * k4 + v] : 0.0f;
     }
     // the four M rows this thread stores: (16-lane half h16, row group r8)
     int row_t[2][2], row_w[2][2];
@@ -278,7 +285,7 @@ __global__ void __launch_bounds__(320, 1)
         row_t[h16][r8] = m / a.Wbox;
         row_w[h16][r8] = m - row_t[h16][r8] * a.Wbox;
       }
-    const long long col_bytes = static_cast<long long>(col0 + VPT * k4) * sizeof(OutT);
+    const long long col_bytes = static_cast<long long>(VPT * k4) * sizeof(OutT);
     int it_tile = 0;
     for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it_tile) {
       const int acc = it_tile & 1;
@@ -318,8 +325,6 @@ __global__ void __launch_bounds__(320, 1)
         if (it + 1 < n_it) tmem_ld_16x256b<NREG>(taddr(it + 1), buf[(it + 1) & 1], skip_ld);
         const int cc = it >> 1, h16 = it & 1;
         const uint32_t(&r)[NREG] = buf[it & 1];
-        const long long coff = static_cast<long long>(2 * cc) * CH * sizeof(OutT);  // chunk c - half, in bytes
-        const long long hoff = static_cast<long long>(half) * CH * sizeof(OutT);
 #pragma unroll
         for (int r8 = 0; r8 < 2; ++r8) {
           float v[VPT];
@@ -332,7 +337,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
             for (int k = 0; k < VPT; ++k) v[k] = (v[k] < 0.0f) ? 0.0f : v[k];
           }
-          if (rowv[h16][r8]) store_row<OutT, VPT>(rowp[h16][r8] + hoff + coff, v);
+          if (rowv[h16][r8]) store_row<OutT, VPT>(rowp[h16][r8] + coff[cc], v);
         }
       }
       tc_fence_before();
@@ -469,13 +474,24 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     a.nt_bsrc[i] = reinterpret_cast<long long>(packed_b + t.b_off);
     max_cols = std::max<uint32_t>(max_cols, static_cast<uint32_t>(t.cols));
   }
-  const uint32_t lbo_b = static_cast<uint32_t>(S.Ng) * 16u;
+  const uint32_t fmt = (in_t == WF_BF16) ? 1u : (in_t == WF_F16 ? 0u : 2u);
+  const uint32_t idesc_base = (1u << 4) | (fmt << 7) | (fmt << 10) | ((static_cast<uint32_t>(kTileM) >> 4) << 24);
   for (size_t i = 0; i < S.entries.size(); ++i) {
     const MmaEntry& e = S.entries[i];
+    const uint32_t n8 = (e.meta >> 22) & 0x1FFu;  // N / 8 of this MMA
+    const uint32_t lbo_b = n8 * 8u * 16u;         // B: [core col][N rows][16 B]
     a.table[i].x = (e.a_off >> 4) | ((static_cast<uint32_t>(S.lbo_a) >> 4) << 16);
     a.table[i].y = (e.b_off >> 4) | ((lbo_b >> 4) << 16);
-    a.table[i].z = e.meta;
+    a.table[i].z = idesc_base | (n8 << 17) | (e.meta & 0x80000000u);
     a.table[i].w = e.tmem_col;
+  }
+  // absolute output column of every epilogue chunk (slot order -> groups)
+  for (int i = 0; i < a.n_tiles; ++i) {
+    const NTile& t = S.ntiles[i];
+    for (int c = 0; c < t.cols / S.CH; ++c) {
+      const int slot = (c * S.CH) / S.Ng;
+      a.chunk_col[i][c] = S.order[t.g0 + slot] * S.Ng + (c * S.CH) % S.Ng;
+    }
   }
   if (num_sms <= 0) {
     int dev = 0;
@@ -484,9 +500,6 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   }
   a.ctas_per_ntile = std::max(1, std::min<int>(num_sms / a.n_tiles, a.num_mtiles));
   a.row_bytes = p.cout_f * oes;
-  const uint32_t fmt = (in_t == WF_BF16) ? 1u : (in_t == WF_F16 ? 0u : 2u);
-  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((static_cast<uint32_t>(S.Ng) >> 3) << 17) |
-            ((static_cast<uint32_t>(kTileM) >> 4) << 24);
   a.acc_stride = pow2ceil(max_cols);
   a.tmem_cols = 2 * a.acc_stride;
   a.epi_flags = static_cast<int>(epilogue);

@@ -18,6 +18,9 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstring>
+#include <vector>
+
 #include "kernels.hpp"
 
 namespace wfb {
@@ -27,6 +30,7 @@ struct PackArgs {
   int entries;
   int n_tiles;
   int nt_entry0[kMaxNTiles];
+  int nt_g0[kMaxNTiles];
   long long nt_boff[kMaxNTiles];
   long long table_bytes;
   int round_tf32;
@@ -38,40 +42,41 @@ template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
 template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
 template <> __device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
 
-// One thread per packed element: entries x 2 core cols x Ng rows x (E/2) elems.
+// One CTA per schedule entry (kh, unit u, run of accumulator slots); threads
+// walk its 2 core cols x N rows x (E/2) elements. Row nrow of the block is
+// accumulator column slot0*Ng + nrow: group order[g0 + slot], output column
+// chunk_perm(nrow % Ng) of that group.
 template <typename T>
 __global__ void pack_b_kernel(const T* __restrict__ w, uint8_t* __restrict__ packed, PackArgs a) {
+  const int ei = blockIdx.x;
+  const uint4 e = reinterpret_cast<const uint4*>(packed)[ei];
+  const int* order = reinterpret_cast<const int*>(packed + 16LL * a.entries);
+  const int kh = e.z & 0xff;
+  const int u = (e.z >> 8) & 0xff;  // first core column of the pair
+  const int slot0 = (e.z >> 16) & 0x3f;
+  const int N = static_cast<int>((e.z >> 22) & 0x1ffu) * 8;
+  int nt = 0;
+  while (nt + 1 < a.n_tiles && ei >= a.nt_entry0[nt + 1]) ++nt;
   const int half = a.E / 2;
-  const long long per_entry = 2LL * a.Ng * half;
-  const long long total = per_entry * a.entries;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int ei = static_cast<int>(idx / per_entry);
-    int rem = static_cast<int>(idx - (long long)ei * per_entry);
-    const int cc = rem / (a.Ng * half);
-    rem -= cc * a.Ng * half;
+  const int total = 2 * N * half;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int cc = idx / (N * half);
+    int rem = idx - cc * N * half;
     const int nrow = rem / half;
     const int e8 = rem - nrow * half;
-    const uint4 e = reinterpret_cast<const uint4*>(packed)[ei];
-    const int kh = e.z & 0xff;
-    const int c0col = (e.z >> 8) & 0xff;  // first core column of the pair
-    const int g = (e.z >> 16) & 0x7fff;
-    int nt = 0;
-    while (nt + 1 < a.n_tiles && ei >= a.nt_entry0[nt + 1]) ++nt;
-    const int widx = (c0col + cc) * half + e8;  // element of the KW'*f*C window row
+    const int widx = (u + cc) * half + e8;  // element of the KW'*f*C window row
     const int kp = widx / (a.f * a.C);
     const int r2 = widx - kp * a.f * a.C;
     const int fi = r2 / a.C;
     const int c = r2 - fi * a.C;
-    // accumulator column nrow of the group holds output column perm(nrow)
-    // (groups start on chunk boundaries, so the permutation stays inside)
-    const int ncol = chunk_perm(nrow, a.CH);
+    const int g = order[a.nt_g0[nt] + slot0 + nrow / a.Ng];
+    const int ncol = chunk_perm(nrow % a.Ng, a.CH);  // output column inside the group
     const int j = g * a.gs + ncol / a.Cout;
     const int co = ncol - (ncol / a.Cout) * a.Cout;
     const int kw = (a.c0 + kp) * a.f + fi - j * a.s + a.pw;
     T val = T(0.0f);
     if (kw >= 0 && kw < a.KW) val = w[((static_cast<long long>(kh) * a.KW + kw) * a.C + c) * a.Cout + co];
-    uint8_t* dst = packed + a.table_bytes + a.nt_boff[nt] + e.y + cc * (a.Ng * 16) + nrow * 16 + e8 * a.esize;
+    uint8_t* dst = packed + a.table_bytes + a.nt_boff[nt] + e.y + cc * (N * 16) + nrow * 16 + e8 * a.esize;
     if constexpr (sizeof(T) == 4) {
       float v = to_f(val);
       if (a.round_tf32) {
@@ -113,9 +118,14 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
                       float* b_rep, cudaStream_t st, std::string* err) {
   const wf_fold_plan& p = S.plan;
   // schedule table first: the pack kernel and the conv kernel both read it.
+  // header = schedule table + slot order. A pageable-source cudaMemcpyAsync
+  // returns once the bytes are staged, so the temporary may go out of scope.
+  std::vector<uint8_t> header(static_cast<size_t>(p.table_bytes), 0);
+  std::memcpy(header.data(), S.entries.data(), S.entries.size() * sizeof(MmaEntry));
+  std::memcpy(header.data() + S.entries.size() * sizeof(MmaEntry), S.order.data(), S.order.size() * sizeof(int));
   cudaError_t e = cudaMemsetAsync(packed, 0, static_cast<size_t>(p.packed_bytes), st);
   if (e == cudaSuccess)
-    e = cudaMemcpyAsync(packed, S.entries.data(), S.entries.size() * sizeof(MmaEntry), cudaMemcpyHostToDevice, st);
+    e = cudaMemcpyAsync(packed, header.data(), header.size(), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) {
     *err = std::string("pack: table upload failed: ") + cudaGetErrorString(e);
     return WF_CUDA_ERROR;
@@ -138,13 +148,13 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
   a.n_tiles = static_cast<int>(S.ntiles.size());
   for (int i = 0; i < a.n_tiles; ++i) {
     a.nt_entry0[i] = S.ntiles[i].entry0;
+    a.nt_g0[i] = S.ntiles[i].g0;
     a.nt_boff[i] = S.ntiles[i].b_off;
   }
   a.table_bytes = p.table_bytes;
   a.round_tf32 = 1;
-  const long long total = 2LL * S.Ng * (S.E / 2) * a.entries;
+  const int blocks = a.entries;
   const int threads = 256;
-  const int blocks = static_cast<int>(std::min<long long>((total + threads - 1) / threads, 4096));
   const wf_dtype t = static_cast<wf_dtype>(p.in_dtype);
   if (t == WF_BF16)
     pack_b_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>(static_cast<const __nv_bfloat16*>(w),

@@ -254,42 +254,114 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
     }
   }
 
-  // ---- the schedule: per N-tile, kh -> group -> unit ------------------------
+  // ---- the schedule: per N-tile, kh -> unit -> run of groups -----------------
+  // Groups that start a unit at the same core column u read the SAME A view;
+  // when they sit in adjacent accumulator slots one MMA with N = Ng * run
+  // serves them all (A is read from shared memory once). The slot order of
+  // each N-tile is chosen to maximise such runs under a per-MMA cost model
+  // measured on B200 (tools/probes/mma_probe.cu: N=64 -> 55, 128 -> 67,
+  // 256 -> 128 cycles; shared-memory operand reads bound small N).
+  auto unit_set = [&](int64_t g) {
+    std::vector<int64_t> u;
+    for (int64_t i = 0; i < n_units(g); ++i) u.push_back(lo[g] + 2 * i);
+    return u;
+  };
+  auto mma_cost = [](int64_t n) { return std::max<int64_t>(n / 2, 32 + n / 4); };
+  // runs of one N-tile for a slot order: (u, first slot, number of slots)
+  struct Run { int64_t u; int slot0, len; };
+  auto runs_for = [&](const NTile& t, const std::vector<int>& order) {
+    std::vector<int> slot_of(G, -1);
+    for (size_t sidx = 0; sidx < order.size(); ++sidx) slot_of[order[sidx]] = static_cast<int>(sidx);
+    std::vector<int64_t> us;
+    for (int g = t.g0; g < t.g1; ++g)
+      for (int64_t u : unit_set(g)) us.push_back(u);
+    std::sort(us.begin(), us.end());
+    us.erase(std::unique(us.begin(), us.end()), us.end());
+    std::vector<Run> runs;
+    for (int64_t u : us) {
+      std::vector<int> slots;
+      for (int g = t.g0; g < t.g1; ++g) {
+        const auto uu = unit_set(g);
+        if (std::find(uu.begin(), uu.end(), u) != uu.end()) slots.push_back(slot_of[g]);
+      }
+      std::sort(slots.begin(), slots.end());
+      for (size_t i = 0; i < slots.size();) {
+        size_t k = i + 1;
+        while (k < slots.size() && slots[k] == slots[k - 1] + 1) ++k;
+        runs.push_back({u, slots[i], static_cast<int>(k - i)});
+        i = k;
+      }
+    }
+    return runs;
+  };
+  auto order_cost = [&](const NTile& t, const std::vector<int>& order) {
+    int64_t c = 0;
+    for (const Run& rn : runs_for(t, order)) c += mma_cost(static_cast<int64_t>(rn.len) * S.Ng);
+    return c;
+  };
   S.entries.clear();
+  S.order.assign(static_cast<size_t>(G), 0);
   int64_t b_cursor = 0;
   for (auto& t : S.ntiles) {
+    std::vector<int> order;
+    for (int g = t.g0; g < t.g1; ++g) order.push_back(g);
+    if (t.g1 - t.g0 <= 8) {  // exhaustive over slot orders (<= 40320)
+      std::vector<int> cand = order;
+      int64_t best = order_cost(t, order);
+      while (std::next_permutation(cand.begin(), cand.end())) {
+        const int64_t c = order_cost(t, cand);
+        if (c < best) { best = c; order = cand; }
+      }
+    }
+    for (size_t sidx = 0; sidx < order.size(); ++sidx) S.order[t.g0 + sidx] = order[sidx];
+    const std::vector<Run> runs = runs_for(t, order);
+    // zero-init: at kh == 0 every group's first MMA must not accumulate; issue
+    // the runs in decreasing length so each run meets either only untouched
+    // or only touched groups (checked below)
+    std::vector<Run> first = runs;
+    std::stable_sort(first.begin(), first.end(), [](const Run& x, const Run& y) { return x.len > y.len; });
     t.entry0 = static_cast<int>(S.entries.size());
     t.b_off = b_cursor;
     uint32_t boff = 0;
+    bool ok_init = true;
     for (int64_t kh = 0; kh < d.kh; ++kh) {
       const int64_t delta = kh - d.pad_h;
       const int b = static_cast<int>(pos_mod(delta, sh));
       const int a = static_cast<int>((delta - b) / sh);
-      // Interleave groups: consecutive MMAs accumulate into different TMEM
-      // columns, so they pipeline instead of serialising on one accumulator.
-      int64_t steps = 0;
-      for (int gg = t.g0; gg < t.g1; ++gg) steps = std::max<int64_t>(steps, n_units(gg));
-      for (int64_t step = 0; step < steps; ++step)
-      for (int gg = t.g0; gg < t.g1; ++gg) {
-        if (step >= n_units(gg)) continue;
-        {
-          const int64_t u = lo[gg] + 2 * step;  // first core column of the pair
-          const int64_t kp = u / Q, q = u % Q;
-          MmaEntry e{};
-          e.a_off = static_cast<uint32_t>(b * S.region_bytes +
-                                          ((a - S.amin[b]) * Wbox + kp) * 16 +
-                                          q * S.lbo_a);
-          e.b_off = boff;
-          boff += static_cast<uint32_t>(block_bytes);
-          const bool acc = !(kh == 0 && u == lo[gg]);
-          e.meta = static_cast<uint32_t>(kh) | (static_cast<uint32_t>(u) << 8) |
-                   (static_cast<uint32_t>(gg) << 16) | (acc ? 0x80000000u : 0u);
-          e.tmem_col = static_cast<uint32_t>((gg - t.g0) * S.Ng);
-          S.entries.push_back(e);
+      std::vector<char> touched(order.size(), 0);
+      for (const Run& rn : (kh == 0 ? first : runs)) {
+        const int64_t u = rn.u;  // first core column of the pair
+        const int64_t kp = u / Q, q = u % Q;
+        MmaEntry e{};
+        e.a_off = static_cast<uint32_t>(b * S.region_bytes + ((a - S.amin[b]) * Wbox + kp) * 16 + q * S.lbo_a);
+        e.b_off = boff;
+        const int64_t n = static_cast<int64_t>(rn.len) * S.Ng;
+        boff += static_cast<uint32_t>(n * 32);
+        bool acc = true;
+        if (kh == 0) {
+          int nt = 0;
+          for (int k = 0; k < rn.len; ++k) nt += touched[rn.slot0 + k];
+          if (nt != 0 && nt != rn.len) ok_init = false;
+          acc = (nt != 0);
+          for (int k = 0; k < rn.len; ++k) touched[rn.slot0 + k] = 1;
         }
+        e.meta = static_cast<uint32_t>(kh) | (static_cast<uint32_t>(u) << 8) |
+                 (static_cast<uint32_t>(rn.slot0) << 16) | (static_cast<uint32_t>(n >> 3) << 22) |
+                 (acc ? 0x80000000u : 0u);
+        e.tmem_col = static_cast<uint32_t>(rn.slot0 * S.Ng);
+        S.entries.push_back(e);
       }
     }
+    if (!ok_init) {  // cannot happen with disjoint per-group units; keep the planner total
+      S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
+      *out = S;
+      return WF_OK;
+    }
     t.entries = static_cast<int>(S.entries.size()) - t.entry0;
+    if (static_cast<int64_t>(boff) != t.b_bytes) {
+      *err = "internal: B operand bytes of a merged schedule differ from the plan";
+      return WF_INVALID_ARGUMENT;
+    }
     b_cursor += t.b_bytes;
   }
 
@@ -318,13 +390,16 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   p.wbox = Wbox;
   p.nrows = NR;
   p.mma_entries = static_cast<int64_t>(S.entries.size());
-  p.table_bytes = (p.mma_entries * 16 + 127) / 128 * 128;
+  // packed header: schedule table, then the slot -> group order (int32 each)
+  p.table_bytes = (p.mma_entries * 16 + G * 4 + 127) / 128 * 128;
   p.packed_bytes = p.table_bytes + b_cursor;
   p.epi_chunk = S.CH;
   S.ohb = ceil_div(OH, OHt);
   S.num_mtiles = d.n * S.ohb;
   p.useful_macs = static_cast<uint64_t>(d.n) * OH * OW * d.cout * d.kh * d.kw * d.c;
-  p.issued_macs = static_cast<uint64_t>(S.num_mtiles) * p.mma_entries * kTileM * S.Ng * S.E;
+  uint64_t issued_per_tile = 0;
+  for (const MmaEntry& e : S.entries) issued_per_tile += static_cast<uint64_t>(kTileM) * ((e.meta >> 22) & 0x1FFu) * 8 * S.E;
+  p.issued_macs = static_cast<uint64_t>(S.num_mtiles) * issued_per_tile;
   *out = std::move(S);
   return WF_OK;
 }

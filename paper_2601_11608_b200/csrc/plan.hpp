@@ -68,7 +68,8 @@ WFB_HD inline int chunk_perm(int col, int CH) {
 struct MmaEntry {          // 16 bytes, lives in the packed buffer and in smem
   uint32_t a_off;          // byte offset of the A view inside an A stage
   uint32_t b_off;          // byte offset of the B block inside the N-tile's B
-  uint32_t meta;           // kh | c << 8 | g << 16 | accumulate << 31 (c: first core column)
+  uint32_t meta;           // kh | u << 8 | slot << 16 | (N/8) << 22 | accumulate << 31
+                           // (u: first core column; slot: first accumulator slot)
   uint32_t tmem_col;       // accumulator column of the group
 };
 
@@ -97,6 +98,7 @@ struct Schedule {
   int64_t num_mtiles = 0, ohb = 0;
   std::vector<MmaEntry> entries;
   std::vector<NTile> ntiles;
+  std::vector<int> order;        // accumulator slot (g0 + s of its N-tile) -> group
 };
 
 // Validates the descriptor like ConvSpec::validate (src/refconv.cpp:5-32) plus

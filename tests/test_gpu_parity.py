@@ -121,39 +121,50 @@ def test_tensor_core_conv_integer_data_exact(golden_configs, name):
 
 
 def test_packed_operand_unpacks_to_the_expansion(oracle):
-    """The once-packed tcgen05 B operand holds exactly W'(kh, kw', fi*C+c, j*Co+co)."""
+    """The once-packed tcgen05 B operand holds exactly W'(kh, kw', fi*C+c, j*Co+co).
+
+    Packed header: per MMA a 16-byte entry (a_off, b_off, meta, tmem_col),
+    meta = kh | u << 8 | slot << 16 | (N/8) << 22 | acc << 31, then the
+    accumulator-slot -> group order (int32). B block of an entry:
+    [core col 0..1][N rows][8 elements]; row n is accumulator column
+    slot*Ng + n = group order[slot + n // Ng], output column chunk_perm(n % Ng).
+    """
     rng = np.random.default_rng(5)
     KH, KW, C, Co, s, p = 7, 7, 3, 64, 2, 3
     w = rng.integers(-8, 9, (KH, KW, C, Co)).astype(np.float32)
     conv = wf.FoldedConv2d(cuda(w, torch.bfloat16), None, (2, 64, 64, 3), stride=s, padding=p,
                            dtype=torch.bfloat16)
     d = conv.device_plan
-    f, gs = d["f"], d["group_size"]
+    f, gs, ch = d["f"], d["group_size"], d["epi_chunk"]
+    Ng = gs * Co
+    G = d["n_groups"]
+    assert d["n_tiles"] == 1
     wexp = oracle.expand_filter_folded(w, f, s, p)  # (KH, KW', f*C, r*Co)
     raw = conv.packed.cpu().numpy()
     n_ent = d["mma_entries"]
     table = raw[: n_ent * 16].view(np.uint32).reshape(n_ent, 4)
-    table_bytes = (n_ent * 16 + 127) // 128 * 128
-    Ng = gs * Co
-    block = Ng * 32
-    base = table_bytes
-    last_end = 0
+    order = raw[n_ent * 16: n_ent * 16 + 4 * G].view(np.int32)
+    assert sorted(order.tolist()) == list(range(G))
+    base = (n_ent * 16 + 4 * G + 127) // 128 * 128
     checked = 0
-    for i, (a_off, b_off, meta, col) in enumerate(table):
-        if i > 0 and b_off == 0:  # B offsets restart at each N-tile
-            base += last_end
-        last_end = int(b_off) + block
-        kh, c, g = meta & 0xFF, (meta >> 8) & 0xFF, (meta >> 16) & 0x7FFF  # c: first 16-byte core column
-        blk = raw[base + b_off: base + b_off + block].view(np.uint16).reshape(2, Ng, 8)
+    covered = np.zeros((KH, G), np.int64)
+    for (a_off, b_off, meta, col) in table:
+        kh, u, slot = meta & 0xFF, (meta >> 8) & 0xFF, (meta >> 16) & 0x3F
+        N = ((meta >> 22) & 0x1FF) * 8
+        assert col == slot * Ng
+        blk = raw[base + b_off: base + b_off + N * 32].view(np.uint16).reshape(2, N, 8)
         vals = (blk.astype(np.uint32) << 16).view(np.float32)
-        for cc in range(2):
-            widx = (c + cc) * 8 + np.arange(8)
-            kp, k = widx // (f * C), widx % (f * C)
-            for nrow in range(0, Ng, 7):
-                n = g * Ng + chunk_perm(nrow, d["epi_chunk"])
-                np.testing.assert_array_equal(vals[cc, nrow], wexp[kh, kp, k, n])
+        for n in range(N):
+            g = order[slot + n // Ng]
+            covered[kh, g] += n % Ng == 0
+            ocol = g * Ng + chunk_perm(n % Ng, ch)
+            for cc in range(2):
+                widx = (u + cc) * 8 + np.arange(8)
+                kp, k = widx // (f * C), widx % (f * C)
+                np.testing.assert_array_equal(vals[cc, n], wexp[kh, kp, k, ocol])
                 checked += 1
-    assert checked > 100
+    assert checked > 1000
+    assert (covered >= 1).all()  # every group gets MMAs at every kh
 
 
 @pytest.mark.parametrize("batch,h,w", [(3, 36, 48), (1, 224, 224), (5, 20, 32), (2, 9, 16)])
