@@ -67,12 +67,17 @@ typedef enum {
   WF_REASON_UNSUPPORTED_CHANNELS = 6,
   WF_REASON_NOT_PROFITABLE = 7,
   WF_REASON_UNALIGNED_PIXEL = 8, /* f*C*elem not a multiple of the 32 B MMA K-step */
-  WF_REASON_OUTPUT_TAIL = 9      /* OW % r != 0 (masked tail not yet supported)     */
+  WF_REASON_OUTPUT_TAIL = 9      /* reserved (OW % r != 0 is now a masked tail)     */
 } wf_fold_reason;
 
 typedef enum { WF_FOLD_APPLY = 0, WF_FOLD_FALLBACK = 1 } wf_fold_status;
 
 typedef enum { WF_EPI_NONE = 0, WF_EPI_BIAS = 1, WF_EPI_RELU = 2 } wf_epilogue;
+
+/* Kernel variant: the width-folded conv, or the same tcgen05 kernel on the
+ * unfolded Cin=C input (explicit im2col A tiles) for the comparison. The
+ * zero-padded Cin 3->8 variant is the folded kernel on a padded tensor. */
+typedef enum { WF_VARIANT_FOLD = 0, WF_VARIANT_UNFOLDED = 1 } wf_variant;
 
 /* Conv problem: x NHWC (n,h,w,c), w HWIO (kh,kw,c,cout), symmetric padding. */
 typedef struct {
@@ -108,6 +113,9 @@ typedef struct {
   int64_t epi_chunk;       /* accumulator columns per epilogue chunk: the period
                               of the output-column permutation baked into the
                               packed filter (coalesced 16x256b TMEM reads) */
+  int32_t variant;         /* wf_variant */
+  int32_t producer;        /* A-tile producer: 0 TMA boxes, 1 software gather
+                              (any row pitch, W % f != 0), 2 explicit im2col */
   uint64_t useful_macs;    /* count_macs of the original conv */
   uint64_t issued_macs;    /* MACs the tensor cores execute (128-row tiles) */
 } wf_fold_plan;
@@ -120,6 +128,10 @@ typedef struct {
  * WF_INVALID_ARGUMENT. Host-only, pure, reentrant. */
 wf_status wf_plan_fold(const wf_conv_desc* desc, int64_t f, int64_t group_size,
                        wf_dtype in_dtype, wf_fold_plan* plan);
+
+/* Plan the UNFOLDED variant (M row = output pixel, explicit im2col, same
+ * MMA/epilogue). bf16/f16 only; Cout a multiple of 32. */
+wf_status wf_plan_unfolded(const wf_conv_desc* desc, wf_dtype in_dtype, wf_fold_plan* plan);
 
 /* Bytes of the packed filter buffer (schedule table + packed B operand). */
 size_t wf_packed_filter_bytes(const wf_fold_plan* plan);

@@ -31,7 +31,7 @@ REASONS = [
 ]
 
 EXPORTED = [
-    "wf_plan_fold", "wf_packed_filter_bytes", "wf_expand_filter_pack", "wf_expand_filter_dense",
+    "wf_plan_fold", "wf_plan_unfolded", "wf_packed_filter_bytes", "wf_expand_filter_pack", "wf_expand_filter_dense",
     "wf_conv_fold_fwd", "wf_set_num_sms", "wf_last_error", "wf_abi_version",
 ]
 
@@ -50,7 +50,7 @@ class FoldPlan(ctypes.Structure):
         ("oh", c_int64), ("ow", c_int64), ("wf", c_int64), ("wfo", c_int64),
         ("units_per_px", c_int64), ("group_size", c_int64), ("n_groups", c_int64),
         ("n_tiles", c_int64), ("tile_rows", c_int64), ("wbox", c_int64), ("nrows", c_int64),
-        ("mma_entries", c_int64), ("table_bytes", c_int64), ("packed_bytes", c_int64), ("epi_chunk", c_int64),
+        ("mma_entries", c_int64), ("table_bytes", c_int64), ("packed_bytes", c_int64), ("epi_chunk", c_int64), ("variant", c_int32), ("producer", c_int32),
         ("useful_macs", c_uint64), ("issued_macs", c_uint64),
     ]
 
@@ -81,6 +81,8 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(LIB_PATH)
         L.wf_plan_fold.argtypes = [POINTER(ConvDesc), c_int64, c_int64, c_int, POINTER(FoldPlan)]
         L.wf_plan_fold.restype = c_int
+        L.wf_plan_unfolded.argtypes = [POINTER(ConvDesc), c_int, POINTER(FoldPlan)]
+        L.wf_plan_unfolded.restype = c_int
         L.wf_packed_filter_bytes.argtypes = [POINTER(FoldPlan)]
         L.wf_packed_filter_bytes.restype = c_size_t
         L.wf_expand_filter_pack.argtypes = [c_void_p, c_void_p, POINTER(ConvDesc), POINTER(FoldPlan),
@@ -109,6 +111,12 @@ def check(status: int) -> None:
 
 def make_desc(n, h, w, c, kh, kw, cout, stride_h=1, stride_w=1, pad_h=0, pad_w=0) -> ConvDesc:
     return ConvDesc(n, h, w, c, kh, kw, cout, stride_h, stride_w, pad_h, pad_w)
+
+
+def plan_unfolded(desc: ConvDesc, in_dtype: int = WF_BF16) -> FoldPlan:
+    p = FoldPlan()
+    check(lib().wf_plan_unfolded(byref(desc), in_dtype, byref(p)))
+    return p
 
 
 def plan_fold(desc: ConvDesc, f: int = 0, group_size: int = 0, in_dtype: int = WF_BF16) -> FoldPlan:

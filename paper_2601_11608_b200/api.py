@@ -92,7 +92,7 @@ class FoldedConv2d:
     """
 
     def __init__(self, w: torch.Tensor, b: torch.Tensor | None, input_shape, stride=1, padding=0,
-                 dtype: torch.dtype | None = None, fold: int = 0, group_size: int = 0):
+                 dtype: torch.dtype | None = None, fold: int = 0, group_size: int = 0, variant: str = "fold"):
         w, _ = _as_tensor(w)
         dtype = dtype or w.dtype
         if dtype not in _DT_NAME:
@@ -102,8 +102,9 @@ class FoldedConv2d:
         ph, pw = _pair(padding)
         self.input_shape = tuple(int(v) for v in input_shape)
         self.dtype = dtype
+        self.variant = variant
         self.core = _core.FoldedConv(list(self.input_shape), list(w.shape), sh, sw, ph, pw,
-                                     _DT_NAME[dtype], fold, group_size)
+                                     _DT_NAME[dtype], fold, group_size, variant)
         dev = w.device
         self.packed = torch.empty(self.core.packed_bytes, dtype=torch.uint8, device=dev)
         self.b_rep = None
@@ -152,7 +153,8 @@ class FoldedConv2d:
         sh, sw, ph, pw = self._geom
         w = self._keep[0]
         other.core = _core.FoldedConv(list(shape), list(w.shape), sh, sw, ph, pw, _DT_NAME[self.dtype],
-                                      self.core.device["f"], self.core.device["group_size"])
+                                      self.core.device["f"] if self.variant == "fold" else 0,
+                                      self.core.device["group_size"] if self.variant == "fold" else 0, self.variant)
         if other.core.packed_bytes != self.core.packed_bytes:
             raise UnsupportedError("batch-specific plan changed the packed operand")
         other.input_shape = shape

@@ -24,7 +24,7 @@ wf_status fail(wf_status st, const std::string& msg) {
 
 extern "C" {
 
-int wf_abi_version(void) { return 2; }
+int wf_abi_version(void) { return 3; }
 
 const char* wf_last_error(void) { return g_last_error.c_str(); }
 
@@ -36,6 +36,16 @@ wf_status wf_plan_fold(const wf_conv_desc* desc, int64_t f, int64_t group_size, 
   wfb::Schedule S;
   std::string err;
   wf_status st = wfb::make_schedule(*desc, f, group_size, in_dtype, &S, &err);
+  if (st != WF_OK) return fail(st, err);
+  *plan = S.plan;
+  return WF_OK;
+}
+
+wf_status wf_plan_unfolded(const wf_conv_desc* desc, wf_dtype in_dtype, wf_fold_plan* plan) {
+  if (!desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
+  wfb::Schedule S;
+  std::string err;
+  wf_status st = wfb::make_schedule_unfolded(*desc, in_dtype, &S, &err);
   if (st != WF_OK) return fail(st, err);
   *plan = S.plan;
   return WF_OK;
@@ -74,7 +84,7 @@ wf_status wf_conv_fold_fwd(const void* x, const void* w_packed, const float* b_r
                            const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype, uint32_t epilogue,
                            void* stream) {
   if (!x || !w_packed || !y || !desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
-  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0x3F00))  // 0x3F00: profiling / epilogue-mode switches
+  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0x7F00))  // 0x7F00: profiling / epilogue-mode switches
     return fail(WF_INVALID_ARGUMENT, "unknown epilogue flags");
   wfb::Schedule S;
   std::string err;

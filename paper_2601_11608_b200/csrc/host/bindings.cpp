@@ -45,7 +45,9 @@ py::dict raw_dict(const wf_fold_plan& p) {
   d["oh"] = p.oh; d["ow"] = p.ow; d["wf"] = p.wf; d["wfo"] = p.wfo; d["units_per_px"] = p.units_per_px;
   d["group_size"] = p.group_size; d["n_groups"] = p.n_groups; d["n_tiles"] = p.n_tiles;
   d["tile_rows"] = p.tile_rows; d["wbox"] = p.wbox; d["nrows"] = p.nrows; d["mma_entries"] = p.mma_entries;
-  d["packed_bytes"] = p.packed_bytes; d["epi_chunk"] = p.epi_chunk; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
+  d["packed_bytes"] = p.packed_bytes; d["epi_chunk"] = p.epi_chunk;
+  d["variant"] = p.variant == WF_VARIANT_UNFOLDED ? "unfolded" : "fold";
+  d["producer"] = p.producer == 0 ? "tma" : (p.producer == 1 ? "gather" : "im2col"); d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
   return d;
 }
 
@@ -180,12 +182,16 @@ PYBIND11_MODULE(_core, m) {
   py::class_<wf::FoldedConv>(m, "FoldedConv")
       .def(py::init([](const wf::Shape& in, const wf::Shape& filt, std::int64_t sh, std::int64_t sw,
                        std::int64_t ph, std::int64_t pw, const std::string& dtype, std::int64_t factor,
-                       std::int64_t group_size) {
-             return wf::FoldedConv(spec_of(in, filt, sh, sw, ph, pw), dtype_of(dtype), factor, group_size);
+                       std::int64_t group_size, const std::string& variant) {
+             if (variant != "fold" && variant != "unfolded")
+               throw std::invalid_argument("variant must be 'fold' or 'unfolded'");
+             return wf::FoldedConv(spec_of(in, filt, sh, sw, ph, pw), dtype_of(dtype), factor, group_size,
+                                   variant == "unfolded" ? wf::FoldedConv::Variant::Unfolded
+                                                         : wf::FoldedConv::Variant::Fold);
            }),
            py::arg("input_shape"), py::arg("filter_shape"), py::arg("stride_h") = 1, py::arg("stride_w") = 1,
            py::arg("pad_h") = 0, py::arg("pad_w") = 0, py::arg("dtype") = "bf16", py::arg("factor") = 0,
-           py::arg("group_size") = 0)
+           py::arg("group_size") = 0, py::arg("variant") = "fold")
       .def_property_readonly("packed_bytes", &wf::FoldedConv::packed_bytes)
       .def_property_readonly("cout_f", &wf::FoldedConv::cout_f)
       .def_property_readonly("plan", [](const wf::FoldedConv& c) { return plan_dict(c.plan()); })

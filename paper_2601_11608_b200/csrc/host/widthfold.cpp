@@ -127,7 +127,7 @@ DevicePlan plan_device_fold(const ConvSpec& spec, std::int64_t factor, std::int6
   out.plan.factor = out.raw.f;
   if (out.plan.ok()) {
     const std::int64_t f = out.raw.f;
-    out.plan.folded_input_shape = {spec.batch(), spec.in_h(), spec.in_w() / f, spec.in_c() * f};
+    out.plan.folded_input_shape = {spec.batch(), spec.in_h(), (spec.in_w() + f - 1) / f, spec.in_c() * f};
     out.plan.expanded_filter_shape = {spec.k_h(), out.raw.kw_f, f * spec.in_c(), out.raw.cout_f};
   }
   return out;
@@ -207,9 +207,24 @@ void check_block_diagonal(const float* w_dense, const Shape& s, std::int64_t gro
   throw_on(wf_check_block_diagonal(w_dense, s[0], s[1], s[2], s[3], groups, scratch, &bad, stream));
 }
 
-FoldedConv::FoldedConv(const ConvSpec& spec, Dtype in_dtype, std::int64_t factor, std::int64_t group_size)
+FoldedConv::FoldedConv(const ConvSpec& spec, Dtype in_dtype, std::int64_t factor, std::int64_t group_size,
+                       Variant variant)
     : spec_(spec), in_(in_dtype) {
-  DevicePlan dp = plan_device_fold(spec, factor, group_size, in_dtype);
+  DevicePlan dp;
+  if (variant == Variant::Unfolded) {
+    spec.validate();
+    const wf_conv_desc d = spec.desc();
+    throw_on(wf_plan_unfolded(&d, static_cast<wf_dtype>(in_dtype), &dp.raw));
+    dp.plan.status = dp.raw.status == WF_FOLD_APPLY ? FoldStatus::Apply : FoldStatus::Fallback;
+    dp.plan.reason = static_cast<FoldReason>(dp.raw.reason);
+    dp.plan.factor = 1;
+    if (dp.plan.ok()) {
+      dp.plan.folded_input_shape = spec.input_shape;
+      dp.plan.expanded_filter_shape = spec.filter_shape;
+    }
+  } else {
+    dp = plan_device_fold(spec, factor, group_size, in_dtype);
+  }
   if (!dp.plan.ok())
     throw Unsupported(std::string("width fold not applicable to this conv: ") + to_string(dp.plan.reason) +
                       " (factor " + std::to_string(dp.plan.factor) + ")");
@@ -227,7 +242,7 @@ void FoldedConv::pack(const void* w, const float* b, void* packed, float* b_rep,
 void FoldedConv::forward(const void* x, const void* packed, const float* b_rep, void* y, Dtype out_dtype, bool bias,
                          bool relu, void* stream, std::uint32_t profile_flags) const {
   std::uint32_t epi = (bias ? static_cast<std::uint32_t>(WF_EPI_BIAS) : 0u) |
-                     (relu ? static_cast<std::uint32_t>(WF_EPI_RELU) : 0u) | (profile_flags & 0x3F00u);
+                     (relu ? static_cast<std::uint32_t>(WF_EPI_RELU) : 0u) | (profile_flags & 0x7F00u);
   throw_on(wf_conv_fold_fwd(x, packed, bias ? b_rep : nullptr, y, &desc_, &raw_, static_cast<wf_dtype>(out_dtype),
                             epi, stream));
 }

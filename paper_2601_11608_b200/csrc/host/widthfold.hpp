@@ -131,7 +131,11 @@ void check_block_diagonal(const float* w_dense, const Shape& dense_shape, std::i
 // The folded tcgen05 convolution with its once-per-weights packed filter.
 class FoldedConv {
  public:
-  FoldedConv(const ConvSpec& spec, Dtype in_dtype, std::int64_t factor = 0, std::int64_t group_size = 0);
+  enum class Variant { Fold = WF_VARIANT_FOLD, Unfolded = WF_VARIANT_UNFOLDED };
+  // Variant::Unfolded runs the same tcgen05 kernel on the unfolded Cin=C input
+  // (explicit im2col A tiles) -- the fold-vs-unfolded comparison.
+  FoldedConv(const ConvSpec& spec, Dtype in_dtype, std::int64_t factor = 0, std::int64_t group_size = 0,
+             Variant variant = Variant::Fold);
   std::size_t packed_bytes() const;
   std::int64_t cout_f() const { return raw_.cout_f; }
   const wf_fold_plan& raw() const { return raw_; }

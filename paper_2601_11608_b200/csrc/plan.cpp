@@ -111,16 +111,20 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
     *out = std::move(S);
     return WF_OK;
   }
-  if (d.w % f != 0) { S.plan = fallback(WF_REASON_WIDTH_NOT_DIVISIBLE, f); *out = S; return WF_OK; }
   if (f % sw != 0) { S.plan = fallback(WF_REASON_STRIDE_ON_FOLD_AXIS, f); *out = S; return WF_OK; }
   if ((f * d.c * S.esize) % 16 != 0) { S.plan = fallback(WF_REASON_UNALIGNED_PIXEL, f); *out = S; return WF_OK; }
   const int64_t r = f / sw;
-  if (OW % r != 0) { S.plan = fallback(WF_REASON_OUTPUT_TAIL, f); *out = S; return WF_OK; }
   if (d.h < sh) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
 
   const int64_t c0 = -ceil_div(d.pad_w, f);
   const int64_t kwf = floor_div(f - sw - d.pad_w + d.kw - 1, f) - c0 + 1;
-  const int64_t Wf = d.w / f, Wfo = OW / r;
+  // W % f != 0: the last folded pixel is partial (zero-filled by the gather
+  // producer); OW % r != 0: the last folded output column is masked per j.
+  const int64_t Wf = ceil_div(d.w, f), Wfo = ceil_div(OW, r);
+  // TMA boxes need the folded view to be a pure reshape with a 16-byte row
+  // pitch; otherwise (AlexNet: W=227, 1362-byte rows) the software gather.
+  S.prod = (d.w % f == 0 && (d.w * d.c * S.esize) % 16 == 0) ? 0 : 1;
+  if (S.prod != 0 && in_dtype == WF_TF32) { S.plan = fallback(WF_REASON_WIDTH_NOT_DIVISIBLE, f); *out = S; return WF_OK; }
   const int64_t Q = f * d.c * S.esize / 16;  // core columns per folded pixel
   S.Q = static_cast<int>(Q);
   const int64_t E2 = S.E / 2;                  // elements per core column
@@ -394,6 +398,8 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   p.table_bytes = (p.mma_entries * 16 + G * 4 + 127) / 128 * 128;
   p.packed_bytes = p.table_bytes + b_cursor;
   p.epi_chunk = S.CH;
+  p.variant = WF_VARIANT_FOLD;
+  p.producer = S.prod;
   S.ohb = ceil_div(OH, OHt);
   S.num_mtiles = d.n * S.ohb;
   p.useful_macs = static_cast<uint64_t>(d.n) * OH * OW * d.cout * d.kh * d.kw * d.c;
@@ -404,13 +410,137 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   return WF_OK;
 }
 
+wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Schedule* out, std::string* err) {
+  wf_status st = validate_desc(d, err);
+  if (st != WF_OK) return st;
+  if (in_dtype != WF_BF16 && in_dtype != WF_F16) {
+    *err = "the unfolded variant runs bf16/f16 inputs";
+    return WF_INVALID_ARGUMENT;
+  }
+  Schedule S;
+  S.esize = elem_bytes(in_dtype);
+  S.E = 32 / S.esize;
+  S.s = static_cast<int>(d.stride_h);
+  S.ph = static_cast<int>(d.pad_h);
+  S.pw = static_cast<int>(d.pad_w);
+  S.prod = 2;
+  const int64_t OH = (d.h + 2 * d.pad_h - d.kh) / d.stride_h + 1;
+  const int64_t OW = (d.w + 2 * d.pad_w - d.kw) / d.stride_w + 1;
+  if (d.cout % 32 != 0 || d.cout > kMaxAccCols) {
+    S.plan = fallback(WF_REASON_UNSUPPORTED_CHANNELS, 1);
+    *out = S;
+    return WF_OK;
+  }
+  // M row = output pixel; per kh one window row of KW*C elements, U 32-byte
+  // K-steps; every A view is materialised ([kh*U + u][core col][128 rows][16 B]).
+  const int64_t U = ceil_div(d.kw * d.c * S.esize, 32);
+  S.U = static_cast<int>(U);
+  S.Q = 2;
+  S.Ng = static_cast<int>(d.cout);
+  S.CH = (S.Ng % 64 == 0) ? 64 : 32;
+  S.lbo_a = kTileM * 16;
+  S.region_bytes = 0;
+  // kh rows per A stage: all of them when two stages fit, else split the
+  // tile's K into ksplit sub-stages (AlexNet: 11 kh x 3 K-steps = 132 KB)
+  const int64_t region = 2 * kTileM * 16;  // one (kh, K-step) view
+  const int64_t b_total = d.kh * U * d.cout * 32;
+  const int64_t fixed0 = 1024 + kTileM * 16 + 128 + (b_total + 127) / 128 * 128 + kMaxAccCols * 4 + 1024;
+  int64_t ksplit = 1;
+  while (ksplit < 8 && fixed0 + 2 * ceil_div(d.kh, ksplit) * U * region > kSmemLimit) ++ksplit;
+  const int64_t khs = ceil_div(d.kh, ksplit);
+  ksplit = ceil_div(d.kh, khs);
+  S.ksplit = static_cast<int>(ksplit);
+  S.stage_bytes = static_cast<int>(khs * U * region);
+  NTile t{};
+  t.g0 = 0;
+  t.g1 = 1;
+  t.col0 = 0;
+  t.cols = static_cast<int>(d.cout);
+  t.b_bytes = d.kh * U * d.cout * 32;
+  t.entry0 = 0;
+  t.b_off = 0;
+  S.order.assign(1, 0);
+  uint32_t boff = 0;
+  for (int64_t kh = 0; kh < d.kh; ++kh) {
+    if (kh % khs == 0) {
+      S.ks_kh0.push_back(static_cast<int>(kh));
+      S.ks_entry0.push_back(static_cast<int>(S.entries.size()));
+      S.ks_chunks.push_back(static_cast<int>(std::min(khs, d.kh - kh) * U * region / 16));
+    }
+    for (int64_t u = 0; u < U; ++u) {
+      MmaEntry e{};
+      e.a_off = static_cast<uint32_t>(((kh % khs) * U + u) * region);
+      e.b_off = boff;
+      boff += static_cast<uint32_t>(d.cout * 32);
+      const bool acc = !(kh == 0 && u == 0);
+      e.meta = static_cast<uint32_t>(kh) | (static_cast<uint32_t>(2 * u) << 8) |
+               (static_cast<uint32_t>(d.cout >> 3) << 22) | (acc ? 0x80000000u : 0u);
+      e.tmem_col = 0;
+      S.entries.push_back(e);
+    }
+  }
+  for (size_t k = 0; k < S.ks_entry0.size(); ++k)
+    S.ks_entries.push_back(
+        (k + 1 < S.ks_entry0.size() ? S.ks_entry0[k + 1] : static_cast<int>(S.entries.size())) - S.ks_entry0[k]);
+  t.entries = static_cast<int>(S.entries.size());
+  S.ntiles.push_back(t);
+  const int64_t fixed = fixed0;
+  S.stages = 0;
+  for (int st2 = 4; st2 >= 2; --st2)
+    if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { S.stages = st2; break; }
+  if (S.stages == 0 || S.entries.size() > 384) {
+    S.plan = fallback(WF_REASON_NOT_PROFITABLE, 1);
+    *out = S;
+    return WF_OK;
+  }
+  S.b_smem_bytes = static_cast<int>((t.b_bytes + 127) / 128 * 128);
+  wf_fold_plan& p = S.plan;
+  p = wf_fold_plan{};
+  p.status = WF_FOLD_APPLY;
+  p.reason = WF_REASON_NONE;
+  p.f = 1;
+  p.r = 1;
+  p.c0 = -d.pad_w;
+  p.kw_f = d.kw;
+  p.k_f = d.kh * d.kw * d.c;
+  p.cout_f = d.cout;
+  p.in_dtype = in_dtype;
+  p.elem_bytes = S.esize;
+  p.oh = OH;
+  p.ow = OW;
+  p.wf = d.w;
+  p.wfo = OW;
+  p.units_per_px = U;
+  p.group_size = 1;
+  p.n_groups = 1;
+  p.n_tiles = 1;
+  p.tile_rows = 0;
+  p.wbox = 0;
+  p.nrows = 0;
+  p.mma_entries = static_cast<int64_t>(S.entries.size());
+  p.table_bytes = (p.mma_entries * 16 + 4 + 127) / 128 * 128;
+  p.packed_bytes = p.table_bytes + t.b_bytes;
+  p.epi_chunk = S.CH;
+  p.variant = WF_VARIANT_UNFOLDED;
+  p.producer = 2;
+  const int64_t total = d.n * OH * OW;
+  S.num_mtiles = ceil_div(total, kTileM);
+  S.ohb = 1;
+  p.useful_macs = static_cast<uint64_t>(total) * d.cout * d.kh * d.kw * d.c;
+  p.issued_macs = static_cast<uint64_t>(S.num_mtiles) * S.entries.size() * kTileM * d.cout * S.E;
+  *out = std::move(S);
+  return WF_OK;
+}
+
 wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
                              Schedule* out, std::string* err) {
   if (p.status != WF_FOLD_APPLY) {
     *err = "plan is not an Apply plan";
     return WF_INVALID_ARGUMENT;
   }
-  wf_status st = make_schedule(d, p.f, p.group_size, static_cast<wf_dtype>(p.in_dtype), out, err);
+  wf_status st = (p.variant == WF_VARIANT_UNFOLDED)
+                     ? make_schedule_unfolded(d, static_cast<wf_dtype>(p.in_dtype), out, err)
+                     : make_schedule(d, p.f, p.group_size, static_cast<wf_dtype>(p.in_dtype), out, err);
   if (st != WF_OK) return st;
   if (out->plan.status != WF_FOLD_APPLY || out->plan.packed_bytes != p.packed_bytes ||
       out->plan.mma_entries != p.mma_entries) {

@@ -89,6 +89,10 @@ struct Schedule {
   bool need_shift = false;       // some unit pairs (Q-1, next pixel's 0)
   int Ng = 64;                   // accumulator columns per group
   int CH = 64;                   // epilogue chunk (columns per 16x256b TMEM read)
+  int prod = 0;                  // A producer: 0 TMA boxes, 1 gather (folded), 2 gather (im2col)
+  int U = 0;                     // im2col: 32-byte K-steps per kh
+  int ksplit = 1;                // A stages per M tile (im2col: kh ranges)
+  std::vector<int> ks_kh0, ks_entry0, ks_entries, ks_chunks;
   int amin[kMaxResidues] = {0};
   int amax[kMaxResidues] = {0};
   bool has_res[kMaxResidues] = {false};
@@ -109,6 +113,10 @@ wf_status validate_desc(const wf_conv_desc& d, std::string* err);
 // or an error status (shape problems, bad arguments).
 wf_status make_schedule(const wf_conv_desc& d, int64_t f, int64_t group_size,
                         wf_dtype in_dtype, Schedule* out, std::string* err);
+
+// The unfolded Cin=C variant of the same kernel (explicit im2col A tiles):
+// the fold-vs-unfolded comparison of the north star.
+wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Schedule* out, std::string* err);
 
 // Rebuild the schedule from a plan previously returned by make_schedule.
 wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,

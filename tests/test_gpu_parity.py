@@ -95,18 +95,18 @@ def test_expand_filters_bitwise(golden_kats, golden_configs, oracle):
         wf.expand_filter_general(np.zeros((3, 3, 1, 1), np.float32), 2)
 
 
-def _config_run(golden_configs, name, suffix, out_dtype=None):
+def _config_run(golden_configs, name, suffix, out_dtype=None, variant="fold", flags=0):
     KH, KW, C, Co, s, p, relu = (int(v) for v in golden_configs[f"{name}_geom"])
     dt = str(golden_configs[f"{name}_dtype"])
     x, w, b = (golden_configs[f"{name}_{k}{suffix}"] for k in ("x", "w", "b"))
     tdt = TDT[dt]
-    conv = wf.FoldedConv2d(cuda(w, tdt), cuda(b), x.shape, stride=s, padding=p, dtype=tdt)
-    y = conv(cuda(x, tdt), relu=bool(relu), out_dtype=out_dtype)
+    conv = wf.FoldedConv2d(cuda(w, tdt), cuda(b), x.shape, stride=s, padding=p, dtype=tdt, variant=variant)
+    y = conv(cuda(x, tdt), relu=bool(relu), out_dtype=out_dtype, _profile_flags=flags)
     torch.cuda.synchronize()
     return y.float().cpu().numpy(), golden_configs[f"{name}_y{suffix}"], dt, conv
 
 
-@pytest.mark.parametrize("name", [n for n in CONFIG_GEOM if n != "alexnet"])
+@pytest.mark.parametrize("name", list(CONFIG_GEOM))
 def test_tensor_core_conv_configs_within_tolerance(golden_configs, name):
     y, ref, dt, conv = _config_run(golden_configs, name, "")
     assert y.shape == ref.shape
@@ -114,7 +114,7 @@ def test_tensor_core_conv_configs_within_tolerance(golden_configs, name):
     assert err <= TOL[dt], f"{name}: normwise rel {err:.3e} > {TOL[dt]} (plan {conv.device_plan})"
 
 
-@pytest.mark.parametrize("name", [n for n in CONFIG_GEOM if n != "alexnet"])
+@pytest.mark.parametrize("name", list(CONFIG_GEOM))
 def test_tensor_core_conv_integer_data_exact(golden_configs, name):
     y, ref, dt, _ = _config_run(golden_configs, name, "i", out_dtype=torch.float32)
     np.testing.assert_array_equal(y, ref, err_msg=name)
@@ -255,3 +255,49 @@ def test_no_cpu_fallback_on_cpu_tensors():
     conv = wf.FoldedConv2d(torch.randn(3, 3, 3, 16, device="cuda").bfloat16(), None, (1, 32, 32, 3), padding=1)
     with pytest.raises(ValueError):
         conv(torch.randn(1, 32, 32, 3).bfloat16())
+
+
+@pytest.mark.parametrize("name", [n for n in CONFIG_GEOM if n != "r50_b1"])
+def test_unfolded_variant_configs(golden_configs, name):
+    """The same tcgen05 kernel on the UNFOLDED input (explicit im2col A tiles)."""
+    y, ref, dt, conv = _config_run(golden_configs, name, "", variant="unfolded")
+    assert conv.device_plan["producer"] == "im2col"
+    assert normrel(y, ref) <= TOL[dt], name
+    y, ref, _, _ = _config_run(golden_configs, name, "i", out_dtype=torch.float32, variant="unfolded")
+    np.testing.assert_array_equal(y, ref, err_msg=name)
+
+
+@pytest.mark.parametrize("name", [n for n in CONFIG_GEOM if n not in ("r50_b1", "alexnet")])
+def test_gather_producer_matches_tma_bitwise(golden_configs, name):
+    """The software-gather producer builds the same shared-memory A image as the TMA boxes."""
+    y0, _, _, conv = _config_run(golden_configs, name, "")
+    assert conv.device_plan["producer"] == "tma"
+    y1, _, _, _ = _config_run(golden_configs, name, "", flags=0x4000)
+    np.testing.assert_array_equal(y0, y1)
+
+
+def test_alexnet_full_geometry_sampled(oracle):
+    """227x227 (1362-byte rows, partial last folded pixel, OW=55 masked tail), batch 5."""
+    rng = np.random.default_rng(77)
+    x = torch.from_numpy(rng.uniform(-1, 1, (5, 227, 227, 3)).astype(np.float32)).cuda().bfloat16()
+    w = torch.from_numpy((rng.uniform(-1, 1, (11, 11, 3, 96)) / 18).astype(np.float32)).cuda().bfloat16()
+    b = torch.from_numpy(rng.uniform(-1, 1, (96,)).astype(np.float32)).cuda()
+    conv = wf.FoldedConv2d(w, b, x.shape, stride=4, padding=0, dtype=torch.bfloat16)
+    assert conv.device_plan["producer"] == "gather"
+    y = conv(x).float().cpu().numpy()
+    assert y.shape == (5, 55, 55, 96)
+    for i in (0, 4):
+        ref = oracle.conv_padded(x[i:i + 1].float().cpu().numpy(), w.float().cpu().numpy(), b.cpu().numpy(), 4, 0)
+        assert normrel(y[i:i + 1], ref) <= 1e-2
+    yu = wf.FoldedConv2d(w, b, x.shape, stride=4, padding=0, dtype=torch.bfloat16, variant="unfolded")(x)
+    assert normrel(yu.float().cpu().numpy(), y) <= 1e-2
+
+
+def test_unfolded_full_size_sampled(oracle):
+    rng = np.random.default_rng(12)
+    x = torch.from_numpy(rng.uniform(-1, 1, (3, 224, 224, 3)).astype(np.float32)).cuda().bfloat16()
+    w = torch.from_numpy((rng.uniform(-1, 1, (7, 7, 3, 64)) / 12).astype(np.float32)).cuda().bfloat16()
+    b = torch.from_numpy(rng.uniform(-1, 1, (64,)).astype(np.float32)).cuda()
+    y = wf.FoldedConv2d(w, b, x.shape, stride=2, padding=3, variant="unfolded")(x).float().cpu().numpy()
+    ref = oracle.conv_padded(x[2:3].float().cpu().numpy(), w.float().cpu().numpy(), b.cpu().numpy(), 2, 3)
+    assert normrel(y[2:3], ref) <= 1e-2

@@ -72,6 +72,7 @@ CONFIGS = {  # name: (input, filter, stride, pad, dtype) -- BASELINE.json config
     "vgg16": ([256, 224, 224, 3], [3, 3, 3, 64], 1, 1, "bf16"),
     "mnv2": ([1024, 224, 224, 3], [3, 3, 3, 32], 2, 1, "f16"),
     "r50_b8192": ([8192, 224, 224, 3], [7, 7, 3, 64], 2, 3, "bf16"),
+    "alexnet": ([512, 227, 227, 3], [11, 11, 3, 96], 4, 0, "bf16"),
 }
 
 
@@ -87,20 +88,40 @@ def test_device_plans_for_configs(name, oracle):
     assert (d["r"], d["c0"], d["kw_f"]) == (r, c0, kwf)
     assert plan["expanded_filter_shape"] == [filt[0], kwf, d["f"] * 3, r * filt[3]]
     oh = (shape[1] + 2 * p - filt[0]) // s + 1
+    assert d["producer"] == ("gather" if name == "alexnet" else "tma")
     assert d["useful_macs"] == wf.count_macs(shape, filt, s, s, p, p)
     assert d["useful_macs"] == shape[0] * oh * oh * filt[3] * filt[0] * filt[1] * 3
     assert d["issued_macs"] >= d["useful_macs"]
 
 
-def test_alexnet_plan_reports_reason():
-    # W = 227 is prime: no pure-reshape fold exists (the reference also says WidthNotDivisible)
+def test_alexnet_plan_uses_the_gather_producer():
+    # W = 227 is prime: no pure-reshape fold exists (the reference says WidthNotDivisible,
+    # src/fold.cpp:58) and the 1362-byte row pitch cannot be a TMA stride, so the
+    # generalized fold runs with the software-gather producer, a partial last
+    # folded pixel and a masked output tail (OW = 55, r = 2).
     plan = wf.plan_fold([512, 227, 227, 3], [11, 11, 3, 96], 4, 4, 0, 0, dtype="bf16")
-    assert plan["status"] == "fallback"
-    assert plan["reason"] in ("WidthNotDivisible", "FactorTooLarge")
+    assert plan["status"] == "apply", plan
+    d = plan["device"]
+    assert (d["f"], d["r"], d["producer"]) == (8, 2, "gather")
+    assert d["wf"] == 29 and d["wfo"] == 28 and d["ow"] == 55
+    ref = wf.check_legality([512, 227, 227, 3], [11, 11, 3, 96], 8, stride_h=4, stride_w=4)
+    assert ref["status"] == "fallback"  # the reference rule is unchanged
+
+
+def test_unfolded_variant_plan():
+    c = _core.FoldedConv([8, 224, 224, 3], [7, 7, 3, 64], 2, 2, 3, 3, "bf16", 0, 0, "unfolded")
+    d = c.device
+    assert d["variant"] == "unfolded" and d["producer"] == "im2col" and d["f"] == 1
+    assert d["mma_entries"] == 7 * 2  # 21-element window rows in two 16-element K-steps per kh
+    assert d["useful_macs"] == 8 * 112 * 112 * 64 * 7 * 7 * 3
+    assert c.output_shape == [8, 112, 112, 64]
+    with pytest.raises(ValueError):
+        _core.FoldedConv([8, 224, 224, 3], [7, 7, 3, 64], 2, 2, 3, 3, "bf16", 0, 0, "sideways")
 
 
 def test_generalized_legality_reasons():
-    assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=16)["reason"] == "WidthNotDivisible"
+    assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=16)["device"]["producer"] == "gather"
+    assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=4, dtype="tf32")["reason"] == "WidthNotDivisible"
     assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], 2, 3, factor=16)["reason"] == "StrideOnFoldAxis"
     assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], factor=4)["reason"] == "UnalignedPixel"
     with pytest.raises(wf.ShapeMismatchError):
