@@ -114,8 +114,11 @@ typedef struct {
                               of the output-column permutation baked into the
                               packed filter (coalesced 16x256b TMEM reads) */
   int32_t variant;         /* wf_variant */
-  int32_t producer;        /* A-tile producer: 0 TMA boxes, 1 software gather
-                              (any row pitch, W % f != 0), 2 explicit im2col */
+  int32_t producer;        /* A-tile producer: 0 TMA boxes on x, 1 row gather
+                              (folded layout), 2 row gather (explicit im2col),
+                              3 re-pitch x into the workspace, then TMA boxes */
+  int64_t pitched_w;       /* producer 3: workspace row width (>= W, % f == 0) */
+  int64_t workspace_bytes; /* device scratch wf_conv_fold_fwd_ws needs (0: none) */
   uint64_t useful_macs;    /* count_macs of the original conv */
   uint64_t issued_macs;    /* MACs the tensor cores execute (128-row tiles) */
 } wf_fold_plan;
@@ -158,6 +161,14 @@ wf_status wf_conv_fold_fwd(const void* x, const void* w_packed,
                            const float* b_rep, void* y,
                            const wf_conv_desc* desc, const wf_fold_plan* plan,
                            wf_dtype out_dtype, uint32_t epilogue, void* stream);
+
+/* Same, with the caller-owned device workspace plan->workspace_bytes long
+ * (producer 3: rows whose pitch is not a 16-byte multiple, e.g. AlexNet's
+ * 227-pixel rows, are re-pitched there first). wf_conv_fold_fwd is this call
+ * with workspace == NULL and fails with WF_INVALID_ARGUMENT for such plans. */
+wf_status wf_conv_fold_fwd_ws(const void* x, void* workspace, const void* w_packed, const float* b_rep, void* y,
+                              const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype,
+                              uint32_t epilogue, void* stream);
 
 /* Exact-order fp32 direct convolution on CUDA cores: widthfold::conv2d
  * (src/refconv.cpp:34-80) bit-for-bit (kh -> kw -> ci, no FMA) plus explicit

@@ -32,7 +32,7 @@ REASONS = [
 
 EXPORTED = [
     "wf_plan_fold", "wf_plan_unfolded", "wf_packed_filter_bytes", "wf_expand_filter_pack", "wf_expand_filter_dense",
-    "wf_conv_fold_fwd", "wf_set_num_sms", "wf_last_error", "wf_abi_version",
+    "wf_conv_fold_fwd", "wf_conv_fold_fwd_ws", "wf_set_num_sms", "wf_last_error", "wf_abi_version",
 ]
 
 
@@ -51,6 +51,7 @@ class FoldPlan(ctypes.Structure):
         ("units_per_px", c_int64), ("group_size", c_int64), ("n_groups", c_int64),
         ("n_tiles", c_int64), ("tile_rows", c_int64), ("wbox", c_int64), ("nrows", c_int64),
         ("mma_entries", c_int64), ("table_bytes", c_int64), ("packed_bytes", c_int64), ("epi_chunk", c_int64), ("variant", c_int32), ("producer", c_int32),
+        ("pitched_w", c_int64), ("workspace_bytes", c_int64),
         ("useful_macs", c_uint64), ("issued_macs", c_uint64),
     ]
 
@@ -93,6 +94,9 @@ def lib() -> ctypes.CDLL:
         L.wf_conv_fold_fwd.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, POINTER(ConvDesc),
                                        POINTER(FoldPlan), c_int, c_uint32, c_void_p]
         L.wf_conv_fold_fwd.restype = c_int
+        L.wf_conv_fold_fwd_ws.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(ConvDesc),
+                                          POINTER(FoldPlan), c_int, c_uint32, c_void_p]
+        L.wf_conv_fold_fwd_ws.restype = c_int
         L.wf_set_num_sms.argtypes = [c_int]
         L.wf_set_num_sms.restype = None
         L.wf_last_error.argtypes = []

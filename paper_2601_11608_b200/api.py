@@ -114,6 +114,9 @@ class FoldedConv2d:
             self.b_rep = torch.empty(self.core.cout_f, dtype=torch.float32, device=dev)
         self.core.pack(w.data_ptr(), _ptr(bf), self.packed.data_ptr(), _ptr(self.b_rep), _stream(dev))
         self._keep = (w, bf)
+        # re-pitched input (rows whose pitch is not TMA-addressable, e.g. AlexNet W=227)
+        self.workspace = (torch.empty(self.core.workspace_bytes, dtype=torch.uint8, device=dev)
+                          if self.core.workspace_bytes else None)
         self._geom = (sh, sw, ph, pw)
         self.output_shape = tuple(self.core.output_shape)
 
@@ -141,7 +144,8 @@ class FoldedConv2d:
             raise ShapeMismatchError("output buffer has the wrong shape/dtype/layout")
         use_bias = bias and self.b_rep is not None
         self.core.forward(x.data_ptr(), self.packed.data_ptr(), _ptr(self.b_rep) if use_bias else 0,
-                          out.data_ptr(), _OUT_NAME[out_dtype], use_bias, relu, _stream(x.device), _profile_flags)
+                          out.data_ptr(), _OUT_NAME[out_dtype], use_bias, relu, _stream(x.device), _profile_flags,
+                          _ptr(self.workspace))
         return out
 
 
@@ -157,6 +161,8 @@ class FoldedConv2d:
                                       self.core.device["group_size"] if self.variant == "fold" else 0, self.variant)
         if other.core.packed_bytes != self.core.packed_bytes:
             raise UnsupportedError("batch-specific plan changed the packed operand")
+        other.workspace = (torch.empty(other.core.workspace_bytes, dtype=torch.uint8, device=self.packed.device)
+                           if other.core.workspace_bytes else None)
         other.input_shape = shape
         other.output_shape = tuple(other.core.output_shape)
         return other

@@ -24,7 +24,7 @@ wf_status fail(wf_status st, const std::string& msg) {
 
 extern "C" {
 
-int wf_abi_version(void) { return 3; }
+int wf_abi_version(void) { return 4; }
 
 const char* wf_last_error(void) { return g_last_error.c_str(); }
 
@@ -80,20 +80,28 @@ wf_status wf_expand_filter_dense(const float* w, const wf_conv_desc* desc, int64
   return WF_OK;
 }
 
-wf_status wf_conv_fold_fwd(const void* x, const void* w_packed, const float* b_rep, void* y,
-                           const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype, uint32_t epilogue,
-                           void* stream) {
+wf_status wf_conv_fold_fwd_ws(const void* x, void* workspace, const void* w_packed, const float* b_rep, void* y,
+                              const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype,
+                              uint32_t epilogue, void* stream) {
   if (!x || !w_packed || !y || !desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
-  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0x7F00))  // 0x7F00: profiling / epilogue-mode switches
+  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0xFF00))  // 0xFF00: profiling / cross-check switches
     return fail(WF_INVALID_ARGUMENT, "unknown epilogue flags");
+  if (plan->workspace_bytes > 0 && !workspace && !(epilogue & 0x4000))
+    return fail(WF_INVALID_ARGUMENT, "this plan needs a workspace of plan->workspace_bytes (wf_conv_fold_fwd_ws)");
   wfb::Schedule S;
   std::string err;
   wf_status st = wfb::schedule_from_plan(*desc, *plan, &S, &err);
   if (st != WF_OK) return fail(st, err);
-  st = wfb::launch_conv(S, *desc, x, w_packed, b_rep, y, out_dtype, epilogue, static_cast<cudaStream_t>(stream),
-                        g_num_sms.load(), &err);
+  st = wfb::launch_conv(S, *desc, x, workspace, w_packed, b_rep, y, out_dtype, epilogue,
+                        static_cast<cudaStream_t>(stream), g_num_sms.load(), &err);
   if (st != WF_OK) return fail(st, err);
   return WF_OK;
+}
+
+wf_status wf_conv_fold_fwd(const void* x, const void* w_packed, const float* b_rep, void* y,
+                           const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype, uint32_t epilogue,
+                           void* stream) {
+  return wf_conv_fold_fwd_ws(x, nullptr, w_packed, b_rep, y, desc, plan, out_dtype, epilogue, stream);
 }
 
 wf_status wf_conv_direct_fwd(const float* x, const float* w, float* y, const wf_conv_desc* desc, void* stream) {

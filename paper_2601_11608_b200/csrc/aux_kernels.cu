@@ -8,16 +8,80 @@
 //                        grouped_conv (src/blockdiag.cpp:138-187), which the
 //                        reference guarantees bitwise equal to the dense conv.
 //   bias_add_kernel      widthfold::bias_add (src/refconv.cpp:82-95) (+ReLU).
+//   repitch_kernel       the device fold for rows whose pitch is not a 16-byte
+//                        multiple or whose width is not a multiple of f
+//                        (AlexNet: W=227, 1362-byte rows): copies x into a
+//                        workspace of pitch Wp*C (zero tail) so the folded view
+//                        is again a TMA-addressable reshape.
 //   blockdiag_check      BlockDiagFilter::from_expanded's strict-zero check
 //                        (src/blockdiag.cpp:24-84): any off-diagonal entry that
 //                        is not +-0.0f is an error.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdint>
 #include <string>
 
 #include "kernels.hpp"
 
 namespace wfb {
+
+// Out row r, 16-byte chunk k = in row r bytes [16k, 16k+16), zero past rb_in.
+// In rows are only element-aligned: two aligned 16-byte loads + funnel shift.
+__global__ void repitch_kernel(const uint8_t* __restrict__ x, uint8_t* __restrict__ y, long long rows, int rb_in,
+                               int rb_out) {
+  const int cpr = rb_out / 16;
+  const long long total = rows * cpr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cpr;
+    const int k = static_cast<int>(i - r * cpr);
+    const int o = 16 * k;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    if (o < rb_in) {
+      const uintptr_t addr = reinterpret_cast<uintptr_t>(x) + r * rb_in + o;
+      const uint32_t sh = static_cast<uint32_t>(addr & 15u);
+      const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(addr - sh));
+      uint32_t q[8] = {v0.x, v0.y, v0.z, v0.w, 0u, 0u, 0u, 0u};
+      if (sh != 0 && o + 16 - static_cast<int>(sh) < rb_in) {
+        const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(addr - sh + 16));
+        q[4] = v1.x; q[5] = v1.y; q[6] = v1.z; q[7] = v1.w;
+      }
+      const int ws = sh >> 2, bs = (sh & 3) * 8;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t lo = q[j + ws], hi = (j + ws + 1 < 8) ? q[j + ws + 1] : 0u;
+        w[j] = bs ? __funnelshift_r(lo, hi, bs) : lo;
+      }
+      if (o + 16 > rb_in) {  // zero the bytes past the input row
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t m = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (o + 4 * j + b < rb_in) m |= 0xFFu << (8 * b);
+          w[j] &= m;
+        }
+      }
+    }
+    *reinterpret_cast<uint4*>(y + r * rb_out + o) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+wf_status launch_repitch(const void* x, void* ws, long long rows, int rb_in, int rb_out, cudaStream_t st,
+                         std::string* err) {
+  const long long total = rows * (rb_out / 16);
+  const int threads = 256;
+  const int blocks = static_cast<int>(std::min<long long>((total + threads - 1) / threads, 148LL * 16));
+  repitch_kernel<<<blocks, threads, 0, st>>>(static_cast<const uint8_t*>(x), static_cast<uint8_t*>(ws), rows, rb_in,
+                                             rb_out);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("repitch_kernel: ") + cudaGetErrorString(e);
+    return WF_CUDA_ERROR;
+  }
+  return WF_OK;
+}
 
 __global__ void conv_direct_kernel(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y,
                                    int B, int H, int W, int C, int KH, int KW, int Co, int sh, int sw, int ph,

@@ -50,7 +50,7 @@ uint32_t pow2ceil(uint32_t v) {
 
 }  // namespace
 
-wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, const void* packed,
+wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, const void* workspace, const void* packed,
                       const float* b_rep, void* y, wf_dtype out_dtype, uint32_t epilogue, cudaStream_t st,
                       int num_sms, std::string* err) {
   const wf_fold_plan& p = S.plan;
@@ -154,7 +154,40 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   a.off_b = a.off_a + a.stages * a.stage_bytes + kTileM * 16;
   a.off_b = (a.off_b + 127) / 128 * 128;
   a.off_bias = a.off_b + S.b_smem_bytes;
-  const int smem = a.off_bias + kMaxAccCols * 4 + 1024;
+  // 0x4000 (profiling / cross-check): build the TMA-layout A tile with the row
+  // producer instead -- same shared-memory image, so results are bit-identical
+  const bool tf32 = (in_t == WF_TF32);
+  const int prod = ((S.prod == 0 || S.prod == 3) && (epilogue & 0x4000u) && !tf32) ? 1 : S.prod;
+  a.prod = prod;
+  a.off_raw = a.off_bias + kMaxAccCols * 4;
+  a.raw_slots = (prod == 1 || prod == 2) ? S.raw_slots : 0;
+  a.raw_slot_bytes = S.raw_slot_bytes;
+  if (prod == 1 && S.prod != 1) {  // forced: make room for the ring by dropping A stages
+    while (a.stages > 2 && a.off_raw + a.raw_slots * a.raw_slot_bytes + 1024 > kSmemLimit) {
+      --a.stages;
+      a.off_b = (a.off_a + a.stages * a.stage_bytes + kTileM * 16 + 127) / 128 * 128;
+      a.off_bias = a.off_b + S.b_smem_bytes;
+      a.off_raw = a.off_bias + kMaxAccCols * 4;
+    }
+  }
+  const int smem = a.off_raw + a.raw_slots * a.raw_slot_bytes + 1024;
+  a.rows_per_stage = 0;
+  a.log_wbox = 0;
+  while ((1 << a.log_wbox) < a.Wbox) ++a.log_wbox;
+  for (int b = 0; b < S.s && prod == 1; ++b) {  // folded raw rows of one stage (row producer)
+    if (!S.has_res[b]) continue;
+    const int rows = S.amax[b] - S.amin[b] + static_cast<int>(p.tile_rows);
+    for (int i = 0; i < rows; ++i) {
+      if (a.rows_per_stage >= kMaxStageRows) {
+        *err = "too many raw rows per stage for the row producer";
+        return WF_UNSUPPORTED;
+      }
+      a.row_b[a.rows_per_stage] = static_cast<signed char>(b);
+      a.row_i[a.rows_per_stage] = static_cast<signed char>(i);
+      a.row_a[a.rows_per_stage] = static_cast<signed char>(S.amin[b] + i);
+      ++a.rows_per_stage;
+    }
+  }
   if (smem > kSmemLimit) {
     *err = "shared-memory budget exceeded";
     return WF_UNSUPPORTED;
@@ -179,23 +212,36 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   a.ph = static_cast<int>(d.pad_h);
   a.pw = static_cast<int>(d.pad_w);
   a.total_px = static_cast<long long>(d.n) * p.oh * p.ow;
-  a.n_gather_chunks = (S.prod == 2) ? S.stage_bytes / 16 : S.s * a.Qr * a.NR * a.Wbox;
+  a.kh_count = static_cast<int>(d.kh);
+  a.n_img = static_cast<int>(d.n);
   a.ksplit = S.ksplit;
   if (S.ksplit > kMaxKsplit) {
     *err = "too many A sub-stages";
     return WF_UNSUPPORTED;
   }
   for (int k = 0; k < S.ksplit && S.ksplit > 1; ++k) {
+    a.ks_nkh[k] = (k + 1 < S.ksplit ? S.ks_kh0[k + 1] : static_cast<int>(d.kh)) - S.ks_kh0[k];
     a.ks_kh0[k] = S.ks_kh0[k];
     a.ks_entry0[k] = S.ks_entry0[k];
     a.ks_entries[k] = S.ks_entries[k];
-    a.ks_chunks[k] = S.ks_chunks[k];
   }
 
+  // ---- producer 3: re-pitch x into the workspace (16-byte rows, Wp % f == 0) ------
+  const void* xt = x;  // what the TMA boxes read
+  if (prod == 3) {
+    if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15u)) {
+      *err = "this plan needs a 16-byte aligned workspace of plan->workspace_bytes";
+      return WF_INVALID_ARGUMENT;
+    }
+    wf_status rs = launch_repitch(x, const_cast<void*>(workspace), d.n * d.h, static_cast<int>(d.w * d.c * es),
+                                  static_cast<int>(S.Wp * d.c * es), st, err);
+    if (rs != WF_OK) return rs;
+    xt = workspace;
+  }
   // ---- input tensor maps (one 5-D view per H-stride residue) --------------------
-  const cuuint64_t rowpitch = static_cast<cuuint64_t>(d.w) * d.c * es;
+  const cuuint64_t rowpitch = static_cast<cuuint64_t>(prod == 3 ? S.Wp : d.w) * d.c * es;
   const cuuint64_t pix = static_cast<cuuint64_t>(p.f) * d.c * es;
-  for (int b = 0; b < S.s && S.prod == 0; ++b) {
+  for (int b = 0; b < S.s && (prod == 0 || prod == 3); ++b) {
     if (!S.has_res[b]) continue;
     const cuuint64_t rows_b = static_cast<cuuint64_t>((d.h - b + S.s - 1) / S.s);
     cuuint64_t gdim[5] = {static_cast<cuuint64_t>(16 / es), static_cast<cuuint64_t>(p.wf), rows_b,
@@ -204,7 +250,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     cuuint32_t box[5] = {static_cast<cuuint32_t>(16 / es), static_cast<cuuint32_t>(p.wbox),
                          static_cast<cuuint32_t>(p.nrows), static_cast<cuuint32_t>(Q), 1};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    void* gaddr = const_cast<uint8_t*>(static_cast<const uint8_t*>(x) + b * rowpitch);
+    void* gaddr = const_cast<uint8_t*>(static_cast<const uint8_t*>(xt) + b * rowpitch);
     CUresult r = encode(&maps.in[b], tmap_type(in_t), 5, gaddr, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -221,16 +267,12 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
 
   const int grid = a.n_tiles * a.ctas_per_ntile;
   cudaError_t e;
-  const bool tf32 = (in_t == WF_TF32);
-  if (tf32 && (S.CH != 32 || S.prod != 0)) {
+  if (tf32 && (S.CH != 32 || prod == 1 || prod == 2)) {
     *err = "tf32 plans use 32-column epilogue chunks and the TMA producer";
     return WF_UNSUPPORTED;
   }
   const int kind = tf32 ? 1 : 0;
-  // 0x4000 (profiling / cross-check): build the TMA-layout A tile with the gather
-  // producer instead -- same shared-memory image, so results are bit-identical
-  const int prod = (S.prod == 0 && (epilogue & 0x4000u) && !tf32) ? 1 : S.prod;
-  if (prod == 0)
+  if (prod == 0 || prod == 3)
     e = launch_conv_prod<0>(a, maps, grid, smem, st, kind, out_dtype, S.CH);
   else if (prod == 1)
     e = launch_conv_prod<1>(a, maps, grid, smem, st, kind, out_dtype, S.CH);

@@ -10,7 +10,8 @@
 //   warp 0       producer. kProd 0: TMA -- per 128-row M tile one 5-D box per
 //                H-stride residue lands the canonical K-major core-matrix
 //                layout directly (plan.hpp explains the view), OOB = padding.
-//                kProd 1/2: with warps 10..11, a software gather (16-byte
+//                kProd 1/2: one bulk copy per raw input row into a slot
+//                ring; transposer warps 10..11 build the A tile from it (16-byte
 //                loads, any row alignment) builds the same folded layout
 //                (AlexNet's 1362-byte pitch) or an explicit im2col layout
 //                (the unfolded Cin=3 variant). Also bulk-copies the packed B.
@@ -25,6 +26,7 @@
 // resident in shared memory for the whole launch.
 #pragma once
 
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -36,8 +38,9 @@
 namespace wfb {
 
 constexpr int kMaxTable = 384;  // schedule entries per launch (constant bank)
-constexpr int kGatherWarps = 3;  // software-gather producer: warp 0 + warps 10, 11
+constexpr int kGatherWarps = 2;  // row-staged producer: transposer warps 10..11
 constexpr int kMaxKsplit = 8;    // A stages per M tile (im2col kh ranges)
+constexpr int kMaxStageRows = 64;  // folded raw rows per A stage (row producer)
 
 struct ConvArgs {
   const float* bias;  // replicated bias (r*Cout fp32) or nullptr
@@ -64,7 +67,13 @@ struct ConvArgs {
   long long pix_bytes;            // folded pixel f*C*elem
   int H, Q, Qr, NR;               // core cols per pixel, regions per residue (+shift), rows per region
   int lbo_a;                      // bytes between core-column regions
-  int n_gather_chunks;            // 16-byte chunks per A stage
+  int prod;                       // A producer (plan.hpp Schedule::prod)
+  int off_raw, raw_slots, raw_slot_bytes;  // staged-row ring (kProd 1/2)
+  int rows_per_stage;             // folded: raw rows per A stage
+  int log_wbox;                   // log2(Wbox)
+  signed char row_b[kMaxStageRows], row_i[kMaxStageRows], row_a[kMaxStageRows];  // folded stage rows
+  int kh_count, n_img;            // KH, N
+  int ks_nkh[kMaxKsplit];         // im2col: kh rows per sub-stage
   // A stages per M tile (im2col: kh ranges; folded: 1) and their MMA / chunk ranges
   int ksplit;
   int ks_kh0[kMaxKsplit], ks_entry0[kMaxKsplit], ks_entries[kMaxKsplit], ks_chunks[kMaxKsplit];
@@ -131,40 +140,151 @@ __device__ __forceinline__ void store_row(uint8_t* dst, const float (&v)[VPT]) {
   }
 }
 
-// Bytes [boff, boff+16) of an input row (any 2-byte alignment), bytes outside
-// [0, rb) read as zero (the conv padding). Loads only the 16-byte aligned
-// blocks that intersect the row.
-__device__ __forceinline__ uint4 load16_row(const uint8_t* row, long long boff, long long rb) {
-  if (boff >= rb || boff + 16 <= 0) return make_uint4(0u, 0u, 0u, 0u);
-  const uintptr_t addr = reinterpret_cast<uintptr_t>(row) + boff;
-  const uint32_t sh = static_cast<uint32_t>(addr & 15u);
-  const long long b0 = boff - sh;  // row offset of the first aligned block
+// ---- row-staged producer (kProd 1 / 2) -----------------------------------------
+// The loader (warp 0, one lane) bulk-copies every raw input row a stage needs
+// -- the 16-byte aligned superset [floor16(row), ceil16(row end)) -- into a
+// ring of shared-memory slots; the transposer warps (10..11) turn each staged
+// row into the stage's A layout with 16-byte shared-memory moves (funnel
+// shifts when the row is not 16-byte aligned, e.g. AlexNet's 1362-byte rows)
+// and zero-fill padding. Global memory is read once per row with one large
+// copy instead of 16-byte TMA box pieces.
+
+// Raw rows of one A stage, enumerated identically by the loader and the
+// transposers. Folded: row r = (residue row_b[r], region row row_i[r]),
+// input row (oh0 + row_a[r]) * s + row_b[r]. im2col: row r = (output row t of
+// the tile, kh of the sub-stage), r = t * nkh + (kh - kh0).
+// Scalars of the row producer, read from the kernel parameters ONCE into
+// registers: the shared-memory asm statements clobber "memory", so fields
+// read through `a` inside the loops would be re-fetched from the constant
+// bank every row (and the parameter block, with the MMA table, is larger
+// than the constant cache).
+struct RowProd {
+  const uint8_t* x;
+  long long in_img_bytes, total_px;
+  int rb, pix, prod, Wbox, lw, Q, Qr, c0, lbo, region_bytes, s, H, n_img, ohb, OHt, OH, OW, U, sw, pw, ph;
+  int rows_per_stage, ksplit, kh_count, raw_slots, raw_slot_bytes;
+  uint32_t row_tab;  // shared address of the folded stage-row table: b | i << 8 | a << 16
+};
+
+__device__ __forceinline__ RowProd row_prod(const ConvArgs& a, uint32_t row_tab) {
+  RowProd p;
+  p.x = a.x;
+  p.in_img_bytes = a.in_img_bytes;
+  p.total_px = a.total_px;
+  p.rb = static_cast<int>(a.in_row_bytes);
+  p.pix = static_cast<int>(a.pix_bytes);
+  p.prod = a.prod;
+  p.Wbox = a.Wbox;
+  p.lw = a.log_wbox;
+  p.Q = a.Q;
+  p.Qr = a.Qr;
+  p.c0 = a.c0;
+  p.lbo = a.lbo_a;
+  p.region_bytes = a.region_bytes;
+  p.s = a.s;
+  p.H = a.H;
+  p.n_img = a.n_img;
+  p.ohb = a.ohb;
+  p.OHt = a.OHt;
+  p.OH = a.OH;
+  p.OW = a.OW;
+  p.U = a.U;
+  p.sw = a.sw;
+  p.pw = a.pw;
+  p.ph = a.ph;
+  p.rows_per_stage = a.rows_per_stage;
+  p.ksplit = a.ksplit;
+  p.kh_count = a.kh_count;
+  p.raw_slots = a.raw_slots;
+  p.raw_slot_bytes = a.raw_slot_bytes;
+  p.row_tab = row_tab;
+  return p;
+}
+
+// Raw rows of one A stage, enumerated identically by the loader and the
+// transposers. Folded: row r = (residue b, region row i), input row
+// (oh0 + a) * s + b with a = amin[b] + i. im2col: row r = (output row t of the
+// tile, kh of the sub-stage), r = t * nkh + (kh - kh0).
+struct StageRows {
+  int count;       // rows in the stage
+  int n0, oh0;     // folded: image and first output row of the tile
+  long long g0;    // im2col: first global output row (n*OH + oh) of the tile
+  int kh0, nkh;    // im2col: kh range of the sub-stage
+};
+
+__device__ __forceinline__ StageRows stage_rows(const ConvArgs& a, const RowProd& p, int mt, int ks) {
+  StageRows sr;
+  if (p.prod == 1) {
+    sr.n0 = mt / p.ohb;
+    sr.oh0 = (mt - sr.n0 * p.ohb) * p.OHt;
+    sr.count = p.rows_per_stage;
+    sr.g0 = 0;
+    sr.kh0 = 0;
+    sr.nkh = 0;
+  } else {
+    sr.kh0 = (p.ksplit == 1) ? 0 : a.ks_kh0[ks];
+    sr.nkh = (p.ksplit == 1) ? p.kh_count : a.ks_nkh[ks];
+    const long long P0 = static_cast<long long>(mt) * 128;
+    const long long P1 = min(P0 + 127, p.total_px - 1);
+    sr.g0 = P0 / p.OW;
+    sr.count = static_cast<int>(P1 / p.OW - sr.g0 + 1) * sr.nkh;
+    sr.n0 = 0;
+    sr.oh0 = 0;
+  }
+  return sr;
+}
+
+// (image, input row) of stage row r; valid = inside the image (else zero-filled)
+__device__ __forceinline__ bool stage_row(const RowProd& p, const StageRows& sr, int r, int& n, int& ih) {
+  if (p.prod == 1) {
+    const uint32_t e = ptx::ld_shared_u32(p.row_tab + 4 * r);
+    n = sr.n0;
+    ih = (sr.oh0 + static_cast<int>(static_cast<int8_t>(e >> 16))) * p.s + static_cast<int>(e & 0xFF);
+  } else {
+    const int t = r / sr.nkh;
+    const long long g = sr.g0 + t;
+    n = static_cast<int>(g / p.OH);
+    const int oh = static_cast<int>(g - static_cast<long long>(n) * p.OH);
+    ih = oh * p.s - p.ph + sr.kh0 + (r - t * sr.nkh);
+  }
+  return ih >= 0 && ih < p.H && n < p.n_img;
+}
+
+// 16 bytes at row offset o of a staged row (slot holds the row from byte sh),
+// bytes outside [0, rb) read as zero.
+__device__ __forceinline__ uint4 raw16(uint32_t slot, int sh, int o, int rb) {
   const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-  const uint4 v0 = (b0 < rb && b0 + 16 > 0) ? __ldg(reinterpret_cast<const uint4*>(addr - sh)) : z;
-  uint32_t w0 = v0.x, w1 = v0.y, w2 = v0.z, w3 = v0.w;
-  if (sh != 0) {
-    const uint4 v1 = (b0 + 16 < rb) ? __ldg(reinterpret_cast<const uint4*>(addr - sh + 16)) : z;
-    uint32_t w4 = v1.x, w5 = v1.y, w6 = v1.z, w7 = v1.w;
-    if (sh & 8) { w0 = w2; w1 = w3; w2 = w4; w3 = w5; w4 = w6; w5 = w7; }
-    if (sh & 4) { w0 = w1; w1 = w2; w2 = w3; w3 = w4; w4 = w5; }
-    if (sh & 2) {
+  if (o >= rb || o + 16 <= 0) return z;
+  const int ad = sh + o;
+  const int a0 = ad & ~15;
+  const int s2 = ad - a0;
+  uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+  if (a0 >= 0) {
+    const uint4 v0 = ptx::ld_shared_v4(slot + a0);
+    w0 = v0.x; w1 = v0.y; w2 = v0.z; w3 = v0.w;
+  }
+  if (s2 != 0) {
+    uint32_t w4 = 0, w5 = 0, w6 = 0, w7 = 0;
+    if (a0 + 16 < sh + rb) {
+      const uint4 v1 = ptx::ld_shared_v4(slot + a0 + 16);
+      w4 = v1.x; w5 = v1.y; w6 = v1.z; w7 = v1.w;
+    }
+    if (s2 & 8) { w0 = w2; w1 = w3; w2 = w4; w3 = w5; w4 = w6; w5 = w7; }
+    if (s2 & 4) { w0 = w1; w1 = w2; w2 = w3; w3 = w4; w4 = w5; }
+    if (s2 & 2) {
       w0 = __funnelshift_r(w0, w1, 16); w1 = __funnelshift_r(w1, w2, 16);
       w2 = __funnelshift_r(w2, w3, 16); w3 = __funnelshift_r(w3, w4, 16);
     }
-    if (sh & 1) {  // byte-aligned rows only occur with 1-byte elements (not used)
-      w0 = __funnelshift_r(w0, w1, 8); w1 = __funnelshift_r(w1, w2, 8);
-      w2 = __funnelshift_r(w2, w3, 8); w3 = __funnelshift_r(w3, w4, 8);
-    }
   }
-  if (boff < 0 || boff + 16 > rb) {  // row edge: zero the bytes outside [0, rb)
+  if (o < 0 || o + 16 > rb) {  // row edge: zero the bytes outside [0, rb)
     uint32_t w[4] = {w0, w1, w2, w3};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       uint32_t m = 0;
 #pragma unroll
       for (int bb = 0; bb < 4; ++bb) {
-        const long long o = boff + 4 * k + bb;
-        if (o >= 0 && o < rb) m |= 0xFFu << (8 * bb);
+        const int oo = o + 4 * k + bb;
+        if (oo >= 0 && oo < rb) m |= 0xFFu << (8 * bb);
       }
       w[k] &= m;
     }
@@ -173,60 +293,60 @@ __device__ __forceinline__ uint4 load16_row(const uint8_t* row, long long boff, 
   return make_uint4(w0, w1, w2, w3);
 }
 
-// One A stage built by the gather warps: chunk d (16 bytes) of the stage.
-template <int kProd>
-__device__ __forceinline__ void gather_chunk(const ConvArgs& a, int d, int mt, int kh0, uint32_t& dst_off, uint4& v) {
-  if constexpr (kProd == 1) {
-    // folded layout, identical to the TMA boxes: [residue b][region q'][row i][folded col w''][16 B]
-    const int w2 = d % a.Wbox;
-    int t = d / a.Wbox;
-    const int i = t % a.NR;
-    t /= a.NR;
-    const int qq = t % a.Qr;
-    const int b = t / a.Qr;
-    dst_off = static_cast<uint32_t>(b * a.region_bytes + qq * a.lbo_a + (i * a.Wbox + w2) * 16);
-    const int n = mt / a.ohb;
-    const int oh0 = (mt - n * a.ohb) * a.OHt;
-    const int ih = (oh0 + a.amin[b] + i) * a.s + b;
-    if (!((a.res_mask >> b) & 1u) || ih < 0 || ih >= a.H) {
-      v = make_uint4(0u, 0u, 0u, 0u);
-      return;
+// Transpose one staged (or zero) raw row r of the stage into the A stage at `dst`.
+__device__ __forceinline__ void transpose_row(const RowProd& p, const StageRows& sr, int r, bool staged, int mt,
+                                              uint32_t dst, uint32_t slot, int sh, int lane) {
+  const int rb = p.rb, pix = p.pix;
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  if (p.prod == 1) {
+    // regions q' of residue b, region row i: chunk (q', w'') = folded pixel
+    // c0 + w'' (+1 for the shift region q' = Q), core column q' % Q
+    const uint32_t e = ptx::ld_shared_u32(p.row_tab + 4 * r);
+    const uint32_t rbase = dst + (e & 0xFF) * p.region_bytes + ((e >> 8) & 0xFF) * p.Wbox * 16;
+    const int nck = p.Qr << p.lw;
+    const int wmask = p.Wbox - 1;
+    // 16-byte aligned rows with 16-byte pixels: every chunk is one aligned
+    // shared-memory load, wholly inside or wholly outside the row
+    const bool fast = sh == 0 && (pix & 15) == 0 && (rb & 15) == 0;
+#pragma unroll 4
+    for (int c = lane; c < nck; c += 32) {
+      const int qq = c >> p.lw;
+      const int w2 = c & wmask;
+      const int o = (p.c0 + w2) * pix + ((qq == p.Q) ? pix : qq * 16);
+      uint4 v = z;
+      if (staged) {
+        if (fast) {
+          if (o >= 0 && o < rb) v = ptx::ld_shared_v4(slot + o);
+        } else {
+          v = raw16(slot, sh, o, rb);
+        }
+      }
+      ptx::st_shared_v4(rbase + qq * p.lbo + w2 * 16, v.x, v.y, v.z, v.w);
     }
-    const int shift = (qq == a.Q) ? 1 : 0;
-    const long long boff = static_cast<long long>(a.c0 + w2 + shift) * a.pix_bytes + (shift ? 0 : qq) * 16;
-    v = load16_row(a.x + n * a.in_img_bytes + ih * a.in_row_bytes, boff, a.in_row_bytes);
   } else {
-    // explicit im2col: [kh*U + u][core col cc][M row m][16 B]; row m = output pixel mt*128 + m
-    const int m = d & 127;
-    const int t = d >> 7;
-    const int cc = t & 1;
-    const int rg = t >> 1;
-    const int khl = rg / a.U;  // kh relative to the sub-stage
-    const int u = rg - khl * a.U;
-    const int kh = kh0 + khl;
-    dst_off = static_cast<uint32_t>(rg * 4096 + cc * 2048 + m * 16);
-    const long long P = static_cast<long long>(mt) * 128 + m;
-    if (P >= a.total_px) {
-      v = make_uint4(0u, 0u, 0u, 0u);
-      return;
+    // im2col: raw row (output row t of the tile, kh) feeds M rows m of that output row
+    const int t = r / sr.nkh;
+    const int kh = sr.kh0 + (r - t * sr.nkh);
+    const long long P0 = static_cast<long long>(mt) * 128;
+    const long long pr0 = (sr.g0 + t) * p.OW;  // first pixel of the output row
+    const int m_lo = static_cast<int>(max(pr0, P0) - P0);
+    const int m_hi = static_cast<int>(min(min(pr0 + p.OW, P0 + 128), p.total_px) - P0);
+    const uint32_t kbase = dst + (kh - sr.kh0) * p.U * 4096;
+    const int step = p.sw * pix;                                       // raw bytes between M rows
+    const int o0 = (static_cast<int>(P0 - pr0) * p.sw - p.pw) * pix;  // raw offset of M row 0
+    for (int uc = 0; uc < 2 * p.U; ++uc) {
+      const uint32_t ubase = kbase + (uc >> 1) * 4096 + (uc & 1) * 2048;
+#pragma unroll 4
+      for (int m = m_lo + lane; m < m_hi; m += 32) {
+        const uint4 v = staged ? raw16(slot, sh, o0 + m * step + uc * 16, rb) : z;
+        ptx::st_shared_v4(ubase + m * 16, v.x, v.y, v.z, v.w);
+      }
     }
-    const long long per_img = static_cast<long long>(a.OH) * a.OW;
-    const int n = static_cast<int>(P / per_img);
-    const int rem = static_cast<int>(P - n * per_img);
-    const int oh = rem / a.OW;
-    const int ow = rem - oh * a.OW;
-    const int ih = oh * a.s - a.ph + kh;
-    if (ih < 0 || ih >= a.H) {
-      v = make_uint4(0u, 0u, 0u, 0u);
-      return;
-    }
-    const long long boff = static_cast<long long>(ow * a.sw - a.pw) * a.pix_bytes + (2 * u + cc) * 16;
-    v = load16_row(a.x + n * a.in_img_bytes + ih * a.in_row_bytes, boff, a.in_row_bytes);
   }
 }
 
 template <int kKind, typename OutT, int CH, int kProd>
-__global__ void __launch_bounds__(kProd == 0 ? 320 : 384, 1)
+__global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     conv_fold_kernel(const __grid_constant__ ConvArgs a, const __grid_constant__ TmaMaps maps) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
@@ -238,6 +358,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 384, 1)
   const uint32_t bar_tfull = base + 128;   // [2] x 8 B
   const uint32_t bar_tempty = base + 144;  // [2] x 8 B
   const uint32_t bar_b = base + 160;
+  const uint32_t bar_raw_full = base + 256;   // [raw_slots <= 32] x 8 B
+  const uint32_t bar_raw_empty = base + 512;  // [raw_slots <= 32] x 8 B
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + 192);
 
   // warp index via shuffle so the compiler knows it is warp-uniform (keeps the
@@ -249,6 +371,11 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 384, 1)
   const int ncols = a.nt_cols[ntile];
   const int col0 = a.nt_col0[ntile];
 
+  if (kProd == 1)  // folded stage-row table of the row producer (b | i << 8 | a << 16)
+    for (int r = threadIdx.x; r < a.rows_per_stage; r += blockDim.x)
+      reinterpret_cast<uint32_t*>(gbase + 768)[r] = static_cast<uint32_t>(static_cast<uint8_t>(a.row_b[r])) |
+                                                    (static_cast<uint32_t>(static_cast<uint8_t>(a.row_i[r])) << 8) |
+                                                    (static_cast<uint32_t>(static_cast<uint8_t>(a.row_a[r])) << 16);
   {  // bias slice of this N-tile into shared memory
     float* sbias = reinterpret_cast<float*>(gbase + a.off_bias);
     const bool has_bias = (a.bias != nullptr) && (a.epi_flags & WF_EPI_BIAS);
@@ -256,7 +383,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 384, 1)
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
-      mbar_init(bar_full + 8 * i, kProd == 0 ? 1 : kGatherWarps);  // TMA: one expect_tx; gather: one arrive per warp
+      mbar_init(bar_full + 8 * i, kProd == 0 ? 1 : kGatherWarps);  // TMA: one expect_tx; rows: one arrive per transposer
       mbar_init(bar_empty + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -264,6 +391,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 384, 1)
       mbar_init(bar_tempty + 8 * i, 256);
     }
     mbar_init(bar_b, 1);
+    for (int i = 0; i < a.raw_slots; ++i) {
+      mbar_init(bar_raw_full + 8 * i, 1);
+      mbar_init(bar_raw_empty + 8 * i, 1);
+    }
     fence_barrier_init();
   }
   if (kProd == 0 && warp == 0 && lane == 0) {
@@ -280,50 +411,83 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 384, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (kProd != 0 && (warp == 0 || warp >= 10)) {
-    // ===================== gather producer (warps 0, 10, 11) =====================
-    // Builds each A stage with 16-byte global loads (any row alignment,
-    // zero-filled padding) and st.shared; rows of AlexNet's 1362-byte pitch
-    // and the explicit im2col of the unfolded variant cannot be TMA boxes.
-    if (warp == 0 && elect_one()) {
-      const uint8_t* gb = reinterpret_cast<const uint8_t*>(a.nt_bsrc[ntile]);
-      const int bb = a.nt_bbytes[ntile];
-      mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
-      for (int off = 0; off < bb; off += 32768)
-        bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
-    }
-    __syncwarp();
-    constexpr int NGT = kGatherWarps * 32;
-    const int gt = (warp == 0 ? 0 : warp - 9) * 32 + lane;  // 0..NGT-1
-    int it = 0;
-    for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile) {
-      for (int ks = 0; ks < a.ksplit; ++ks, ++it) {  // im2col: kh ranges of one M tile
-        const int stage = it % a.stages;
-        const uint32_t round = static_cast<uint32_t>(it / a.stages);
-        mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
-        const uint32_t dst = base + a.off_a + stage * a.stage_bytes;
-        const int nch = (a.ksplit == 1) ? a.n_gather_chunks : a.ks_chunks[ks];
-        const int kh0 = (a.ksplit == 1) ? 0 : a.ks_kh0[ks];
-        if (!(a.epi_flags & 0x1000)) {
-          int d = gt;
-          for (; d + 3 * NGT < nch; d += 4 * NGT) {  // 4 loads in flight per thread
-            uint32_t o[4];
-            uint4 v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) gather_chunk<kProd>(a, d + k * NGT, mt, kh0, o[k], v[k]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) st_shared_v4(dst + o[k], v[k].x, v[k].y, v[k].z, v[k].w);
+    // ===================== row-staged producer =====================
+    // warp 0 (one lane): B operand, then one bulk copy per raw input row into
+    // the slot ring; warps 10..12: transpose staged rows into the A stages.
+    const uint32_t ring = base + a.off_raw;
+    const RowProd rp = row_prod(a, base + 768);
+    if (warp == 0) {
+      if (elect_one()) {
+        const uint8_t* gb = reinterpret_cast<const uint8_t*>(a.nt_bsrc[ntile]);
+        const int bb = a.nt_bbytes[ntile];
+        mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
+        for (int off = 0; off < bb; off += 32768)
+          bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
+        int slot_it = 0;
+        const bool no_loads = (a.epi_flags & 0x1000) != 0;
+        for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile)
+          for (int ks = 0; ks < rp.ksplit; ++ks) {
+            const StageRows sr = stage_rows(a, rp, mt, ks);
+            for (int r = 0; r < sr.count; ++r) {  // every row takes a slot; padding rows carry no bytes
+              int n, ih;
+              const bool staged = stage_row(rp, sr, r, n, ih) && !no_loads;
+              const int slot = slot_it % rp.raw_slots;
+              const uint32_t round = static_cast<uint32_t>(slot_it / rp.raw_slots);
+              ++slot_it;
+              mbar_wait(bar_raw_empty + 8 * slot, (round & 1u) ^ 1u);
+              if (!staged) {
+                mbar_arrive(bar_raw_full + 8 * slot);
+                continue;
+              }
+              const uintptr_t src = reinterpret_cast<uintptr_t>(rp.x + n * rp.in_img_bytes + static_cast<long long>(ih) * rp.rb);
+              const uintptr_t s0 = src & ~static_cast<uintptr_t>(15);
+              const uintptr_t s1 = (src + rp.rb + 15) & ~static_cast<uintptr_t>(15);
+              const uint32_t bytes = static_cast<uint32_t>(s1 - s0);
+              mbar_arrive_expect_tx(bar_raw_full + 8 * slot, bytes);
+              bulk_g2s(ring + slot * rp.raw_slot_bytes, reinterpret_cast<const void*>(s0), bytes, bar_raw_full + 8 * slot);
+            }
           }
-          for (; d < nch; d += NGT) {
-            uint32_t o;
-            uint4 v;
-            gather_chunk<kProd>(a, d, mt, kh0, o, v);
-            st_shared_v4(dst + o, v.x, v.y, v.z, v.w);
-          }
-        }
-        fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05 (async proxy)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_full + 8 * stage);
       }
+      __syncwarp();
+    } else {
+      const int tw = warp - 10;  // transposer 0..kGatherWarps-1
+      const bool dbg = (a.epi_flags & 0x8000) && blockIdx.x == 0 && tw == 0 && lane == 0;
+      long long t_empty = 0, t_full = 0, t_work = 0, t0 = 0;
+      int it = 0, slot_it = 0;
+      const bool no_loads = (a.epi_flags & 0x1000) != 0;
+      const int nstages = a.stages, stage_bytes = a.stage_bytes;
+      const uint32_t a_base = base + a.off_a;
+      for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile) {
+        for (int ks = 0; ks < rp.ksplit; ++ks, ++it) {
+          const int stage = it % nstages;
+          const uint32_t round = static_cast<uint32_t>(it / nstages);
+          const StageRows sr = stage_rows(a, rp, mt, ks);
+          if (dbg) t0 = clock64();
+          mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
+          if (dbg) t_empty += clock64() - t0;
+          const uint32_t dst = a_base + stage * stage_bytes;
+          for (int r = tw; r < sr.count; r += kGatherWarps) {  // rows dealt round-robin to the transposers
+            int n, ih;
+            const bool staged = stage_row(rp, sr, r, n, ih) && !no_loads;
+            const int slot = (slot_it + r) % rp.raw_slots;
+            if (dbg) t0 = clock64();
+            mbar_wait(bar_raw_full + 8 * slot, static_cast<uint32_t>((slot_it + r) / rp.raw_slots) & 1u);
+            if (dbg) { const long long t1 = clock64(); t_full += t1 - t0; t0 = t1; }
+            const uintptr_t src = reinterpret_cast<uintptr_t>(rp.x + n * rp.in_img_bytes + static_cast<long long>(ih) * rp.rb);
+            transpose_row(rp, sr, r, staged, mt, dst, ring + slot * rp.raw_slot_bytes, static_cast<int>(src & 15u),
+                          lane);
+            __syncwarp();
+            if (dbg) t_work += clock64() - t0;
+            if (lane == 0) mbar_arrive(bar_raw_empty + 8 * slot);
+          }
+          slot_it += sr.count;
+          fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05 (async proxy)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_full + 8 * stage);
+        }
+      }
+      if (dbg) printf("transposer0 cta0: stages %d  wait-empty %lld  wait-row %lld  transpose %lld cycles\n", it,
+                      t_empty, t_full, t_work);
     }
   } else if (warp == 0) {
     // ===================== TMA producer (one elected lane) =====================
@@ -535,7 +699,7 @@ cudaError_t launch_typed(const ConvArgs& args, const TmaMaps& maps, int grid, in
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  kern<<<grid, kProd == 0 ? 320 : 384, smem, st>>>(args, maps);
+  kern<<<grid, kProd == 0 ? 320 : 320 + 32 * kGatherWarps, smem, st>>>(args, maps);
   return cudaGetLastError();
 }
 

@@ -47,7 +47,8 @@ py::dict raw_dict(const wf_fold_plan& p) {
   d["tile_rows"] = p.tile_rows; d["wbox"] = p.wbox; d["nrows"] = p.nrows; d["mma_entries"] = p.mma_entries;
   d["packed_bytes"] = p.packed_bytes; d["epi_chunk"] = p.epi_chunk;
   d["variant"] = p.variant == WF_VARIANT_UNFOLDED ? "unfolded" : "fold";
-  d["producer"] = p.producer == 0 ? "tma" : (p.producer == 1 ? "gather" : "im2col"); d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
+  d["producer"] = p.producer == 0 ? "tma" : (p.producer == 1 ? "gather" : (p.producer == 2 ? "im2col" : "repitch+tma"));
+  d["pitched_w"] = p.pitched_w; d["workspace_bytes"] = p.workspace_bytes; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
   return d;
 }
 
@@ -208,11 +209,14 @@ PYBIND11_MODULE(_core, m) {
       .def(
           "forward",
           [](const wf::FoldedConv& c, std::uintptr_t x, std::uintptr_t packed, std::uintptr_t brep, std::uintptr_t y,
-             const std::string& out_dtype, bool bias, bool relu, std::uintptr_t stream, std::uint32_t flags) {
+             const std::string& out_dtype, bool bias, bool relu, std::uintptr_t stream, std::uint32_t flags,
+             std::uintptr_t workspace) {
             const wf::Dtype od = dtype_of(out_dtype);
             py::gil_scoped_release nogil;
-            c.forward(P(x), P(packed), brep ? F(brep) : nullptr, P(y), od, bias, relu, P(stream), flags);
+            c.forward(P(x), P(packed), brep ? F(brep) : nullptr, P(y), od, bias, relu, P(stream), flags,
+                      workspace ? P(workspace) : nullptr);
           },
           py::arg("x"), py::arg("packed"), py::arg("b_rep"), py::arg("y"), py::arg("out_dtype"), py::arg("bias"),
-          py::arg("relu"), py::arg("stream"), py::arg("profile_flags") = 0);
+          py::arg("relu"), py::arg("stream"), py::arg("profile_flags") = 0, py::arg("workspace") = 0)
+      .def_property_readonly("workspace_bytes", &wf::FoldedConv::workspace_bytes);
 }

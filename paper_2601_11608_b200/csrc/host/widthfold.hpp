@@ -137,6 +137,9 @@ class FoldedConv {
   FoldedConv(const ConvSpec& spec, Dtype in_dtype, std::int64_t factor = 0, std::int64_t group_size = 0,
              Variant variant = Variant::Fold);
   std::size_t packed_bytes() const;
+  // Device scratch forward() needs (re-pitched input when W's row pitch is not
+  // TMA-addressable, e.g. AlexNet's 227-pixel rows); 0 for zero-copy folds.
+  std::size_t workspace_bytes() const { return static_cast<std::size_t>(raw_.workspace_bytes); }
   std::int64_t cout_f() const { return raw_.cout_f; }
   const wf_fold_plan& raw() const { return raw_; }
   const FoldPlan& plan() const { return plan_; }
@@ -146,7 +149,7 @@ class FoldedConv {
   void pack(const void* w, const float* b, void* packed, float* b_rep, void* stream) const;
   // y = ReLU?(conv(x) + b?) ; x in in_dtype, y in out_dtype, NHWC.
   void forward(const void* x, const void* packed, const float* b_rep, void* y, Dtype out_dtype, bool bias, bool relu,
-               void* stream, std::uint32_t profile_flags = 0) const;
+               void* stream, std::uint32_t profile_flags = 0, void* workspace = nullptr) const;
 
  private:
   ConvSpec spec_;

@@ -19,8 +19,8 @@ wf_status launch_expand_dense(const wf_conv_desc& d, int64_t f, const float* w, 
                               cudaStream_t st, std::string* err);
 
 // K2: the folded implicit-GEMM convolution (TMA -> tcgen05.mma -> TMEM -> epilogue).
-wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, const void* packed,
-                      const float* b_rep, void* y, wf_dtype out_dtype, uint32_t epilogue,
+wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, const void* workspace,
+                      const void* packed, const float* b_rep, void* y, wf_dtype out_dtype, uint32_t epilogue,
                       cudaStream_t st, int num_sms, std::string* err);
 
 // Exact-order fp32 direct conv (reference conv2d semantics, with padding).
@@ -30,6 +30,9 @@ wf_status launch_bias_add(const float* y, const float* b, float* out, long long 
                           std::string* err);
 wf_status launch_blockdiag_check(const float* wd, int KH, int KW, int Cif, int Cof, int groups,
                                  unsigned long long* scratch, long long* first_bad, cudaStream_t st, std::string* err);
+// Device fold for unaligned rows: copy x (rows of rb_in bytes) into ws (rows of rb_out, zero tail).
+wf_status launch_repitch(const void* x, void* ws, long long rows, int rb_in, int rb_out, cudaStream_t st,
+                         std::string* err);
 wf_status launch_replicate_bias(const float* b, int cout, int r, float* out, cudaStream_t st, std::string* err);
 
 }  // namespace wfb

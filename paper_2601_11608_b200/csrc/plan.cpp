@@ -120,11 +120,18 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   const int64_t kwf = floor_div(f - sw - d.pad_w + d.kw - 1, f) - c0 + 1;
   // W % f != 0: the last folded pixel is partial (zero-filled by the gather
   // producer); OW % r != 0: the last folded output column is masked per j.
-  const int64_t Wf = ceil_div(d.w, f), Wfo = ceil_div(OW, r);
+  int64_t Wf = ceil_div(d.w, f);
+  const int64_t Wfo = ceil_div(OW, r);
   // TMA boxes need the folded view to be a pure reshape with a 16-byte row
-  // pitch; otherwise (AlexNet: W=227, 1362-byte rows) the software gather.
-  S.prod = (d.w % f == 0 && (d.w * d.c * S.esize) % 16 == 0) ? 0 : 1;
-  if (S.prod != 0 && in_dtype == WF_TF32) { S.plan = fallback(WF_REASON_WIDTH_NOT_DIVISIBLE, f); *out = S; return WF_OK; }
+  // pitch. When W % f != 0 or the row pitch is not a 16-byte multiple (AlexNet:
+  // W=227, 1362-byte rows)
+  // pitch, the input is first re-pitched into a workspace of Wp columns
+  // (Wp % f == 0, 16-byte rows, zero tail; producer 3) and then read by TMA.
+  int64_t Wp = d.w;
+  while (Wp % f != 0 || (Wp * d.c * S.esize) % 16 != 0) ++Wp;
+  S.Wp = Wp;
+  S.prod = (Wp == d.w) ? 0 : 3;
+  Wf = Wp / f;
   const int64_t Q = f * d.c * S.esize / 16;  // core columns per folded pixel
   S.Q = static_cast<int>(Q);
   const int64_t E2 = S.E / 2;                  // elements per core column
@@ -155,6 +162,12 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   // for the TMA destination: pad rows so NR*Wbox*16 % 128 == 0
   while ((NR * Wbox) % 8 != 0) ++NR;
   if (NR > 256) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
+  if (S.prod == 1) {  // the row producer enumerates a stage's raw rows in a 64-entry table
+    int64_t rows = 0;
+    for (int b = 0; b < sh; ++b)
+      if (S.has_res[b]) rows += S.amax[b] - S.amin[b] + OHt;
+    if (rows > 64) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
+  }
 
   // ---- MMA groups ---------------------------------------------------------
   int64_t gs = gs_req;
@@ -239,7 +252,8 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
     }
     const int64_t table_b = max_entries * 16;
     (void)table_b;  // the schedule lives in the kernel's constant bank
-    const int64_t fixed = ctrl_bytes + staging + a_pad + 128 + (max_b + 127) / 128 * 128 + bias_bytes + 1024;
+    const int64_t ring = (S.prod == 1 || S.prod == 2) ? static_cast<int64_t>(kRawSlots) * raw_slot_bytes_for(d.w * d.c * S.esize) : 0;
+    const int64_t fixed = ctrl_bytes + staging + a_pad + 128 + (max_b + 127) / 128 * 128 + bias_bytes + ring + 1024;
     int stages = 0;
     for (int st2 = 4; st2 >= 2; --st2)
       if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { stages = st2; break; }
@@ -398,8 +412,12 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   p.table_bytes = (p.mma_entries * 16 + G * 4 + 127) / 128 * 128;
   p.packed_bytes = p.table_bytes + b_cursor;
   p.epi_chunk = S.CH;
+  S.raw_slots = kRawSlots;
+  S.raw_slot_bytes = raw_slot_bytes_for(d.w * d.c * S.esize);
   p.variant = WF_VARIANT_FOLD;
   p.producer = S.prod;
+  p.pitched_w = (S.prod == 3) ? S.Wp : 0;
+  p.workspace_bytes = (S.prod == 3) ? d.n * d.h * S.Wp * d.c * S.esize : 0;
   S.ohb = ceil_div(OH, OHt);
   S.num_mtiles = d.n * S.ohb;
   p.useful_macs = static_cast<uint64_t>(d.n) * OH * OW * d.cout * d.kh * d.kw * d.c;
@@ -444,7 +462,10 @@ wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Sched
   // tile's K into ksplit sub-stages (AlexNet: 11 kh x 3 K-steps = 132 KB)
   const int64_t region = 2 * kTileM * 16;  // one (kh, K-step) view
   const int64_t b_total = d.kh * U * d.cout * 32;
-  const int64_t fixed0 = 1024 + kTileM * 16 + 128 + (b_total + 127) / 128 * 128 + kMaxAccCols * 4 + 1024;
+  S.raw_slots = kRawSlots;
+  S.raw_slot_bytes = raw_slot_bytes_for(d.w * d.c * S.esize);
+  const int64_t fixed0 = 1024 + kTileM * 16 + 128 + (b_total + 127) / 128 * 128 + kMaxAccCols * 4 +
+                         static_cast<int64_t>(S.raw_slots) * S.raw_slot_bytes + 1024;
   int64_t ksplit = 1;
   while (ksplit < 8 && fixed0 + 2 * ceil_div(d.kh, ksplit) * U * region > kSmemLimit) ++ksplit;
   const int64_t khs = ceil_div(d.kh, ksplit);

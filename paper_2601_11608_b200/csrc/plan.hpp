@@ -48,6 +48,8 @@ constexpr int kMaxResidues = 8;
 constexpr int kMaxNTiles = 16;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kStagingBytes = 0;  // epilogue writes straight from registers (no staging)
+constexpr int kRawSlots = 16;     // staged-row ring slots (row producer)
+inline int raw_slot_bytes_for(int64_t row_bytes) { return static_cast<int>((row_bytes + 32 + 127) / 128 * 128); }
 
 // Output-column permutation inside an epilogue chunk of CH accumulator
 // columns. tcgen05.ld.16x256b hands thread t of a warp the columns
@@ -89,9 +91,12 @@ struct Schedule {
   bool need_shift = false;       // some unit pairs (Q-1, next pixel's 0)
   int Ng = 64;                   // accumulator columns per group
   int CH = 64;                   // epilogue chunk (columns per 16x256b TMEM read)
-  int prod = 0;                  // A producer: 0 TMA boxes, 1 gather (folded), 2 gather (im2col)
+  int prod = 0;                  // A producer: 0 TMA boxes, 1 row gather (folded), 2 row gather
+                                 // (im2col), 3 re-pitch into the workspace + TMA boxes
+  int64_t Wp = 0;                // input width the TMA view uses (re-pitched when != W)
   int U = 0;                     // im2col: 32-byte K-steps per kh
   int ksplit = 1;                // A stages per M tile (im2col: kh ranges)
+  int raw_slots = 0, raw_slot_bytes = 0;  // staged-row ring of the row producer (prod 1/2)
   std::vector<int> ks_kh0, ks_entry0, ks_entries, ks_chunks;
   int amin[kMaxResidues] = {0};
   int amax[kMaxResidues] = {0};

@@ -88,21 +88,22 @@ def test_device_plans_for_configs(name, oracle):
     assert (d["r"], d["c0"], d["kw_f"]) == (r, c0, kwf)
     assert plan["expanded_filter_shape"] == [filt[0], kwf, d["f"] * 3, r * filt[3]]
     oh = (shape[1] + 2 * p - filt[0]) // s + 1
-    assert d["producer"] == ("gather" if name == "alexnet" else "tma")
+    assert d["producer"] == ("repitch+tma" if name == "alexnet" else "tma")
     assert d["useful_macs"] == wf.count_macs(shape, filt, s, s, p, p)
     assert d["useful_macs"] == shape[0] * oh * oh * filt[3] * filt[0] * filt[1] * 3
     assert d["issued_macs"] >= d["useful_macs"]
 
 
-def test_alexnet_plan_uses_the_gather_producer():
+def test_alexnet_plan_repitches_then_uses_tma():
     # W = 227 is prime: no pure-reshape fold exists (the reference says WidthNotDivisible,
     # src/fold.cpp:58) and the 1362-byte row pitch cannot be a TMA stride, so the
-    # generalized fold runs with the software-gather producer, a partial last
-    # folded pixel and a masked output tail (OW = 55, r = 2).
+    # generalized fold re-pitches x into a 232-pixel workspace (zero tail) on the
+    # device, then runs the TMA path with a masked output tail (OW = 55, r = 2).
     plan = wf.plan_fold([512, 227, 227, 3], [11, 11, 3, 96], 4, 4, 0, 0, dtype="bf16")
     assert plan["status"] == "apply", plan
     d = plan["device"]
-    assert (d["f"], d["r"], d["producer"]) == (8, 2, "gather")
+    assert (d["f"], d["r"], d["producer"]) == (8, 2, "repitch+tma")
+    assert d["pitched_w"] == 232 and d["workspace_bytes"] == 512 * 227 * 232 * 3 * 2
     assert d["wf"] == 29 and d["wfo"] == 28 and d["ow"] == 55
     ref = wf.check_legality([512, 227, 227, 3], [11, 11, 3, 96], 8, stride_h=4, stride_w=4)
     assert ref["status"] == "fallback"  # the reference rule is unchanged
@@ -120,8 +121,8 @@ def test_unfolded_variant_plan():
 
 
 def test_generalized_legality_reasons():
-    assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=16)["device"]["producer"] == "gather"
-    assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=4, dtype="tf32")["reason"] == "WidthNotDivisible"
+    assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=16)["device"]["producer"] == "repitch+tma"
+    assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=4, dtype="tf32")["device"]["pitched_w"] == 32
     assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], 2, 3, factor=16)["reason"] == "StrideOnFoldAxis"
     assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], factor=4)["reason"] == "UnalignedPixel"
     with pytest.raises(wf.ShapeMismatchError):
