@@ -38,7 +38,7 @@
 namespace wfb {
 
 constexpr int kMaxTable = 384;  // schedule entries per launch (constant bank)
-constexpr int kGatherWarps = 2;  // row-staged producer: transposer warps 10..11
+constexpr int kGatherWarps = 4;  // row-staged producer: transposer warps 10..13
 constexpr int kMaxKsplit = 8;    // A stages per M tile (im2col kh ranges)
 constexpr int kMaxStageRows = 64;  // folded raw rows per A stage (row producer)
 
@@ -149,10 +149,6 @@ __device__ __forceinline__ void store_row(uint8_t* dst, const float (&v)[VPT]) {
 // and zero-fill padding. Global memory is read once per row with one large
 // copy instead of 16-byte TMA box pieces.
 
-// Raw rows of one A stage, enumerated identically by the loader and the
-// transposers. Folded: row r = (residue row_b[r], region row row_i[r]),
-// input row (oh0 + row_a[r]) * s + row_b[r]. im2col: row r = (output row t of
-// the tile, kh of the sub-stage), r = t * nkh + (kh - kh0).
 // Scalars of the row producer, read from the kernel parameters ONCE into
 // registers: the shared-memory asm statements clobber "memory", so fields
 // read through `a` inside the loops would be re-fetched from the constant
@@ -166,37 +162,51 @@ struct RowProd {
   uint32_t row_tab;  // shared address of the folded stage-row table: b | i << 8 | a << 16
 };
 
+// Launders a parameter value through a register: without it the compiler
+// re-reads the field from the constant bank at every use (cheap to encode,
+// but ~20+ cycles of latency on the transposers' serial per-row path).
+__device__ __forceinline__ int opq(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ long long opq64(long long v) {
+  long long r;
+  asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(v));
+  return r;
+}
+
 __device__ __forceinline__ RowProd row_prod(const ConvArgs& a, uint32_t row_tab) {
   RowProd p;
-  p.x = a.x;
-  p.in_img_bytes = a.in_img_bytes;
-  p.total_px = a.total_px;
-  p.rb = static_cast<int>(a.in_row_bytes);
-  p.pix = static_cast<int>(a.pix_bytes);
+  p.x = reinterpret_cast<const uint8_t*>(opq64(reinterpret_cast<long long>(a.x)));
+  p.in_img_bytes = opq64(a.in_img_bytes);
+  p.total_px = opq64(a.total_px);
+  p.rb = opq(static_cast<int>(a.in_row_bytes));
+  p.pix = opq(static_cast<int>(a.pix_bytes));
   p.prod = a.prod;
-  p.Wbox = a.Wbox;
-  p.lw = a.log_wbox;
-  p.Q = a.Q;
-  p.Qr = a.Qr;
-  p.c0 = a.c0;
-  p.lbo = a.lbo_a;
-  p.region_bytes = a.region_bytes;
-  p.s = a.s;
-  p.H = a.H;
-  p.n_img = a.n_img;
-  p.ohb = a.ohb;
-  p.OHt = a.OHt;
-  p.OH = a.OH;
-  p.OW = a.OW;
-  p.U = a.U;
-  p.sw = a.sw;
-  p.pw = a.pw;
-  p.ph = a.ph;
-  p.rows_per_stage = a.rows_per_stage;
-  p.ksplit = a.ksplit;
-  p.kh_count = a.kh_count;
+  p.Wbox = opq(a.Wbox);
+  p.lw = opq(a.log_wbox);
+  p.Q = opq(a.Q);
+  p.Qr = opq(a.Qr);
+  p.c0 = opq(a.c0);
+  p.lbo = opq(a.lbo_a);
+  p.region_bytes = opq(a.region_bytes);
+  p.s = opq(a.s);
+  p.H = opq(a.H);
+  p.n_img = opq(a.n_img);
+  p.ohb = opq(a.ohb);
+  p.OHt = opq(a.OHt);
+  p.OH = opq(a.OH);
+  p.OW = opq(a.OW);
+  p.U = opq(a.U);
+  p.sw = opq(a.sw);
+  p.pw = opq(a.pw);
+  p.ph = opq(a.ph);
+  p.rows_per_stage = opq(a.rows_per_stage);
+  p.ksplit = opq(a.ksplit);
+  p.kh_count = opq(a.kh_count);
   p.raw_slots = a.raw_slots;
-  p.raw_slot_bytes = a.raw_slot_bytes;
+  p.raw_slot_bytes = opq(a.raw_slot_bytes);
   p.row_tab = row_tab;
   return p;
 }
@@ -212,9 +222,10 @@ struct StageRows {
   int kh0, nkh;    // im2col: kh range of the sub-stage
 };
 
+template <int kProd>
 __device__ __forceinline__ StageRows stage_rows(const ConvArgs& a, const RowProd& p, int mt, int ks) {
   StageRows sr;
-  if (p.prod == 1) {
+  if constexpr (kProd == 1) {
     sr.n0 = mt / p.ohb;
     sr.oh0 = (mt - sr.n0 * p.ohb) * p.OHt;
     sr.count = p.rows_per_stage;
@@ -235,8 +246,9 @@ __device__ __forceinline__ StageRows stage_rows(const ConvArgs& a, const RowProd
 }
 
 // (image, input row) of stage row r; valid = inside the image (else zero-filled)
+template <int kProd>
 __device__ __forceinline__ bool stage_row(const RowProd& p, const StageRows& sr, int r, int& n, int& ih) {
-  if (p.prod == 1) {
+  if constexpr (kProd == 1) {
     const uint32_t e = ptx::ld_shared_u32(p.row_tab + 4 * r);
     n = sr.n0;
     ih = (sr.oh0 + static_cast<int>(static_cast<int8_t>(e >> 16))) * p.s + static_cast<int>(e & 0xFF);
@@ -293,12 +305,57 @@ __device__ __forceinline__ uint4 raw16(uint32_t slot, int sh, int o, int rb) {
   return make_uint4(w0, w1, w2, w3);
 }
 
+// Per-lane chunk map of the folded layout (identical for every raw row):
+// chunk k of this lane = (region q', folded column w''), its byte offset in the
+// raw row (src) and in the region row (dst). Computed once per warp.
+struct FoldChunks {
+  int n;            // chunks of this lane (<= 4; 0 = use the generic loop)
+  int src[4], dst[4];
+};
+
+__device__ __forceinline__ FoldChunks fold_chunks(const RowProd& p, int lane) {
+  // (only meaningful for the folded layout; harmless otherwise)
+  FoldChunks fc;
+  const int nck = p.Qr << p.lw;
+  fc.n = (nck <= 128) ? (nck - lane + 31) / 32 : 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = lane + 32 * k;
+    const int qq = c >> p.lw;
+    const int w2 = c & (p.Wbox - 1);
+    fc.src[k] = (p.c0 + w2) * p.pix + ((qq == p.Q) ? p.pix : qq * 16);
+    fc.dst[k] = qq * p.lbo + w2 * 16;
+  }
+  return fc;
+}
+
 // Transpose one staged (or zero) raw row r of the stage into the A stage at `dst`.
-__device__ __forceinline__ void transpose_row(const RowProd& p, const StageRows& sr, int r, bool staged, int mt,
-                                              uint32_t dst, uint32_t slot, int sh, int lane) {
+template <int kProd>
+__device__ __forceinline__ void transpose_row(const RowProd& p, const FoldChunks& fc, const StageRows& sr, int r,
+                                              bool staged, int mt, uint32_t dst, uint32_t slot, int sh, int lane) {
   const int rb = p.rb, pix = p.pix;
   const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-  if (p.prod == 1) {
+  if (kProd == 1 && fc.n > 0) {
+    const uint32_t e = ptx::ld_shared_u32(p.row_tab + 4 * r);
+    const uint32_t rbase = dst + (e & 0xFF) * p.region_bytes + ((e >> 8) & 0xFF) * p.Wbox * 16;
+    const bool fast = sh == 0 && (pix & 15) == 0 && (rb & 15) == 0;
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = z;
+      if (k < fc.n && staged) {
+        const int o = fc.src[k];
+        if (fast) {
+          if (o >= 0 && o < rb) v[k] = ptx::ld_shared_v4(slot + o);
+        } else {
+          v[k] = raw16(slot, sh, o, rb);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < fc.n) ptx::st_shared_v4(rbase + fc.dst[k], v[k].x, v[k].y, v[k].z, v[k].w);
+  } else if (kProd == 1) {
     // regions q' of residue b, region row i: chunk (q', w'') = folded pixel
     // c0 + w'' (+1 for the shift region q' = Q), core column q' % Q
     const uint32_t e = ptx::ld_shared_u32(p.row_tab + 4 * r);
@@ -416,6 +473,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // the slot ring; warps 10..12: transpose staged rows into the A stages.
     const uint32_t ring = base + a.off_raw;
     const RowProd rp = row_prod(a, base + 768);
+    const FoldChunks fc = fold_chunks(rp, lane);
     if (warp == 0) {
       if (elect_one()) {
         const uint8_t* gb = reinterpret_cast<const uint8_t*>(a.nt_bsrc[ntile]);
@@ -427,12 +485,12 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         const bool no_loads = (a.epi_flags & 0x1000) != 0;
         for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile)
           for (int ks = 0; ks < rp.ksplit; ++ks) {
-            const StageRows sr = stage_rows(a, rp, mt, ks);
+            const StageRows sr = stage_rows<kProd>(a, rp, mt, ks);
             for (int r = 0; r < sr.count; ++r) {  // every row takes a slot; padding rows carry no bytes
               int n, ih;
-              const bool staged = stage_row(rp, sr, r, n, ih) && !no_loads;
-              const int slot = slot_it % rp.raw_slots;
-              const uint32_t round = static_cast<uint32_t>(slot_it / rp.raw_slots);
+              const bool staged = stage_row<kProd>(rp, sr, r, n, ih) && !no_loads;
+              const int slot = slot_it & (kRawSlots - 1);
+              const uint32_t round = static_cast<uint32_t>(slot_it) / kRawSlots;
               ++slot_it;
               mbar_wait(bar_raw_empty + 8 * slot, (round & 1u) ^ 1u);
               if (!staged) {
@@ -452,7 +510,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     } else {
       const int tw = warp - 10;  // transposer 0..kGatherWarps-1
       const bool dbg = (a.epi_flags & 0x8000) && blockIdx.x == 0 && tw == 0 && lane == 0;
-      long long t_empty = 0, t_full = 0, t_work = 0, t0 = 0;
+      long long t_empty = 0, t_full = 0, t_work = 0, t_fence = 0, t0 = 0;
       int it = 0, slot_it = 0;
       const bool no_loads = (a.epi_flags & 0x1000) != 0;
       const int nstages = a.stages, stage_bytes = a.stage_bytes;
@@ -461,31 +519,34 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         for (int ks = 0; ks < rp.ksplit; ++ks, ++it) {
           const int stage = it % nstages;
           const uint32_t round = static_cast<uint32_t>(it / nstages);
-          const StageRows sr = stage_rows(a, rp, mt, ks);
+          const StageRows sr = stage_rows<kProd>(a, rp, mt, ks);
           if (dbg) t0 = clock64();
           mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
           if (dbg) t_empty += clock64() - t0;
           const uint32_t dst = a_base + stage * stage_bytes;
           for (int r = tw; r < sr.count; r += kGatherWarps) {  // rows dealt round-robin to the transposers
             int n, ih;
-            const bool staged = stage_row(rp, sr, r, n, ih) && !no_loads;
-            const int slot = (slot_it + r) % rp.raw_slots;
+            const bool staged = stage_row<kProd>(rp, sr, r, n, ih) && !no_loads;
+            const int slot = (slot_it + r) & (kRawSlots - 1);
             if (dbg) t0 = clock64();
-            mbar_wait(bar_raw_full + 8 * slot, static_cast<uint32_t>((slot_it + r) / rp.raw_slots) & 1u);
+            mbar_wait(bar_raw_full + 8 * slot, (static_cast<uint32_t>(slot_it + r) / kRawSlots) & 1u);
             if (dbg) { const long long t1 = clock64(); t_full += t1 - t0; t0 = t1; }
             const uintptr_t src = reinterpret_cast<uintptr_t>(rp.x + n * rp.in_img_bytes + static_cast<long long>(ih) * rp.rb);
-            transpose_row(rp, sr, r, staged, mt, dst, ring + slot * rp.raw_slot_bytes, static_cast<int>(src & 15u),
-                          lane);
+            transpose_row<kProd>(rp, fc, sr, r, staged, mt, dst, ring + slot * rp.raw_slot_bytes,
+                          static_cast<int>(src & 15u), lane);
             __syncwarp();
             if (dbg) t_work += clock64() - t0;
             if (lane == 0) mbar_arrive(bar_raw_empty + 8 * slot);
           }
           slot_it += sr.count;
-          fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05 (async proxy)
+          if (dbg) t0 = clock64();
+          if (!(a.epi_flags & 0x10000)) fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05
           __syncwarp();
+          if (dbg) t_fence += clock64() - t0;
           if (lane == 0) mbar_arrive(bar_full + 8 * stage);
         }
       }
+      if (dbg) printf("transposer0 cta0: fence %lld cycles\n", t_fence);
       if (dbg) printf("transposer0 cta0: stages %d  wait-empty %lld  wait-row %lld  transpose %lld cycles\n", it,
                       t_empty, t_full, t_work);
     }
