@@ -114,6 +114,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     const NTile& t = S.ntiles[i];
     a.nt_entry0[i] = t.entry0;
     a.nt_entries[i] = t.entries;
+    a.nt_split[i] = t.split;
     a.nt_col0[i] = t.col0;
     a.nt_cols[i] = t.cols;
     a.nt_bbytes[i] = static_cast<int>(t.b_bytes);

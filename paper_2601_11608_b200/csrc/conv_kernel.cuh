@@ -53,6 +53,7 @@ struct ConvArgs {
   int stages, stage_bytes;
   int n_tiles, ctas_per_ntile;
   int nt_entry0[kMaxNTiles], nt_entries[kMaxNTiles], nt_col0[kMaxNTiles], nt_cols[kMaxNTiles];
+  int nt_split[kMaxNTiles];       // lower-half MMAs of the N-tile (-1: no accumulator half-split)
   int nt_bbytes[kMaxNTiles];
   long long nt_bsrc[kMaxNTiles];  // device address of the N-tile's packed B
   long long row_bytes;            // bytes of one folded output row = r*Cout*out_elem
@@ -413,7 +414,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   const uint32_t bar_full = base;          // [stages] x 8 B
   const uint32_t bar_empty = base + 64;    // [stages] x 8 B
   const uint32_t bar_tfull = base + 128;   // [2] x 8 B
-  const uint32_t bar_tempty = base + 144;  // [2] x 8 B
+  const uint32_t bar_tempty = base + 144;     // [2] x 8 B: lower half of the accumulator drained
+  const uint32_t bar_tempty_hi = base + 168;  // [2] x 8 B: upper half drained
   const uint32_t bar_b = base + 160;
   const uint32_t bar_raw_full = base + 256;   // [raw_slots <= 32] x 8 B
   const uint32_t bar_raw_empty = base + 512;  // [raw_slots <= 32] x 8 B
@@ -446,6 +448,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_tfull + 8 * i, 1);
       mbar_init(bar_tempty + 8 * i, 256);
+      mbar_init(bar_tempty_hi + 8 * i, 256);
     }
     mbar_init(bar_b, 1);
     for (int i = 0; i < a.raw_slots; ++i) {
@@ -571,11 +574,21 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
           mbar_arrive(bar_full + 8 * stage);
           continue;
         }
-        mbar_arrive_expect_tx(bar_full + 8 * stage, tx);
+        // profiling only: 0x20000 drops the shift boxes, 0x40000 loads residue 0 only
+        const bool dbg_noshift = (a.epi_flags & 0x20000) != 0, dbg_oneres = (a.epi_flags & 0x40000) != 0;
+        uint32_t txs = tx;
+        if (dbg_noshift || dbg_oneres) {
+          txs = 0;
+          for (int b = 0; b < a.s; ++b)
+            if (((a.res_mask >> b) & 1u) && !(dbg_oneres && b != __ffs(a.res_mask) - 1))
+              txs += a.box_bytes + (dbg_noshift ? 0 : a.shift_box_bytes);
+        }
+        mbar_arrive_expect_tx(bar_full + 8 * stage, txs);
         for (int b = 0; b < a.s; ++b) {
           if (!((a.res_mask >> b) & 1u)) continue;
+          if (dbg_oneres && b != __ffs(a.res_mask) - 1) continue;
           tma_load_5d(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, bar_full + 8 * stage);
-          if (a.shift_box_bytes)
+          if (a.shift_box_bytes && !dbg_noshift)
             tma_load_5d(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1, oh0 + a.amin[b], 0, n,
                         bar_full + 8 * stage);
         }
@@ -595,7 +608,9 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++tile) {
       const int acc = tile & 1;
       const uint32_t acc_round = static_cast<uint32_t>(tile >> 1);
+      const int split = (a.ksplit == 1) ? a.nt_split[ntile] : -1;
       mbar_wait(bar_tempty + 8 * acc, (acc_round & 1u) ^ 1u);
+      if (split < 0) mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
       const uint32_t d_base = tmem_base + acc * a.acc_stride;
       for (int ks = 0; ks < a.ksplit; ++ks, ++it) {
         const int stage = it % a.stages;
@@ -607,6 +622,16 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         const uint32_t a_lo = (base + a.off_a + stage * a.stage_bytes) >> 4;
         if (!skip_mma) {
           int i = 0;
+          if (split > 0) {  // lower half first, then wait for the epilogue to drain the upper half
+            for (; i < split; ++i) {
+              const uint4 e = a.table[e0 + i];
+              const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
+              const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
+              if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
+            }
+            mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
+            tc_fence_after();
+          }
           for (; i + 8 <= entries; i += 8) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -622,6 +647,9 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
             const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
             if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
           }
+        }
+        else if (split > 0) {
+          mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
         }
         if (leader) mma_commit(bar_empty + 8 * stage);
       }
@@ -645,6 +673,9 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     const int nchunks = ncols / CH;
     const int nc_w = (nchunks > half) ? (nchunks - half + 1) / 2 : 0;  // this warp's chunks
     const int n_it = 2 * nc_w;                                          // x two 16-lane halves
+    // accumulator half-split: iterations [0, lo_it) read the lower half of the columns
+    const bool split_acc = a.nt_split[ntile] > 0 && a.ksplit == 1;
+    const int lo_it = split_acc ? 2 * ((nchunks / 2 - half + 1) / 2) : n_it;
     const int k4 = lane & 3;
     const bool relu = (a.epi_flags & WF_EPI_RELU) != 0;
     const bool dbg_skip_epi = (a.epi_flags & 0x200) != 0;
@@ -684,6 +715,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       if (dbg_skip_epi || n_it == 0) {
         tc_fence_before();
         mbar_arrive(bar_tempty + 8 * acc);
+        mbar_arrive(bar_tempty_hi + 8 * acc);
         continue;
       }
       uint8_t* rowp[2][2];  // first output pixel of the row (its j = 0 sub-column)
@@ -712,6 +744,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       auto taddr = [&](int it) {
         return tq + (static_cast<uint32_t>((it & 1) * 16) << 16) + static_cast<uint32_t>((half + 2 * (it >> 1)) * CH);
       };
+      if (lo_it == 0) mbar_arrive(bar_tempty + 8 * acc);  // this warp reads no lower-half column
       uint32_t buf[2][NREG];
       tmem_ld_16x256b<NREG>(taddr(0), buf[0], skip_ld);
 #pragma unroll
@@ -736,9 +769,13 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
           }
           if (rowv[h16][r8] && roww[h16][r8] + jsub[cc] < a.OW) store_row<OutT, VPT>(rowp[h16][r8] + coff[cc], v);
         }
+        if (it + 1 == lo_it) {  // lower half of the accumulator read (its wait::ld is done)
+          tc_fence_before();
+          mbar_arrive(bar_tempty + 8 * acc);
+        }
       }
       tc_fence_before();
-      mbar_arrive(bar_tempty + 8 * acc);
+      mbar_arrive(bar_tempty_hi + 8 * acc);
     }
   }
 

@@ -376,6 +376,26 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
       return WF_OK;
     }
     t.entries = static_cast<int>(S.entries.size()) - t.entry0;
+    // Half-split accumulator release: MMAs writing only the lower half of the
+    // columns go first, so the next tile's lower-half MMAs can start as soon as
+    // the epilogue has drained that half (1.5 accumulator buffers in effect).
+    {
+      const int mid = t.cols / 2;
+      bool clean = (t.cols / S.CH) % 2 == 0 && mid % S.CH == 0;
+      std::vector<MmaEntry> lo_e, hi_e;
+      for (int i = t.entry0; i < t.entry0 + t.entries && clean; ++i) {
+        const MmaEntry& e = S.entries[i];
+        const int c0e = static_cast<int>(e.tmem_col), ne = static_cast<int>((e.meta >> 22) & 0x1FFu) * 8;
+        if (c0e + ne <= mid) lo_e.push_back(e);
+        else if (c0e >= mid) hi_e.push_back(e);
+        else clean = false;
+      }
+      if (clean && !lo_e.empty() && !hi_e.empty()) {
+        std::copy(lo_e.begin(), lo_e.end(), S.entries.begin() + t.entry0);
+        std::copy(hi_e.begin(), hi_e.end(), S.entries.begin() + t.entry0 + lo_e.size());
+        t.split = static_cast<int>(lo_e.size());
+      }
+    }
     if (static_cast<int64_t>(boff) != t.b_bytes) {
       *err = "internal: B operand bytes of a merged schedule differ from the plan";
       return WF_INVALID_ARGUMENT;

@@ -79,6 +79,8 @@ struct NTile {
   int g0, g1;              // groups [g0, g1)
   int col0, cols;          // output columns [col0, col0 + cols) of the r*Cout row
   int entry0, entries;     // slice of the schedule
+  int split = -1;          // entries writing only the lower half of the columns
+                           // (issued first; -1: no half-split of the accumulator)
   int64_t b_off, b_bytes;  // B region inside the packed buffer (after the table)
 };
 
