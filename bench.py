@@ -247,35 +247,41 @@ def run_gpu(args) -> None:
         csum = float(y.double().sum().item())
         verify = shard.gather_scalars([float(lo + i), err, csum], dev)
 
-    # ---- variant: zero-padded Cin 3 -> 8 (same kernel, f=2) -------------------------
+    # ---- variants of the same kernel: zero-padded Cin 3 -> 8 (f=2) and unfolded Cin=3 ----
     variants = {}
     if not args.no_variants:
+        def time_variant(c_, xin, steps):
+            for _ in range(3):
+                c_(xin, out=y)
+            barrier()
+            ev0.record(stream)
+            for _ in range(steps):
+                c_(xin, out=y)
+            ev1.record(stream)
+            barrier()
+            return shard.max_over_ranks(ev0.elapsed_time(ev1), dev) / steps
+
         xz = torch.zeros((n, H, W, 8), dtype=torch.bfloat16, device=dev)
         xz[..., :C] = x
         wz = torch.zeros((K, K, 8, COUT), dtype=torch.bfloat16, device=dev)
         wz[:, :, :C] = wt
         convz = wf.FoldedConv2d(wz, bias, xz.shape, stride=STRIDE, padding=PAD, dtype=torch.bfloat16)
-        for _ in range(3):
-            convz(xz, out=y)
-        barrier()
-        vs = max(5, args.steps // 4)
-        ev0.record(stream)
-        for _ in range(vs):
-            convz(xz, out=y)
-        ev1.record(stream)
-        barrier()
-        zms = shard.max_over_ranks(ev0.elapsed_time(ev1), dev) / vs
+        zms = time_variant(convz, xz, max(5, args.steps // 4))
         del xz, wz
-        for name, ms_, c_ in (("fold", ms_step, conv), ("zeropad_cin8", zms, convz)):
+        convu = wf.FoldedConv2d(wt, bias, x.shape, stride=STRIDE, padding=PAD, dtype=torch.bfloat16,
+                                variant="unfolded")
+        ums = time_variant(convu, x, max(3, args.steps // 20))
+        for name, ms_, c_ in (("fold", ms_step, conv), ("zeropad_cin8", zms, convz), ("unfolded_cin3", ums, convu)):
             d = c_.device_plan
             variants[name] = {"images_per_s": N_IMG / (ms_ / 1e3), "ms_per_step": ms_,
                               "useful_tflops": N_IMG * USEFUL_FLOP_PER_IMG / (ms_ / 1e3) / 1e12,
                               "issued_tflops": 2 * d["issued_macs"] * world / (ms_ / 1e3) / 1e12,
                               "useful_over_issued": d["useful_macs"] / d["issued_macs"] * (
                                   C / 8 if name.startswith("zero") else 1.0),
-                              "fold_factor": d["f"], "group_size": d["group_size"]}
+                              "fold_factor": d["f"], "group_size": d["group_size"], "a_producer": d["producer"]}
         variants["fold_speedup_vs_zeropad"] = zms / ms_step
-        variants["unfolded_cin3"] = "not built: 6-byte pixels cannot be addressed by TMA; gather producer pending"
+        variants["fold_speedup_vs_unfolded"] = ums / ms_step
+        del convz, convu
 
     # ---- e2e: public API from pinned host buffers, H2D + D2H inside the timing -------
     e2e = None
