@@ -8,6 +8,9 @@ re-designed for sm_100a (TMA + tcgen05 + TMEM). Same public names as
 from .api import (  # noqa: F401
     DegenerateOutputError,
     FoldedConv2d,
+    Graph,
+    MissingInputError,
+    ShapeInferenceFailureError,
     IllegalFoldError,
     NotBlockDiagonalError,
     ShapeMismatchError,
@@ -29,11 +32,13 @@ from .api import (  # noqa: F401
     gemm_as_conv1x1,
     gemm_ref,
     grouped_conv,
+    interpret,
     mac_report,
     plan_fold,
     reconstruct_output,
     replicate_bias,
     unfold_input_general,
+    width_fold_pass,
 )
 from .api import __all__  # noqa: F401
 

@@ -503,6 +503,51 @@ def fold_tall_skinny(a, b, factor: int):
     return _ret(reconstruct_output(y_f, factor).reshape(M, N), host)
 
 
+# ------------------------------------------------ graph pass + interpreter (8.F-2)
+class Graph:
+    """The reference mini-IR (include/widthfold/graph.hpp:21-45) as node dicts
+    (``id``, ``op``, ``inputs``, ``shape``, ``tensor``, ``stride_h/w``,
+    ``groups``, ``pad_h/w``; ``folded_conv2d`` adds ``factor``, ``bias``) and
+    float32 weights. The pass and the interpreter run in the C++ host layer."""
+
+    def __init__(self, nodes=None, weights=None):
+        self.nodes = [dict(n) for n in (nodes or [])]
+        self.weights = {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in (weights or {}).items()}
+
+    def add(self, id, op, inputs=(), **attrs):
+        self.nodes.append({"id": id, "op": op, "inputs": list(inputs), **attrs})
+        return id
+
+    def constant(self, id, array):
+        self.weights[id] = np.ascontiguousarray(array, dtype=np.float32)
+        return self.add(id, "constant", tensor=id)
+
+    def infer_shapes(self) -> "Graph":
+        return Graph(_core.infer_shapes(self.nodes, self.weights), self.weights)
+
+    def find(self, id):
+        return next((n for n in self.nodes if n["id"] == id), None)
+
+
+def width_fold_pass(graph: Graph, factor: int | None = None, align: int = 8):
+    """Rewrite every conv2d the generalized device fold applies to into one
+    ``folded_conv2d`` (tcgen05 TF32, sole-consumer constant bias fused).
+    Returns ``(graph, report)`` like PassResult (include/widthfold/pass.hpp:45-52)."""
+    nodes, weights, report = _core.width_fold_pass(graph.nodes, graph.weights, int(factor or 0), int(align))
+    return Graph(nodes, weights), report
+
+
+def interpret(graph: Graph, inputs: dict, mode: str = "device") -> dict:
+    """Execute on the GPU; returns {output id: float32 ndarray} (src/interpreter.cpp:8-66)."""
+    if mode not in ("dense", "grouped", "device"):
+        raise ValueError("mode must be 'dense', 'grouped' or 'device'")
+    arrays = {k: np.ascontiguousarray(np.asarray(v, dtype=np.float32)) for k, v in inputs.items()}
+    return _core.interpret(graph.nodes, graph.weights, arrays, mode)
+
+
+ShapeInferenceFailureError = _core.ShapeInferenceFailureError
+MissingInputError = _core.MissingInputError
+
 __all__ = [
     "apply_width_fold", "apply_width_fold_general", "bias_add", "check_legality", "choose_fold_factor",
     "conv1d_h", "conv2d", "count_macs", "expand_filter", "expand_filter_general", "fold_input",
@@ -511,4 +556,5 @@ __all__ = [
     # additions
     "FoldedConv2d", "expand_filter_folded", "plan_fold", "ShapeMismatchError", "IllegalFoldError",
     "DegenerateOutputError", "NotBlockDiagonalError", "UnsupportedError",
+    "Graph", "width_fold_pass", "interpret", "ShapeInferenceFailureError", "MissingInputError",
 ]

@@ -4,7 +4,12 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstring>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "kernels.hpp"
 #include "plan.hpp"
@@ -14,6 +19,43 @@ namespace {
 
 thread_local std::string g_last_error;
 std::atomic<int> g_num_sms{0};
+
+// Rebuilding a schedule from a plan re-runs the planner (including the
+// accumulator-slot order search); forward calls look it up here instead.
+// Keyed by the descriptor and the plan bytes; small, thread-safe, bounded.
+struct SchedKey {
+  wf_conv_desc d;
+  wf_fold_plan p;
+  bool operator==(const SchedKey& o) const {
+    return std::memcmp(&d, &o.d, sizeof(d)) == 0 && std::memcmp(&p, &o.p, sizeof(p)) == 0;
+  }
+};
+std::mutex g_sched_mu;
+std::vector<std::pair<SchedKey, std::shared_ptr<const wfb::Schedule>>> g_sched;
+
+wf_status cached_schedule(const wf_conv_desc& d, const wf_fold_plan& p, std::shared_ptr<const wfb::Schedule>* out,
+                          std::string* err) {
+  SchedKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.d = d;
+  key.p = p;
+  {
+    std::lock_guard<std::mutex> lk(g_sched_mu);
+    for (auto& e : g_sched)
+      if (e.first == key) {
+        *out = e.second;
+        return WF_OK;
+      }
+  }
+  auto S = std::make_shared<wfb::Schedule>();
+  wf_status st = wfb::schedule_from_plan(d, p, S.get(), err);
+  if (st != WF_OK) return st;
+  std::lock_guard<std::mutex> lk(g_sched_mu);
+  if (g_sched.size() >= 64) g_sched.erase(g_sched.begin());
+  g_sched.emplace_back(key, S);
+  *out = S;
+  return WF_OK;
+}
 
 wf_status fail(wf_status st, const std::string& msg) {
   g_last_error = msg;
@@ -88,11 +130,11 @@ wf_status wf_conv_fold_fwd_ws(const void* x, void* workspace, const void* w_pack
     return fail(WF_INVALID_ARGUMENT, "unknown epilogue flags");
   if (plan->workspace_bytes > 0 && !workspace && !(epilogue & 0x4000))
     return fail(WF_INVALID_ARGUMENT, "this plan needs a workspace of plan->workspace_bytes (wf_conv_fold_fwd_ws)");
-  wfb::Schedule S;
+  std::shared_ptr<const wfb::Schedule> S;
   std::string err;
-  wf_status st = wfb::schedule_from_plan(*desc, *plan, &S, &err);
+  wf_status st = cached_schedule(*desc, *plan, &S, &err);
   if (st != WF_OK) return fail(st, err);
-  st = wfb::launch_conv(S, *desc, x, workspace, w_packed, b_rep, y, out_dtype, epilogue,
+  st = wfb::launch_conv(*S, *desc, x, workspace, w_packed, b_rep, y, out_dtype, epilogue,
                         static_cast<cudaStream_t>(stream), g_num_sms.load(), &err);
   if (st != WF_OK) return fail(st, err);
   return WF_OK;

@@ -11,6 +11,9 @@
 
 #include <cstdint>
 
+#include <pybind11/numpy.h>
+
+#include "graph.hpp"
 #include "widthfold.hpp"
 
 namespace py = pybind11;
@@ -55,6 +58,85 @@ py::dict raw_dict(const wf_fold_plan& p) {
 wf::ConvSpec spec_of(const wf::Shape& in, const wf::Shape& filt, std::int64_t sh, std::int64_t sw, std::int64_t ph,
                      std::int64_t pw) {
   return wf::ConvSpec{in, filt, sh, sw, ph, pw};
+}
+
+// ---- graph <-> Python (list of node dicts, dict of float32 arrays) ----------------
+using F32Array = py::array_t<float, py::array::c_style | py::array::forcecast>;
+
+wf::HostTensor host_tensor(const F32Array& a) {
+  wf::HostTensor t;
+  for (py::ssize_t i = 0; i < a.ndim(); ++i) t.shape.push_back(a.shape(i));
+  t.data.assign(a.data(), a.data() + a.size());
+  return t;
+}
+
+F32Array to_array(const wf::HostTensor& t) {
+  std::vector<py::ssize_t> shape(t.shape.begin(), t.shape.end());
+  F32Array a(shape);
+  std::copy(t.data.begin(), t.data.end(), a.mutable_data());
+  return a;
+}
+
+template <typename T>
+T get_or(const py::dict& d, const char* k, T dflt) {
+  return d.contains(k) ? d[k].cast<T>() : dflt;
+}
+
+wf::Graph graph_of(const py::list& nodes, const py::dict& weights) {
+  wf::Graph g;
+  for (auto item : weights) g.weights[item.first.cast<std::string>()] = host_tensor(item.second.cast<F32Array>());
+  for (auto h : nodes) {
+    const py::dict d = h.cast<py::dict>();
+    wf::Node n;
+    n.id = d["id"].cast<std::string>();
+    n.op = wf::op_kind_from_string(d["op"].cast<std::string>());
+    n.inputs = get_or<std::vector<std::string>>(d, "inputs", {});
+    n.shape = get_or<wf::Shape>(d, "shape", {});
+    n.tensor = get_or<std::string>(d, "tensor", "");
+    n.stride_h = get_or<std::int64_t>(d, "stride_h", 1);
+    n.stride_w = get_or<std::int64_t>(d, "stride_w", 1);
+    n.groups = get_or<std::int64_t>(d, "groups", 1);
+    n.pad_h = get_or<std::int64_t>(d, "pad_h", 0);
+    n.pad_w = get_or<std::int64_t>(d, "pad_w", 0);
+    n.factor = get_or<std::int64_t>(d, "factor", 0);
+    n.bias = get_or<bool>(d, "bias", false);
+    g.nodes.push_back(std::move(n));
+  }
+  return g;
+}
+
+py::list nodes_of(const wf::Graph& g) {
+  py::list out;
+  for (const auto& n : g.nodes) {
+    py::dict d;
+    d["id"] = n.id;
+    d["op"] = wf::to_string(n.op);
+    d["inputs"] = n.inputs;
+    if (!n.shape.empty()) d["shape"] = n.shape;
+    if (!n.tensor.empty()) d["tensor"] = n.tensor;
+    if (n.op == wf::OpKind::Conv2d || n.op == wf::OpKind::FoldedConv2d) {
+      d["stride_h"] = n.stride_h;
+      d["stride_w"] = n.stride_w;
+      d["groups"] = n.groups;
+      d["pad_h"] = n.pad_h;
+      d["pad_w"] = n.pad_w;
+    }
+    if (n.op == wf::OpKind::FoldedConv2d) {
+      d["factor"] = n.factor;
+      d["bias"] = n.bias;
+    }
+    d["out_shape"] = n.out_shape;
+    out.append(d);
+  }
+  return out;
+}
+
+py::dict cost_dict(const wf::CostEstimate& c) {
+  py::dict d;
+  d["macs"] = c.macs;
+  d["issued_macs"] = c.issued_macs;
+  d["aligned"] = c.aligned;
+  return d;
 }
 
 }  // namespace
@@ -179,6 +261,60 @@ PYBIND11_MODULE(_core, m) {
         wf::check_block_diagonal(F(w), s, groups, P(scratch), P(stream));
       },
       py::arg("w"), py::arg("dense_shape"), py::arg("groups"), py::arg("scratch"), py::arg("stream"));
+
+  py::register_exception<wf::ShapeInferenceFailure>(m, "ShapeInferenceFailureError", PyExc_ValueError);
+  py::register_exception<wf::MissingInput>(m, "MissingInputError", PyExc_ValueError);
+
+  m.def(
+      "infer_shapes",
+      [](const py::list& nodes, const py::dict& weights) { return nodes_of(wf::infer_shapes(graph_of(nodes, weights))); },
+      py::arg("nodes"), py::arg("weights"), "Validate a graph and annotate out_shape (graph.hpp).");
+  m.def(
+      "width_fold_pass",
+      [](const py::list& nodes, const py::dict& weights, std::int64_t factor, std::int64_t align) {
+        const wf::FoldFactor ff = factor > 0 ? wf::FoldFactor::fixed(factor) : wf::FoldFactor::automatic();
+        wf::PassResult r = wf::width_fold_pass(graph_of(nodes, weights), ff, align);
+        py::list decisions;
+        for (const auto& d : r.report.decisions) {
+          py::dict e;
+          e["id"] = d.id;
+          e["kind"] = wf::to_string(d.kind);
+          e["applied"] = d.applied;
+          e["plan"] = plan_dict(d.plan);
+          e["note"] = d.note;
+          decisions.append(e);
+        }
+        py::dict report;
+        report["decisions"] = decisions;
+        report["before"] = cost_dict(r.report.before);
+        report["after"] = cost_dict(r.report.after);
+        report["applied_count"] = r.report.applied_count();
+        py::dict w;
+        for (const auto& kv : r.graph.weights) w[py::str(kv.first)] = to_array(kv.second);
+        return py::make_tuple(nodes_of(r.graph), w, report);
+      },
+      py::arg("nodes"), py::arg("weights"), py::arg("factor") = 0, py::arg("align") = 8,
+      "Rewrite-rule pass (src/pass.cpp:71): every conv2d the device fold applies to becomes folded_conv2d.");
+  m.def(
+      "interpret",
+      [](const py::list& nodes, const py::dict& weights, const py::dict& inputs, const std::string& mode) {
+        wf::TensorMap in;
+        for (auto item : inputs) in[item.first.cast<std::string>()] = host_tensor(item.second.cast<F32Array>());
+        const wf::ExecMode em = mode == "dense" ? wf::ExecMode::Dense
+                                : mode == "grouped" ? wf::ExecMode::Grouped
+                                                    : wf::ExecMode::Device;
+        wf::Graph g = graph_of(nodes, weights);
+        wf::TensorMap out;
+        {
+          py::gil_scoped_release nogil;
+          out = wf::interpret(g, in, em);
+        }
+        py::dict d;
+        for (const auto& kv : out) d[py::str(kv.first)] = to_array(kv.second);
+        return d;
+      },
+      py::arg("nodes"), py::arg("weights"), py::arg("inputs"), py::arg("mode") = "device",
+      "Execute the graph on the GPU (src/interpreter.cpp:8).");
 
   py::class_<wf::FoldedConv>(m, "FoldedConv")
       .def(py::init([](const wf::Shape& in, const wf::Shape& filt, std::int64_t sh, std::int64_t sw,

@@ -1,0 +1,422 @@
+// graph.cpp -- see graph.hpp. Reference: /root/reference/proj/src/graph.cpp
+// (infer_shapes :88-186, cost :188-211), src/pass.cpp:71-218 (conv branch),
+// src/interpreter.cpp:8-66.
+#include "graph.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <memory>
+#include <numeric>
+#include <set>
+#include <stdexcept>
+
+namespace widthfold {
+
+namespace {
+
+std::int64_t numel(const Shape& s) {
+  return std::accumulate(s.begin(), s.end(), std::int64_t{1}, std::multiplies<std::int64_t>());
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+const char* to_string(OpKind kind) {
+  switch (kind) {
+    case OpKind::Input: return "input";
+    case OpKind::Output: return "output";
+    case OpKind::Constant: return "constant";
+    case OpKind::Conv2d: return "conv2d";
+    case OpKind::Matmul: return "matmul";
+    case OpKind::BiasAdd: return "bias_add";
+    case OpKind::Reshape: return "reshape";
+    case OpKind::FoldedConv2d: return "folded_conv2d";
+  }
+  return "?";
+}
+
+OpKind op_kind_from_string(const std::string& name) {
+  for (OpKind k : {OpKind::Input, OpKind::Output, OpKind::Constant, OpKind::Conv2d, OpKind::Matmul, OpKind::BiasAdd,
+                   OpKind::Reshape, OpKind::FoldedConv2d})
+    if (name == to_string(k)) return k;
+  throw std::invalid_argument("unknown op kind '" + name + "'");
+}
+
+const Node* Graph::find(const std::string& id) const {
+  for (const auto& n : nodes)
+    if (n.id == id) return &n;
+  return nullptr;
+}
+Node* Graph::find(const std::string& id) {
+  for (auto& n : nodes)
+    if (n.id == id) return &n;
+  return nullptr;
+}
+std::vector<std::string> Graph::input_ids() const {
+  std::vector<std::string> r;
+  for (const auto& n : nodes)
+    if (n.op == OpKind::Input) r.push_back(n.id);
+  return r;
+}
+std::vector<std::string> Graph::output_ids() const {
+  std::vector<std::string> r;
+  for (const auto& n : nodes)
+    if (n.op == OpKind::Output) r.push_back(n.id);
+  return r;
+}
+
+std::size_t RewriteReport::applied_count() const {
+  std::size_t n = 0;
+  for (const auto& d : decisions) n += d.applied ? 1 : 0;
+  return n;
+}
+
+// ---- shapes (src/graph.cpp:88-186) -------------------------------------------------
+ConvSpec conv_spec_of(const Graph& g, const Node& node) {
+  const Node* x = g.find(node.inputs.at(0));
+  const Node* w = g.find(node.inputs.at(1));
+  ConvSpec s;
+  s.input_shape = x->out_shape;
+  s.filter_shape = w->out_shape;
+  s.stride_h = node.stride_h;
+  s.stride_w = node.stride_w;
+  s.pad_h = node.pad_h;
+  s.pad_w = node.pad_w;
+  return s;
+}
+
+Graph infer_shapes(Graph g) {
+  std::set<std::string> seen;
+  for (auto& n : g.nodes) {
+    auto fail = [&](const std::string& why) {
+      throw ShapeInferenceFailure("node '" + n.id + "' (" + to_string(n.op) + "): " + why);
+    };
+    if (n.id.empty() || seen.count(n.id)) fail("missing or duplicate id");
+    for (const auto& in : n.inputs)
+      if (!seen.count(in)) fail("input '" + in + "' is not an earlier node (graph must be topological)");
+    auto in_shape = [&](std::size_t i) -> const Shape& { return g.find(n.inputs.at(i))->out_shape; };
+    auto arity = [&](std::size_t k) {
+      if (n.inputs.size() != k) fail("expects " + std::to_string(k) + " inputs");
+    };
+    switch (n.op) {
+      case OpKind::Input:
+        arity(0);
+        if (n.shape.empty()) fail("input needs a declared shape");
+        n.out_shape = n.shape;
+        break;
+      case OpKind::Constant: {
+        arity(0);
+        auto it = g.weights.find(n.tensor);
+        if (it == g.weights.end()) fail("unknown weight tensor '" + n.tensor + "'");
+        n.out_shape = it->second.shape;
+        break;
+      }
+      case OpKind::Output:
+        arity(1);
+        n.out_shape = in_shape(0);
+        break;
+      case OpKind::Conv2d:
+      case OpKind::FoldedConv2d: {
+        if (n.inputs.size() != (n.op == OpKind::FoldedConv2d && n.bias ? 3u : 2u)) fail("wrong number of inputs");
+        ConvSpec s = conv_spec_of(g, n);
+        try {
+          s.validate();
+        } catch (const std::exception& e) {
+          fail(e.what());
+        }
+        if (n.groups < 1 || s.in_c() % n.groups || s.out_c() % n.groups) fail("groups must divide Cin and Cout");
+        if (n.bias && in_shape(2) != Shape{s.out_c()}) fail("fused bias must be (Cout)");
+        n.out_shape = s.output_shape();
+        break;
+      }
+      case OpKind::BiasAdd: {
+        arity(2);
+        const Shape& y = in_shape(0);
+        const Shape& b = in_shape(1);
+        if (y.empty() || b.size() != 1 || b[0] != y.back()) fail("bias must be (C) of the input's last axis");
+        n.out_shape = y;
+        break;
+      }
+      case OpKind::Reshape:
+        arity(1);
+        if (numel(n.shape) != numel(in_shape(0))) fail("reshape changes the element count");
+        n.out_shape = n.shape;
+        break;
+      case OpKind::Matmul: {
+        arity(2);
+        const Shape& a = in_shape(0);
+        const Shape& b = in_shape(1);
+        if (a.size() != 2 || b.size() != 2 || a[1] != b[0]) fail("matmul needs (M,K) x (K,N)");
+        n.out_shape = {a[0], b[1]};
+        break;
+      }
+    }
+    seen.insert(n.id);
+  }
+  return g;
+}
+
+// ---- cost (src/graph.cpp:188-211) ---------------------------------------------------
+CostEstimate cost(const Graph& g0, std::int64_t align) {
+  const Graph g = infer_shapes(g0);
+  CostEstimate c;
+  for (const auto& n : g.nodes) {
+    if (n.op == OpKind::Conv2d) {
+      const ConvSpec s = conv_spec_of(g, n);
+      c.macs += count_macs(s);
+      c.issued_macs += count_macs(s);
+      if (s.in_c() % align) c.aligned = false;
+    } else if (n.op == OpKind::FoldedConv2d) {
+      const ConvSpec s = conv_spec_of(g, n);
+      c.macs += count_macs(s);
+      c.issued_macs += plan_device_fold(s, n.factor, 0, Dtype::TF32).raw.issued_macs;
+    } else if (n.op == OpKind::Matmul) {
+      const Shape& a = g.find(n.inputs[0])->out_shape;
+      const std::uint64_t m = static_cast<std::uint64_t>(a[0]) * a[1] * n.out_shape[1];
+      c.macs += m;
+      c.issued_macs += m;
+      if (a[1] % align) c.aligned = false;
+    }
+  }
+  return c;
+}
+
+// ---- the pass (src/pass.cpp:89-218, conv branch) ------------------------------------
+PassResult width_fold_pass(Graph g, FoldFactor factor, std::int64_t align) {
+  if (align < 1) throw std::invalid_argument("alignment must be >= 1");
+  if (!factor.is_auto() && *factor.value < 1) throw std::invalid_argument("fold factor must be >= 1");
+  g = infer_shapes(std::move(g));
+  RewriteReport report;
+  report.before = cost(g, align);
+
+  std::map<std::string, std::vector<std::string>> consumers;
+  for (const auto& n : g.nodes)
+    for (const auto& in : n.inputs) consumers[in].push_back(n.id);
+
+  auto skipped = [](const Node& n, FoldReason r, std::int64_t f, std::string note = "") {
+    NodeDecision d;
+    d.id = n.id;
+    d.kind = OpKind::Conv2d;
+    d.applied = false;
+    d.plan.status = FoldStatus::Fallback;
+    d.plan.reason = r;
+    d.plan.factor = f;
+    d.note = std::move(note);
+    return d;
+  };
+
+  std::vector<Node> out;
+  // folded convs whose fused bias_add comes later: emitted at the bias_add's
+  // position (the bias constant may be declared between the two)
+  std::map<std::string, Node> pending;
+  for (std::size_t i = 0; i < g.nodes.size(); ++i) {
+    Node node = g.nodes[i];
+    auto pit = pending.find(node.id);
+    if (pit != pending.end()) {
+      Node ident;
+      ident.id = node.id;  // the bias_add keeps its value id as an identity view
+      ident.op = OpKind::Reshape;
+      ident.inputs = {pit->second.id};
+      ident.shape = node.out_shape;
+      out.push_back(pit->second);
+      out.push_back(ident);
+      pending.erase(pit);
+      continue;
+    }
+    if (node.op == OpKind::FoldedConv2d) {  // a second run: already folded
+      report.decisions.push_back(skipped(node, FoldReason::AlreadyAligned, node.factor, "already folded"));
+      out.push_back(node);
+      continue;
+    }
+    if (node.op != OpKind::Conv2d) {
+      out.push_back(node);
+      continue;
+    }
+    const ConvSpec spec = conv_spec_of(g, node);
+    if (spec.in_c() % align == 0) {
+      report.decisions.push_back(skipped(node, FoldReason::AlreadyAligned, 1));
+      out.push_back(node);
+      continue;
+    }
+    const Node* w_node = g.find(node.inputs[1]);
+    if (w_node->op != OpKind::Constant) {
+      report.decisions.push_back(skipped(node, FoldReason::NotProfitable, 1,
+                                         "filter is not a constant; cannot expand statically"));
+      out.push_back(node);
+      continue;
+    }
+    if (node.groups != 1) {
+      report.decisions.push_back(skipped(node, FoldReason::NotProfitable, 1, "grouped conv: runs as is"));
+      out.push_back(node);
+      continue;
+    }
+    if (!factor.is_auto() && *factor.value == 1) {
+      report.decisions.push_back(skipped(node, FoldReason::AlreadyAligned, 1, "factor 1 is the identity fold"));
+      out.push_back(node);
+      continue;
+    }
+    const DevicePlan dp = plan_device_fold(spec, factor.is_auto() ? 0 : *factor.value, 0, Dtype::TF32);
+    if (!dp.plan.ok()) {
+      report.decisions.push_back(skipped(node, dp.plan.reason, dp.plan.factor));
+      out.push_back(node);
+      continue;
+    }
+    NodeDecision d;
+    d.id = node.id;
+    d.kind = OpKind::Conv2d;
+    d.applied = true;
+    d.plan = dp.plan;
+    // sole-consumer bias_add with a constant bias: fused into the epilogue; the
+    // bias_add node keeps its id as an identity reshape of the folded conv
+    const Node* bias_node = nullptr;
+    auto it = consumers.find(node.id);
+    if (it != consumers.end() && it->second.size() == 1) {
+      const Node* cand = g.find(it->second[0]);
+      if (cand->op == OpKind::BiasAdd && cand->inputs[0] == node.id &&
+          g.find(cand->inputs[1])->op == OpKind::Constant)
+        bias_node = cand;
+    }
+    Node folded = node;
+    folded.op = OpKind::FoldedConv2d;
+    folded.factor = dp.raw.f;
+    if (bias_node) {
+      folded.bias = true;
+      folded.inputs.push_back(bias_node->inputs[1]);
+      d.note = "bias folded via " + bias_node->id;
+      pending.emplace(bias_node->id, folded);
+    } else {
+      out.push_back(folded);
+    }
+    report.decisions.push_back(d);
+  }
+  g.nodes = std::move(out);
+  g = infer_shapes(std::move(g));
+  report.after = cost(g, align);
+  return PassResult{std::move(g), std::move(report)};
+}
+
+// ---- the interpreter (src/interpreter.cpp:8-66), on the device -------------------------
+namespace {
+
+struct DevBuf {
+  float* p = nullptr;
+  Shape shape;
+  std::shared_ptr<void> owner;  // shared by reshape views
+};
+
+std::shared_ptr<void> dev_alloc(std::size_t bytes) {
+  void* p = nullptr;
+  cuda_check(cudaMalloc(&p, std::max<std::size_t>(bytes, 16)), "cudaMalloc");
+  return std::shared_ptr<void>(p, [](void* q) { cudaFree(q); });
+}
+
+DevBuf upload(const HostTensor& t) {
+  DevBuf b;
+  b.shape = t.shape;
+  b.owner = dev_alloc(t.data.size() * sizeof(float));
+  b.p = static_cast<float*>(b.owner.get());
+  cuda_check(cudaMemcpy(b.p, t.data.data(), t.data.size() * sizeof(float), cudaMemcpyHostToDevice), "upload");
+  return b;
+}
+
+DevBuf make(const Shape& s) {
+  DevBuf b;
+  b.shape = s;
+  b.owner = dev_alloc(static_cast<std::size_t>(numel(s)) * sizeof(float));
+  b.p = static_cast<float*>(b.owner.get());
+  return b;
+}
+
+}  // namespace
+
+TensorMap interpret(const Graph& g0, const TensorMap& inputs, ExecMode mode) {
+  (void)mode;  // Dense and Grouped both run the exact-order conv (bitwise equal, src/blockdiag.cpp:138-187)
+  const Graph g = infer_shapes(g0);
+  std::map<std::string, DevBuf> val;
+  TensorMap outs;
+  cudaStream_t st = nullptr;  // legacy default stream: ordered with the synchronous copies
+  for (const auto& n : g.nodes) {
+    switch (n.op) {
+      case OpKind::Input: {
+        auto it = inputs.find(n.id);
+        if (it == inputs.end()) throw MissingInput("no binding for input '" + n.id + "'");
+        if (it->second.shape != n.out_shape)
+          throw ShapeMismatch("input '" + n.id + "' bound to " + shape_str(it->second.shape) + ", declared " +
+                              shape_str(n.out_shape));
+        val[n.id] = upload(it->second);
+        break;
+      }
+      case OpKind::Constant:
+        val[n.id] = upload(g.weights.at(n.tensor));
+        break;
+      case OpKind::Conv2d: {
+        const ConvSpec s = conv_spec_of(g, n);
+        DevBuf y = make(n.out_shape);
+        conv2d_exact(val.at(n.inputs[0]).p, val.at(n.inputs[1]).p, y.p, s, st);
+        val[n.id] = y;
+        break;
+      }
+      case OpKind::FoldedConv2d: {
+        const ConvSpec s = conv_spec_of(g, n);
+        FoldedConv fc(s, Dtype::TF32, n.factor, 0);
+        auto packed = dev_alloc(fc.packed_bytes());
+        std::shared_ptr<void> brep;
+        if (n.bias) brep = dev_alloc(static_cast<std::size_t>(fc.cout_f()) * sizeof(float));
+        fc.pack(val.at(n.inputs[1]).p, n.bias ? val.at(n.inputs[2]).p : nullptr, packed.get(),
+                n.bias ? static_cast<float*>(brep.get()) : nullptr, st);
+        std::shared_ptr<void> ws;
+        if (fc.workspace_bytes()) ws = dev_alloc(fc.workspace_bytes());
+        DevBuf y = make(n.out_shape);
+        fc.forward(val.at(n.inputs[0]).p, packed.get(), n.bias ? static_cast<float*>(brep.get()) : nullptr, y.p,
+                   Dtype::F32, n.bias, false, st, 0, ws.get());
+        cuda_check(cudaStreamSynchronize(st), "folded conv");  // packed/brep/ws are freed below
+        val[n.id] = y;
+        break;
+      }
+      case OpKind::BiasAdd: {
+        const DevBuf& y = val.at(n.inputs[0]);
+        const DevBuf& b = val.at(n.inputs[1]);
+        DevBuf o = make(n.out_shape);
+        bias_add(y.p, b.p, o.p, numel(n.out_shape), b.shape[0], false, st);
+        val[n.id] = o;
+        break;
+      }
+      case OpKind::Reshape: {
+        DevBuf v = val.at(n.inputs[0]);  // zero-copy view
+        v.shape = n.out_shape;
+        val[n.id] = v;
+        break;
+      }
+      case OpKind::Matmul: {  // gemm_ref (src/gemm.cpp:26-41) as the exact 1x1 conv
+        const DevBuf& a = val.at(n.inputs[0]);
+        const DevBuf& b = val.at(n.inputs[1]);
+        ConvSpec s;
+        s.input_shape = {1, 1, a.shape[0], a.shape[1]};
+        s.filter_shape = {1, 1, b.shape[0], b.shape[1]};
+        DevBuf y = make(n.out_shape);
+        conv2d_exact(a.p, b.p, y.p, s, st);
+        val[n.id] = y;
+        break;
+      }
+      case OpKind::Output: {
+        const DevBuf& v = val.at(n.inputs[0]);
+        HostTensor t;
+        t.shape = v.shape;
+        t.data.resize(static_cast<std::size_t>(numel(v.shape)));
+        cuda_check(cudaMemcpy(t.data.data(), v.p, t.data.size() * sizeof(float), cudaMemcpyDeviceToHost),
+                   "download");
+        outs[n.id] = std::move(t);
+        val[n.id] = v;
+        break;
+      }
+    }
+  }
+  cuda_check(cudaDeviceSynchronize(), "interpret");
+  return outs;
+}
+
+}  // namespace widthfold
