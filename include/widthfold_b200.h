@@ -117,6 +117,9 @@ typedef struct {
   int32_t producer;        /* A-tile producer: 0 TMA boxes on x, 1 row gather
                               (folded layout), 2 row gather (explicit im2col),
                               3 re-pitch x into the workspace, then TMA boxes */
+  int32_t cta_pair;        /* 2: the conv runs on CTA pairs (cta_group::2, M = 256
+                              per MMA), each SM holding half of every B block */
+  int32_t reserved0;
   int64_t pitched_w;       /* producer 3: workspace row width (>= W, % f == 0) */
   int64_t workspace_bytes; /* device scratch wf_conv_fold_fwd_ws needs (0: none) */
   uint64_t useful_macs;    /* count_macs of the original conv */

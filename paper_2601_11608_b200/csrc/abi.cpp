@@ -66,7 +66,7 @@ wf_status fail(wf_status st, const std::string& msg) {
 
 extern "C" {
 
-int wf_abi_version(void) { return 4; }
+int wf_abi_version(void) { return 5; }
 
 const char* wf_last_error(void) { return g_last_error.c_str(); }
 

@@ -117,18 +117,19 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     a.nt_split[i] = t.split;
     a.nt_col0[i] = t.col0;
     a.nt_cols[i] = t.cols;
-    a.nt_bbytes[i] = static_cast<int>(t.b_bytes);
+    a.nt_bbytes[i] = static_cast<int>(t.b_bytes / S.pair);  // per CTA: half of every block in pair mode
     a.nt_bsrc[i] = reinterpret_cast<long long>(packed_b + t.b_off);
     max_cols = std::max<uint32_t>(max_cols, static_cast<uint32_t>(t.cols));
   }
   const uint32_t fmt = (in_t == WF_BF16) ? 1u : (in_t == WF_F16 ? 0u : 2u);
-  const uint32_t idesc_base = (1u << 4) | (fmt << 7) | (fmt << 10) | ((static_cast<uint32_t>(kTileM) >> 4) << 24);
+  const uint32_t idesc_base =
+      (1u << 4) | (fmt << 7) | (fmt << 10) | ((static_cast<uint32_t>(kTileM * S.pair) >> 4) << 24);  // M = 128 / 256
   for (size_t i = 0; i < S.entries.size(); ++i) {
     const MmaEntry& e = S.entries[i];
     const uint32_t n8 = (e.meta >> 22) & 0x1FFu;  // N / 8 of this MMA
     const uint32_t lbo_b = n8 * 8u * 16u;         // B: [core col][N rows][16 B]
     a.table[i].x = (e.a_off >> 4) | ((static_cast<uint32_t>(S.lbo_a) >> 4) << 16);
-    a.table[i].y = (e.b_off >> 4) | ((lbo_b >> 4) << 16);
+    a.table[i].y = ((e.b_off / S.pair) >> 4) | (((lbo_b / S.pair) >> 4) << 16);
     a.table[i].z = idesc_base | (n8 << 17) | (e.meta & 0x80000000u);
     a.table[i].w = e.tmem_col;
   }
@@ -146,6 +147,9 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   a.ctas_per_ntile = std::max(1, std::min<int>(num_sms / a.n_tiles, a.num_mtiles));
+  if (S.pair == 2) a.ctas_per_ntile = std::max(2, a.ctas_per_ntile & ~1);  // whole CTA pairs
+  a.num_units = static_cast<int>((a.num_mtiles + S.pair - 1) / S.pair);
+  a.unit_stride = a.ctas_per_ntile / S.pair;
   a.row_bytes = p.cout_f * oes;
   a.acc_stride = pow2ceil(max_cols);
   a.tmem_cols = 2 * a.acc_stride;
@@ -268,12 +272,18 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
 
   const int grid = a.n_tiles * a.ctas_per_ntile;
   cudaError_t e;
+  if (S.pair == 2 && (prod == 1 || prod == 2)) {
+    *err = "the row producers run single-CTA plans";
+    return WF_UNSUPPORTED;
+  }
   if (tf32 && (S.CH != 32 || prod == 1 || prod == 2)) {
     *err = "tf32 plans use 32-column epilogue chunks and the TMA producer";
     return WF_UNSUPPORTED;
   }
   const int kind = tf32 ? 1 : 0;
-  if (prod == 0 || prod == 3)
+  if ((prod == 0 || prod == 3) && S.pair == 2)
+    e = launch_conv_pair(a, maps, grid, smem, st, out_dtype, S.CH);
+  else if (prod == 0 || prod == 3)
     e = launch_conv_prod<0>(a, maps, grid, smem, st, kind, out_dtype, S.CH);
   else if (prod == 1)
     e = launch_conv_prod<1>(a, maps, grid, smem, st, kind, out_dtype, S.CH);

@@ -54,6 +54,7 @@ struct ConvArgs {
   int n_tiles, ctas_per_ntile;
   int nt_entry0[kMaxNTiles], nt_entries[kMaxNTiles], nt_col0[kMaxNTiles], nt_cols[kMaxNTiles];
   int nt_split[kMaxNTiles];       // lower-half MMAs of the N-tile (-1: no accumulator half-split)
+  int num_units, unit_stride;     // M-tile units (pairs of M tiles in cta_group::2 mode) and the CTA stride
   int nt_bbytes[kMaxNTiles];
   long long nt_bsrc[kMaxNTiles];  // device address of the N-tile's packed B
   long long row_bytes;            // bytes of one folded output row = r*Cout*out_elem
@@ -403,7 +404,37 @@ __device__ __forceinline__ void transpose_row(const RowProd& p, const FoldChunks
   }
 }
 
-template <int kKind, typename OutT, int CH, int kProd>
+template <int kKind, int kPair>
+__device__ __forceinline__ void issue_mma(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  if constexpr (kPair == 2) {
+    static_assert(kKind == 0, "pair mode runs kind::f16");
+    ptx::mma_pair(d, adesc, bdesc, idesc, acc);
+  } else {
+    ptx::mma<kKind>(d, adesc, bdesc, idesc, acc);
+  }
+}
+template <int kPair>
+__device__ __forceinline__ void commit_to(uint32_t bar) {
+  if constexpr (kPair == 2) ptx::mma_commit_pair(bar, 0x3);  // both CTAs of the pair
+  else ptx::mma_commit(bar);
+}
+// Accumulator-drained signal. Single CTA: every thread arrives on its own
+// CTA's barrier. Pair: one remote arrive per warp (after every lane's
+// tcgen05.wait::ld) on the leader's barrier.
+template <int kPair>
+__device__ __forceinline__ void arrive_at(uint32_t bar) {
+  if constexpr (kPair == 2) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) ptx::mbar_arrive_cluster(bar);
+  } else {
+    ptx::mbar_arrive(bar);
+  }
+}
+
+// kPair = 2: a cluster of two CTAs (one per SM of a TPC) runs cta_group::2
+// MMAs -- M = 256 (each CTA's 128-row tile), each CTA holding half of every B
+// block, so the per-SM shared-memory operand traffic drops by the B half.
+template <int kKind, typename OutT, int CH, int kProd, int kPair = 1>
 __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     conv_fold_kernel(const __grid_constant__ ConvArgs a, const __grid_constant__ TmaMaps maps) {
   using namespace ptx;
@@ -416,6 +447,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   const uint32_t bar_tfull = base + 128;   // [2] x 8 B
   const uint32_t bar_tempty = base + 144;     // [2] x 8 B: lower half of the accumulator drained
   const uint32_t bar_tempty_hi = base + 168;  // [2] x 8 B: upper half drained
+  const uint32_t bar_bpeer = base + 184;      // pair: the peer's B half landed (leader's barrier)
   const uint32_t bar_b = base + 160;
   const uint32_t bar_raw_full = base + 256;   // [raw_slots <= 32] x 8 B
   const uint32_t bar_raw_empty = base + 512;  // [raw_slots <= 32] x 8 B
@@ -425,8 +457,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   // MMA issuer's operands in uniform registers)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const int ntile = blockIdx.x % a.n_tiles;
-  const int local = blockIdx.x / a.n_tiles;
+  const uint32_t rank = (kPair == 2) ? cluster_ctarank() : 0u;  // 0: pair leader (issues the MMAs)
+  const int cl = static_cast<int>(blockIdx.x) / kPair;           // cluster (or CTA) index
+  const int ntile = cl % a.n_tiles;
+  const int local = cl / a.n_tiles;                               // first M-tile unit of this CTA
   const int ncols = a.nt_cols[ntile];
   const int col0 = a.nt_col0[ntile];
 
@@ -447,10 +481,12 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_tfull + 8 * i, 1);
-      mbar_init(bar_tempty + 8 * i, 256);
-      mbar_init(bar_tempty_hi + 8 * i, 256);
+      // every epilogue thread arrives (pair: one arrive per warp of both CTAs, on the leader's)
+      mbar_init(bar_tempty + 8 * i, kPair == 2 ? 16 : 256);
+      mbar_init(bar_tempty_hi + 8 * i, kPair == 2 ? 16 : 256);
     }
     mbar_init(bar_b, 1);
+    mbar_init(bar_bpeer, 1);
     for (int i = 0; i < a.raw_slots; ++i) {
       mbar_init(bar_raw_full + 8 * i, 1);
       mbar_init(bar_raw_empty + 8 * i, 1);
@@ -464,9 +500,13 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         if (a.shift_box_bytes) prefetch_tmap(&maps.in_shift[b]);
       }
   }
-  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), a.tmem_cols);
+  if (warp == 1) {
+    if constexpr (kPair == 2) tmem_alloc_pair(smem_u32(tmem_slot), a.tmem_cols);
+    else tmem_alloc(smem_u32(tmem_slot), a.tmem_cols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair == 2) cluster_sync();  // the peer's barriers are initialised before remote use
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -556,22 +596,29 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   } else if (warp == 0) {
     // ===================== TMA producer (one elected lane) =====================
     if (elect_one()) {
-      const uint8_t* gb = reinterpret_cast<const uint8_t*>(a.nt_bsrc[ntile]);
-      const int bb = a.nt_bbytes[ntile];
+      const int bb = a.nt_bbytes[ntile];  // this CTA's B bytes (a half per CTA in pair mode)
+      const uint8_t* gb = reinterpret_cast<const uint8_t*>(a.nt_bsrc[ntile]) + rank * bb;
       mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
       for (int off = 0; off < bb; off += 32768)
         bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
+      if (kPair == 2 && rank != 0) {  // tell the leader's MMA issuer that our B half landed
+        mbar_wait(bar_b, 0);
+        mbar_arrive_cluster(mapa(bar_bpeer, 0));
+      }
       const uint32_t tx = static_cast<uint32_t>((a.box_bytes + a.shift_box_bytes) * __popc(a.res_mask));
       int it = 0;
-      for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it) {
+      for (int u = local; u < a.num_units; u += a.unit_stride, ++it) {
+        const int mt = u * kPair + static_cast<int>(rank);
         const int stage = it % a.stages;
         const uint32_t round = static_cast<uint32_t>(it / a.stages);
         mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
+        // pair: both CTAs' boxes complete on the leader's full barrier
+        const uint32_t fbar = (kPair == 2) ? mapa(bar_full + 8 * stage, 0) : bar_full + 8 * stage;
         const int n = mt / a.ohb;
         const int oh0 = (mt - n * a.ohb) * a.OHt;
         const uint32_t dst = base + a.off_a + stage * a.stage_bytes;
         if (a.epi_flags & 0x1000) {  // profiling: no A loads (stage contents stale)
-          mbar_arrive(bar_full + 8 * stage);
+          if (rank == 0) mbar_arrive(bar_full + 8 * stage);
           continue;
         }
         // profiling only: 0x20000 drops the shift boxes, 0x40000 loads residue 0 only
@@ -583,14 +630,21 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
             if (((a.res_mask >> b) & 1u) && !(dbg_oneres && b != __ffs(a.res_mask) - 1))
               txs += a.box_bytes + (dbg_noshift ? 0 : a.shift_box_bytes);
         }
-        mbar_arrive_expect_tx(bar_full + 8 * stage, txs);
+        if (rank == 0) mbar_arrive_expect_tx(bar_full + 8 * stage, txs * kPair);
         for (int b = 0; b < a.s; ++b) {
           if (!((a.res_mask >> b) & 1u)) continue;
           if (dbg_oneres && b != __ffs(a.res_mask) - 1) continue;
-          tma_load_5d(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, bar_full + 8 * stage);
-          if (a.shift_box_bytes && !dbg_noshift)
-            tma_load_5d(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1, oh0 + a.amin[b], 0, n,
-                        bar_full + 8 * stage);
+          if constexpr (kPair == 2) {
+            tma_load_5d_pair(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, fbar);
+            if (a.shift_box_bytes && !dbg_noshift)
+              tma_load_5d_pair(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1,
+                               oh0 + a.amin[b], 0, n, fbar);
+          } else {
+            tma_load_5d(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, fbar);
+            if (a.shift_box_bytes && !dbg_noshift)
+              tma_load_5d(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1, oh0 + a.amin[b], 0,
+                          n, fbar);
+          }
         }
       }
     }
@@ -601,11 +655,14 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // uniform registers straight from the constant bank; one lane issues.
     const bool skip_mma = (a.epi_flags & 0x100) != 0;  // profiling switch
     const uint32_t b_lo = (base + a.off_b) >> 4;
-    const bool leader = elect_one();
+    const bool leader = elect_one() && rank == 0;  // pair: the leader CTA issues for both SMs
+    if (kPair == 2 && rank != 0) goto mma_done;
     mbar_wait(bar_b, 0);
+    if constexpr (kPair == 2) mbar_wait_cluster(bar_bpeer, 0);
+    {
     int it = 0;  // A stages consumed (ksplit per M tile)
     int tile = 0;
-    for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++tile) {
+    for (int u = local; u < a.num_units; u += a.unit_stride, ++tile) {
       const int acc = tile & 1;
       const uint32_t acc_round = static_cast<uint32_t>(tile >> 1);
       const int split = (a.ksplit == 1) ? a.nt_split[ntile] : -1;
@@ -627,7 +684,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
               const uint4 e = a.table[e0 + i];
               const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
               const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
-              if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
+              if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
             }
             mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
             tc_fence_after();
@@ -638,24 +695,26 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
               const uint4 e = a.table[e0 + i + j];
               const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
               const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
-              if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
+              if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
             }
           }
           for (; i < entries; ++i) {
             const uint4 e = a.table[e0 + i];
             const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
             const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
-            if (leader) mma<kKind>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
+            if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
           }
         }
         else if (split > 0) {
           mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
         }
-        if (leader) mma_commit(bar_empty + 8 * stage);
+        if (leader) commit_to<kPair>(bar_empty + 8 * stage);
       }
-      if (leader) mma_commit(bar_tfull + 8 * acc);
+      if (leader) commit_to<kPair>(bar_tfull + 8 * acc);
       __syncwarp();
     }
+    }
+  mma_done:;
   } else if (warp >= 2 && warp < 10) {
     // ===================== epilogue (warps 2..9) =====================
     // Warp w owns TMEM lanes [32q, 32q+32), q = w % 4, and every other
@@ -705,7 +764,11 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         row_w[h16][r8] = m - row_t[h16][r8] * a.Wbox;
       }
     int it_tile = 0;
-    for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile, ++it_tile) {
+    // pair: arrivals go to the leader's accumulator-free barriers
+    const uint32_t te_lo = (kPair == 2) ? mapa(bar_tempty, 0) : bar_tempty;
+    const uint32_t te_hi = (kPair == 2) ? mapa(bar_tempty_hi, 0) : bar_tempty_hi;
+    for (int u = local; u < a.num_units; u += a.unit_stride, ++it_tile) {
+      const int mt = u * kPair + static_cast<int>(rank);
       const int acc = it_tile & 1;
       const uint32_t acc_round = static_cast<uint32_t>(it_tile >> 1);
       const int n = mt / a.ohb;
@@ -714,8 +777,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       tc_fence_after();
       if (dbg_skip_epi || n_it == 0) {
         tc_fence_before();
-        mbar_arrive(bar_tempty + 8 * acc);
-        mbar_arrive(bar_tempty_hi + 8 * acc);
+        arrive_at<kPair>(te_lo + 8 * acc);
+        arrive_at<kPair>(te_hi + 8 * acc);
         continue;
       }
       uint8_t* rowp[2][2];  // first output pixel of the row (its j = 0 sub-column)
@@ -733,7 +796,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
           } else {
             const int t = row_t[h16][r8], wq = row_w[h16][r8];
             const int oh = oh0 + t;
-            rowv[h16][r8] = (wq < a.Wfo) && (t < a.OHt) && (oh < a.OH) && !dbg_skip_store;
+            rowv[h16][r8] = (wq < a.Wfo) && (t < a.OHt) && (oh < a.OH) && (n < a.n_img) && !dbg_skip_store;
             roww[h16][r8] = wq * a.r;
             rowp[h16][r8] = a.out + ((static_cast<long long>(n) * a.OH + oh) * a.OW + wq * a.r) * a.Cout *
                                         static_cast<long long>(sizeof(OutT));
@@ -744,7 +807,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       auto taddr = [&](int it) {
         return tq + (static_cast<uint32_t>((it & 1) * 16) << 16) + static_cast<uint32_t>((half + 2 * (it >> 1)) * CH);
       };
-      if (lo_it == 0) mbar_arrive(bar_tempty + 8 * acc);  // this warp reads no lower-half column
+      if (lo_it == 0) arrive_at<kPair>(te_lo + 8 * acc);  // this warp reads no lower-half column
       uint32_t buf[2][NREG];
       tmem_ld_16x256b<NREG>(taddr(0), buf[0], skip_ld);
 #pragma unroll
@@ -771,19 +834,21 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         }
         if (it + 1 == lo_it) {  // lower half of the accumulator read (its wait::ld is done)
           tc_fence_before();
-          mbar_arrive(bar_tempty + 8 * acc);
+          arrive_at<kPair>(te_lo + 8 * acc);
         }
       }
       tc_fence_before();
-      mbar_arrive(bar_tempty_hi + 8 * acc);
+      arrive_at<kPair>(te_hi + 8 * acc);
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair == 2) cluster_sync();  // the leader's MMAs wrote this CTA's TMEM
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, a.tmem_cols);
+    if constexpr (kPair == 2) tmem_dealloc_pair(tmem_base, a.tmem_cols);
+    else tmem_dealloc(tmem_base, a.tmem_cols);
   }
 }
 
@@ -822,6 +887,34 @@ cudaError_t launch_conv_prod(const ConvArgs& args, const TmaMaps& maps, int grid
   if (out == WF_F16) return launch_typed<0, __half, 32, kProd>(args, maps, grid, smem, st);
   return launch_typed<0, float, 32, kProd>(args, maps, grid, smem, st);
 }
+
+// CTA-pair launch (cluster of 2, cta_group::2 MMAs), TMA producer, kind::f16.
+template <typename OutT, int CH>
+cudaError_t launch_pair_typed(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st) {
+  auto kern = conv_fold_kernel<0, OutT, CH, 0, 2>;
+  static int configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args, maps);
+}
+
+cudaError_t launch_conv_pair(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st,
+                             wf_dtype out, int ch);
 
 extern template cudaError_t launch_conv_prod<0>(const ConvArgs&, const TmaMaps&, int, int, cudaStream_t, int, wf_dtype,
                                                 int);

@@ -32,6 +32,8 @@ struct PackArgs {
   int nt_entry0[kMaxNTiles];
   int nt_g0[kMaxNTiles];
   long long nt_boff[kMaxNTiles];
+  long long nt_bbytes[kMaxNTiles];
+  int pair;  // 2: rows [0, N/2) of every block go to the first half of the N-tile's B, [N/2, N) to the second
   long long table_bytes;
   int round_tf32;
 };
@@ -76,7 +78,14 @@ __global__ void pack_b_kernel(const T* __restrict__ w, uint8_t* __restrict__ pac
     const int kw = (a.c0 + kp) * a.f + fi - j * a.s + a.pw;
     T val = T(0.0f);
     if (kw >= 0 && kw < a.KW) val = w[((static_cast<long long>(kh) * a.KW + kw) * a.C + c) * a.Cout + co];
-    uint8_t* dst = packed + a.table_bytes + a.nt_boff[nt] + e.y + cc * (N * 16) + nrow * 16 + e8 * a.esize;
+    uint8_t* dst;
+    if (a.pair == 2) {  // CTA r of the pair loads [nt_boff + r * b_bytes / 2, ...): its half of every block
+      const int h = nrow / (N / 2), rr = nrow - h * (N / 2);
+      dst = packed + a.table_bytes + a.nt_boff[nt] + h * (a.nt_bbytes[nt] / 2) + e.y / 2 + cc * (N / 2 * 16) +
+            rr * 16 + e8 * a.esize;
+    } else {
+      dst = packed + a.table_bytes + a.nt_boff[nt] + e.y + cc * (N * 16) + nrow * 16 + e8 * a.esize;
+    }
     if constexpr (sizeof(T) == 4) {
       float v = to_f(val);
       if (a.round_tf32) {
@@ -144,12 +153,14 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
   a.E = S.E;
   a.esize = S.esize;
   a.CH = S.CH;
+  a.pair = S.pair;
   a.entries = static_cast<int>(S.entries.size());
   a.n_tiles = static_cast<int>(S.ntiles.size());
   for (int i = 0; i < a.n_tiles; ++i) {
     a.nt_entry0[i] = S.ntiles[i].entry0;
     a.nt_g0[i] = S.ntiles[i].g0;
     a.nt_boff[i] = S.ntiles[i].b_off;
+    a.nt_bbytes[i] = S.ntiles[i].b_bytes;
   }
   a.table_bytes = p.table_bytes;
   a.round_tf32 = 1;

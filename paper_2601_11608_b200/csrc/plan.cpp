@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 namespace wfb {
@@ -440,6 +441,27 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   p.workspace_bytes = (S.prod == 3) ? d.n * d.h * S.Wp * d.c * S.esize : 0;
   S.ohb = ceil_div(OH, OHt);
   S.num_mtiles = d.n * S.ohb;
+  // CTA pairs (cta_group::2, M = 256): each SM holds and reads half of every
+  // B block. bf16/fp16 TMA plans with N a multiple of 16; more A stages fit.
+  // Opt-in (WF_CTA_PAIR=1): measured slower on B200 for these shapes -- the
+  // pair MMA saves only ~10% at N=64 and nothing at N>=128
+  // (tools/probes/pair_probe.cu) while the pair synchronisation costs more.
+  {
+    const char* env = std::getenv("WF_CTA_PAIR");
+    bool pair = env != nullptr && env[0] == '1';
+    pair = pair && in_dtype != WF_TF32 && (S.prod == 0 || S.prod == 3) && S.num_mtiles >= 2;
+    for (const MmaEntry& e : S.entries) pair = pair && (((e.meta >> 22) & 0x1FFu) * 8) % 16 == 0;
+    if (pair) {
+      int64_t max_b = 0;
+      for (const auto& t : S.ntiles) max_b = std::max(max_b, t.b_bytes / 2);
+      S.pair = 2;
+      S.b_smem_bytes = static_cast<int>((max_b + 127) / 128 * 128);
+      const int64_t fixed = 1024 + kTileM * 16 + 128 + S.b_smem_bytes + kMaxAccCols * 4 + 1024;
+      for (int st2 = 6; st2 >= 2; --st2)
+        if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { S.stages = st2; break; }
+    }
+    p.cta_pair = S.pair;
+  }
   p.useful_macs = static_cast<uint64_t>(d.n) * OH * OW * d.cout * d.kh * d.kw * d.c;
   uint64_t issued_per_tile = 0;
   for (const MmaEntry& e : S.entries) issued_per_tile += static_cast<uint64_t>(kTileM) * ((e.meta >> 22) & 0x1FFu) * 8 * S.E;
@@ -564,6 +586,7 @@ wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Sched
   p.epi_chunk = S.CH;
   p.variant = WF_VARIANT_UNFOLDED;
   p.producer = 2;
+  p.cta_pair = 1;
   const int64_t total = d.n * OH * OW;
   S.num_mtiles = ceil_div(total, kTileM);
   S.ohb = 1;

@@ -96,6 +96,7 @@ struct Schedule {
   int prod = 0;                  // A producer: 0 TMA boxes, 1 row gather (folded), 2 row gather
                                  // (im2col), 3 re-pitch into the workspace + TMA boxes
   int64_t Wp = 0;                // input width the TMA view uses (re-pitched when != W)
+  int pair = 1;                  // 2: CTA-pair (cta_group::2) MMAs, B blocks split across the pair
   int U = 0;                     // im2col: 32-byte K-steps per kh
   int ksplit = 1;                // A stages per M tile (im2col: kh ranges)
   int raw_slots = 0, raw_slot_bytes = 0;  // staged-row ring of the row producer (prod 1/2)

@@ -146,13 +146,22 @@ def test_packed_operand_unpacks_to_the_expansion(oracle):
     order = raw[n_ent * 16: n_ent * 16 + 4 * G].view(np.int32)
     assert sorted(order.tolist()) == list(range(G))
     base = (n_ent * 16 + 4 * G + 127) // 128 * 128
+    pair = d["cta_pair"]
+    b_total = len(raw) - base
     checked = 0
     covered = np.zeros((KH, G), np.int64)
     for (a_off, b_off, meta, col) in table:
         kh, u, slot = meta & 0xFF, (meta >> 8) & 0xFF, (meta >> 16) & 0x3F
         N = ((meta >> 22) & 0x1FF) * 8
         assert col == slot * Ng
-        blk = raw[base + b_off: base + b_off + N * 32].view(np.uint16).reshape(2, N, 8)
+        if pair == 2:  # CTA r of the pair holds rows [r*N/2, (r+1)*N/2) of every block
+            halves = []
+            for r in range(2):
+                o = base + r * (b_total // 2) + b_off // 2
+                halves.append(raw[o: o + N * 16].view(np.uint16).reshape(2, N // 2, 8))
+            blk = np.concatenate(halves, axis=1)
+        else:
+            blk = raw[base + b_off: base + b_off + N * 32].view(np.uint16).reshape(2, N, 8)
         vals = (blk.astype(np.uint32) << 16).view(np.float32)
         for n in range(N):
             g = order[slot + n // Ng]
