@@ -118,9 +118,13 @@ __device__ __forceinline__ void tmem_ld_16x256b(uint32_t taddr, uint32_t (&r)[NR
   if constexpr (NREG == 32) ptx::tmem_ld_16x256b_x8(taddr, r); else ptx::tmem_ld_16x256b_x4(taddr, r);
 }
 
-// VPT consecutive output channels of one row -> global, 32-byte stores.
-template <typename OutT, int VPT>
+// VPT consecutive output channels of one row -> global, 32-byte stores
+// (kStream: L1::no_allocate + L2::evict_first).
+template <typename OutT, int VPT, bool kStream>
 __device__ __forceinline__ void store_row(uint8_t* dst, const float (&v)[VPT]) {
+  auto st8 = [](uint8_t* p, const uint32_t* w) {
+    if constexpr (kStream) ptx::st_global_v8_stream(p, w); else ptx::st_global_v8(p, w);
+  };
   if constexpr (sizeof(OutT) == 4) {
     static_assert(VPT % 8 == 0, "fp32 rows are stored 8 values at a time");
 #pragma unroll
@@ -128,17 +132,18 @@ __device__ __forceinline__ void store_row(uint8_t* dst, const float (&v)[VPT]) {
       uint32_t pk[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) pk[k] = __float_as_uint(v[8 * q + k]);
-      ptx::st_global_v8(dst + 32 * q, pk);
+      st8(dst + 32 * q, pk);
     }
   } else if constexpr (VPT == 16) {
     uint32_t pk[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) pk[k] = pack2<OutT>(v[2 * k], v[2 * k + 1]);
-    ptx::st_global_v8(dst, pk);
+    st8(dst, pk);
   } else {
     static_assert(VPT == 8, "2-byte rows are 8 or 16 values");
-    ptx::st_global_v4(dst, make_uint4(pack2<OutT>(v[0], v[1]), pack2<OutT>(v[2], v[3]), pack2<OutT>(v[4], v[5]),
-                                      pack2<OutT>(v[6], v[7])));
+    const uint4 w = make_uint4(pack2<OutT>(v[0], v[1]), pack2<OutT>(v[2], v[3]), pack2<OutT>(v[4], v[5]),
+                               pack2<OutT>(v[6], v[7]));
+    if constexpr (kStream) ptx::st_global_v4_stream(dst, w); else ptx::st_global_v4(dst, w);
   }
 }
 
@@ -660,14 +665,19 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     mbar_wait(bar_b, 0);
     if constexpr (kPair == 2) mbar_wait_cluster(bar_bpeer, 0);
     {
+    // profiling (0x80000, CTA 0): cycles the issuer waits on the accumulator / the A stage
+    const bool dbg = (a.epi_flags & 0x80000) && blockIdx.x == 0;
+    long long w_acc = 0, w_full = 0, w_hi = 0, t_all = dbg ? clock64() : 0;
     int it = 0;  // A stages consumed (ksplit per M tile)
     int tile = 0;
     for (int u = local; u < a.num_units; u += a.unit_stride, ++tile) {
       const int acc = tile & 1;
       const uint32_t acc_round = static_cast<uint32_t>(tile >> 1);
       const int split = (a.ksplit == 1) ? a.nt_split[ntile] : -1;
+      long long t0 = dbg ? clock64() : 0;
       mbar_wait(bar_tempty + 8 * acc, (acc_round & 1u) ^ 1u);
       if (split < 0) mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
+      if (dbg) { const long long t1 = clock64(); w_acc += t1 - t0; t0 = t1; }
       const uint32_t d_base = tmem_base + acc * a.acc_stride;
       for (int ks = 0; ks < a.ksplit; ++ks, ++it) {
         const int stage = it % a.stages;
@@ -675,6 +685,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         const int e0 = (a.ksplit == 1) ? a.nt_entry0[ntile] : a.ks_entry0[ks];
         const int entries = (a.ksplit == 1) ? a.nt_entries[ntile] : a.ks_entries[ks];
         mbar_wait(bar_full + 8 * stage, round & 1u);
+        if (dbg) { const long long t1 = clock64(); w_full += t1 - t0; t0 = t1; }
         tc_fence_after();
         const uint32_t a_lo = (base + a.off_a + stage * a.stage_bytes) >> 4;
         if (!skip_mma) {
@@ -686,7 +697,9 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
               const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
               if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
             }
+            if (dbg) t0 = clock64();
             mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
+            if (dbg) w_hi += clock64() - t0;
             tc_fence_after();
           }
           for (; i + 8 <= entries; i += 8) {
@@ -713,6 +726,9 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       if (leader) commit_to<kPair>(bar_tfull + 8 * acc);
       __syncwarp();
     }
+    if (dbg && leader)
+      printf("mma issuer cta0: %d tiles, %lld cycles: wait accumulator %lld (upper half %lld), wait A stage %lld\n",
+             tile, clock64() - t_all, w_acc, w_hi, w_full);
     }
   mma_done:;
   } else if (warp >= 2 && warp < 10) {
@@ -740,6 +756,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     const bool dbg_skip_epi = (a.epi_flags & 0x200) != 0;
     const bool dbg_skip_store = (a.epi_flags & 0x400) != 0;
     const bool skip_ld = (a.epi_flags & 0x800) != 0;
+    const bool stream_st = (a.epi_flags & 0x100000) != 0;  // experiment: streaming store hints
     const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
     float breg[CPW][VPT];   // bias of this thread's channels in each of its chunks
     long long coff[CPW];    // byte offset of each chunk's first output column in a row
@@ -830,7 +847,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
 #pragma unroll
             for (int k = 0; k < VPT; ++k) v[k] = (v[k] < 0.0f) ? 0.0f : v[k];
           }
-          if (rowv[h16][r8] && roww[h16][r8] + jsub[cc] < a.OW) store_row<OutT, VPT>(rowp[h16][r8] + coff[cc], v);
+          if (rowv[h16][r8] && roww[h16][r8] + jsub[cc] < a.OW) {
+            if (stream_st) store_row<OutT, VPT, true>(rowp[h16][r8] + coff[cc], v);
+            else store_row<OutT, VPT, false>(rowp[h16][r8] + coff[cc], v);
+          }
         }
         if (it + 1 == lo_it) {  // lower half of the accumulator read (its wait::ld is done)
           tc_fence_before();

@@ -25,6 +25,9 @@
 
 namespace wfb {
 
+constexpr int kPackMaxGroups = 32;
+constexpr int kPackMaxUnits = 12;
+
 struct PackArgs {
   int KH, KW, C, Cout, f, s, pw, c0, gs, Ng, E, esize, CH;
   int entries;
@@ -34,6 +37,11 @@ struct PackArgs {
   long long nt_boff[kMaxNTiles];
   long long nt_bbytes[kMaxNTiles];
   int pair;  // 2: rows [0, N/2) of every block go to the first half of the N-tile's B, [N/2, N) to the second
+  // per group: its K-step starts (a K column covered by two steps of a group is
+  // kept in the lower one and zeroed in the upper one)
+  int n_groups;
+  int n_units[kPackMaxGroups];
+  unsigned char units[kPackMaxGroups][kPackMaxUnits];
   long long table_bytes;
   int round_tf32;
 };
@@ -76,8 +84,12 @@ __global__ void pack_b_kernel(const T* __restrict__ w, uint8_t* __restrict__ pac
     const int j = g * a.gs + ncol / a.Cout;
     const int co = ncol - (ncol / a.Cout) * a.Cout;
     const int kw = (a.c0 + kp) * a.f + fi - j * a.s + a.pw;
+    // core column u of this step is owned by the group's step at u-1 if it has one
+    bool dup = false;
+    if (cc == 0 && g < a.n_groups)
+      for (int k = 0; k < a.n_units[g]; ++k) dup = dup || (a.units[g][k] + 1 == u);
     T val = T(0.0f);
-    if (kw >= 0 && kw < a.KW) val = w[((static_cast<long long>(kh) * a.KW + kw) * a.C + c) * a.Cout + co];
+    if (!dup && kw >= 0 && kw < a.KW) val = w[((static_cast<long long>(kh) * a.KW + kw) * a.C + c) * a.Cout + co];
     uint8_t* dst;
     if (a.pair == 2) {  // CTA r of the pair loads [nt_boff + r * b_bytes / 2, ...): its half of every block
       const int h = nrow / (N / 2), rr = nrow - h * (N / 2);
@@ -154,6 +166,19 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
   a.esize = S.esize;
   a.CH = S.CH;
   a.pair = S.pair;
+  a.n_groups = static_cast<int>(std::min<size_t>(S.units.size(), kPackMaxGroups));
+  for (int g = 0; g < a.n_groups; ++g) {
+    if (S.units[g].size() > static_cast<size_t>(kPackMaxUnits)) {
+      *err = "pack: too many K-steps per group";
+      return WF_UNSUPPORTED;
+    }
+    a.n_units[g] = static_cast<int>(S.units[g].size());
+    for (size_t k = 0; k < S.units[g].size(); ++k) a.units[g][k] = static_cast<unsigned char>(S.units[g][k]);
+  }
+  if (S.units.size() > static_cast<size_t>(kPackMaxGroups)) {
+    *err = "pack: too many output groups";
+    return WF_UNSUPPORTED;
+  }
   a.entries = static_cast<int>(S.entries.size());
   a.n_tiles = static_cast<int>(S.ntiles.size());
   for (int i = 0; i < a.n_tiles; ++i) {

@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <functional>
 #include <cstdlib>
 #include <numeric>
 
@@ -201,12 +202,101 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
       hi[g] = std::max(hi[g], (off + d.kw * d.c - 1) / E2);
     }
   }
-  // units of group g start at core columns lo, lo+2, ... (pairs (c, c+1))
-  auto n_units = [&](int64_t g) { return (hi[g] - lo[g] + 2) / 2; };
+  // ---- 32-byte K-steps ("units": core columns (c, c+1)) covering each group's window
+  // Legacy cover: starts lo, lo+2, ... A start c with c % Q == Q-1 straddles two
+  // folded pixels and needs the shifted A region (25% more TMA pieces). When
+  // Q >= 2 the planner also tries covers that never straddle (overlapping K
+  // columns are zeroed in B for all but the first covering unit) and keeps
+  // them when the merged MMA cost is no higher: fewer A views per kh, wider
+  // merged MMAs, no shift region.
+  std::vector<std::vector<int64_t>> U(G);
+  for (int64_t g = 0; g < G; ++g)
+    for (int64_t c = lo[g]; c <= hi[g]; c += 2) U[g].push_back(c);
+  const int64_t max_col = kwf * Q - 1;  // last core column of the KW'*f*C window row
+  auto mma_cost = [](int64_t n) { return std::max<int64_t>(n / 2, 32 + n / 4); };
+  // merged cost of groups [g0, g1) in slot order `order` with unit sets `us`
+  auto merged_cost = [&](const std::vector<int>& order, const std::vector<std::vector<int64_t>>& us) {
+    std::vector<int64_t> starts;
+    for (const auto& v : us) starts.insert(starts.end(), v.begin(), v.end());
+    std::sort(starts.begin(), starts.end());
+    starts.erase(std::unique(starts.begin(), starts.end()), starts.end());
+    int64_t cost = 0;
+    for (int64_t st : starts) {
+      int run = 0;
+      for (size_t k = 0; k <= order.size(); ++k) {
+        const bool has = k < order.size() &&
+                         std::find(us[order[k]].begin(), us[order[k]].end(), st) != us[order[k]].end();
+        if (has) {
+          ++run;
+        } else if (run) {
+          cost += mma_cost(run * static_cast<int64_t>(gs * d.cout));
+          run = 0;
+        }
+      }
+    }
+    return cost;
+  };
+  auto best_order_cost = [&](const std::vector<std::vector<int64_t>>& us) {
+    std::vector<int> order(us.size());
+    std::iota(order.begin(), order.end(), 0);
+    int64_t best = merged_cost(order, us);
+    while (std::next_permutation(order.begin(), order.end())) best = std::min(best, merged_cost(order, us));
+    return best;
+  };
+  if (Q >= 2) {
+    // all minimal non-straddling covers of [l, h]
+    std::function<void(int64_t, int64_t, std::vector<int64_t>&, std::vector<std::vector<int64_t>>&)> covers =
+        [&](int64_t p, int64_t h, std::vector<int64_t>& cur, std::vector<std::vector<int64_t>>& outv) {
+          if (p > h) {
+            outv.push_back(cur);
+            return;
+          }
+          for (int64_t st : {p, p - 1}) {
+            if (st < 0 || st + 1 > max_col || st % Q == Q - 1) continue;
+            cur.push_back(st);
+            covers(st + 2, h, cur, outv);
+            cur.pop_back();
+          }
+        };
+    // column tiles of at most 256 accumulator columns, searched jointly (<= 5 groups)
+    for (int64_t g0 = 0; g0 < G;) {
+      int64_t g1 = g0;
+      while (g1 < G && (g1 - g0 + 1) * S.Ng <= kMaxAccCols) ++g1;
+      const int64_t ng = g1 - g0;
+      std::vector<std::vector<std::vector<int64_t>>> cand(ng);
+      bool ok = ng <= 5;
+      for (int64_t k = 0; k < ng && ok; ++k) {
+        std::vector<int64_t> cur;
+        covers(lo[g0 + k], hi[g0 + k], cur, cand[k]);
+        ok = !cand[k].empty();
+      }
+      if (ok) {
+        std::vector<std::vector<int64_t>> legacy(U.begin() + g0, U.begin() + g1);
+        const int64_t legacy_cost = best_order_cost(legacy);
+        std::vector<size_t> idx(ng, 0);
+        std::vector<std::vector<int64_t>> best_us;
+        int64_t best = INT64_MAX;
+        for (int guard = 0; guard < 4096; ++guard) {
+          std::vector<std::vector<int64_t>> us(ng);
+          for (int64_t k = 0; k < ng; ++k) us[k] = cand[k][idx[k]];
+          const int64_t c = best_order_cost(us);
+          if (c < best) { best = c; best_us = us; }
+          int64_t k = 0;
+          while (k < ng && ++idx[k] == cand[k].size()) idx[k++] = 0;
+          if (k == ng) break;
+        }
+        if (best <= legacy_cost)
+          for (int64_t k = 0; k < ng; ++k) U[g0 + k] = best_us[k];
+      }
+      g0 = g1;
+    }
+  }
+  auto n_units = [&](int64_t g) { return static_cast<int64_t>(U[g].size()); };
   S.need_shift = false;
   for (int64_t g = 0; g < G; ++g)
-    for (int64_t i = 0; i < n_units(g); ++i)
-      if ((lo[g] + 2 * i) % Q == Q - 1) S.need_shift = true;
+    for (int64_t st : U[g])
+      if (st % Q == Q - 1) S.need_shift = true;
+  S.units = U;
   S.lbo_a = static_cast<int>(NR * Wbox * 16);
   S.region_bytes = static_cast<int>((((Q + (S.need_shift ? 1 : 0)) * S.lbo_a) + 127) / 128 * 128);
   S.stage_bytes = static_cast<int>(sh) * S.region_bytes;
@@ -280,12 +370,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   // each N-tile is chosen to maximise such runs under a per-MMA cost model
   // measured on B200 (tools/probes/mma_probe.cu: N=64 -> 55, 128 -> 67,
   // 256 -> 128 cycles; shared-memory operand reads bound small N).
-  auto unit_set = [&](int64_t g) {
-    std::vector<int64_t> u;
-    for (int64_t i = 0; i < n_units(g); ++i) u.push_back(lo[g] + 2 * i);
-    return u;
-  };
-  auto mma_cost = [](int64_t n) { return std::max<int64_t>(n / 2, 32 + n / 4); };
+  auto unit_set = [&](int64_t g) { return U[g]; };
   // runs of one N-tile for a slot order: (u, first slot, number of slots)
   struct Run { int64_t u; int slot0, len; };
   auto runs_for = [&](const NTile& t, const std::vector<int>& order) {
@@ -334,11 +419,35 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
     }
     for (size_t sidx = 0; sidx < order.size(); ++sidx) S.order[t.g0 + sidx] = order[sidx];
     const std::vector<Run> runs = runs_for(t, order);
-    // zero-init: at kh == 0 every group's first MMA must not accumulate; issue
-    // the runs in decreasing length so each run meets either only untouched
-    // or only touched groups (checked below)
-    std::vector<Run> first = runs;
-    std::stable_sort(first.begin(), first.end(), [](const Run& x, const Run& y) { return x.len > y.len; });
+    // zero-init: at kh == 0 every group's first MMA must not accumulate, so the
+    // kh == 0 runs are ordered such that each one meets either only untouched
+    // groups (accumulate = 0) or only touched ones (backtracking, few runs)
+    std::vector<Run> first;
+    {
+      std::vector<Run> pool = runs;
+      std::stable_sort(pool.begin(), pool.end(), [](const Run& x, const Run& y) { return x.len > y.len; });
+      std::vector<char> used(pool.size(), 0), tch(order.size(), 0);
+      std::vector<Run> seq;
+      std::function<bool()> place = [&]() -> bool {
+        if (seq.size() == pool.size()) return true;
+        for (size_t k = 0; k < pool.size(); ++k) {
+          if (used[k]) continue;
+          int nt = 0;
+          for (int q = 0; q < pool[k].len; ++q) nt += tch[pool[k].slot0 + q];
+          if (nt != 0 && nt != pool[k].len) continue;
+          std::vector<char> saved = tch;
+          for (int q = 0; q < pool[k].len; ++q) tch[pool[k].slot0 + q] = 1;
+          used[k] = 1;
+          seq.push_back(pool[k]);
+          if (place()) return true;
+          seq.pop_back();
+          used[k] = 0;
+          tch = saved;
+        }
+        return false;
+      };
+      first = place() ? seq : pool;  // no valid order: the check below falls back
+    }
     t.entry0 = static_cast<int>(S.entries.size());
     t.b_off = b_cursor;
     uint32_t boff = 0;

@@ -111,6 +111,7 @@ struct Schedule {
   std::vector<MmaEntry> entries;
   std::vector<NTile> ntiles;
   std::vector<int> order;        // accumulator slot (g0 + s of its N-tile) -> group
+  std::vector<std::vector<int64_t>> units;  // per group: the first core columns of its K-steps
 };
 
 // Validates the descriptor like ConvSpec::validate (src/refconv.cpp:5-32) plus
