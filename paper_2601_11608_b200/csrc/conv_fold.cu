@@ -101,7 +101,8 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     a.amin[b] = S.amin[b];
   }
   const int Q = S.Q;
-  a.box_bytes = Q * S.lbo_a;
+  // bytes each residue's boxes land per stage (the A full barrier's tx count)
+  a.box_bytes = S.sw32 ? static_cast<int>(S.qs.size() * p.wbox * p.nrows * 32) : Q * S.lbo_a;
   a.shift_box_bytes = S.need_shift ? S.lbo_a : 0;
   a.shift_off = Q * S.lbo_a;
   a.region_bytes = S.region_bytes;
@@ -243,12 +244,43 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     if (rs != WF_OK) return rs;
     xt = workspace;
   }
+  // ---- A descriptor high word and the SWIZZLE_32B layout parameters -------------
+  a.sw32 = S.sw32 ? 1 : 0;
+  a.a_desc_hi = S.sw32 ? ((6u << 29) | (1u << 14) | (256u >> 4))   // SWIZZLE_32B, version 1, SBO 256 B
+                       : ((1u << 14) | (128u >> 4));                // no swizzle, version 1, SBO 128 B
+  a.nq = static_cast<int>(S.qs.size());
+  a.qregion_bytes = S.qregion_bytes;
+  for (int qi = 0; qi < a.nq && qi < 4; ++qi) {
+    a.qcoord[qi] = S.qs[qi] * (16 / es);
+    a.qbyte[qi] = S.qs[qi] * 16;
+  }
+  if (a.nq > 4) {
+    *err = "too many SWIZZLE_32B regions";
+    return WF_UNSUPPORTED;
+  }
   // ---- input tensor maps (one 5-D view per H-stride residue) --------------------
   const cuuint64_t rowpitch = static_cast<cuuint64_t>(prod == 3 ? S.Wp : d.w) * d.c * es;
   const cuuint64_t pix = static_cast<cuuint64_t>(p.f) * d.c * es;
   for (int b = 0; b < S.s && (prod == 0 || prod == 3); ++b) {
     if (!S.has_res[b]) continue;
     const cuuint64_t rows_b = static_cast<cuuint64_t>((d.h - b + S.s - 1) / S.s);
+    if (S.sw32) {  // {pixel elements, folded col, input row of residue b, image}; 32-byte boxes
+      cuuint64_t gdim4[4] = {static_cast<cuuint64_t>(p.f * d.c), static_cast<cuuint64_t>(p.wf), rows_b,
+                             static_cast<cuuint64_t>(d.n)};
+      cuuint64_t gstr4[3] = {pix, rowpitch * S.s, rowpitch * d.h};
+      cuuint32_t box4[4] = {static_cast<cuuint32_t>(32 / es), static_cast<cuuint32_t>(p.wbox),
+                            static_cast<cuuint32_t>(p.nrows), 1};
+      cuuint32_t estr4[4] = {1, 1, 1, 1};
+      void* gaddr4 = const_cast<uint8_t*>(static_cast<const uint8_t*>(xt) + b * rowpitch);
+      const CUresult r4 = encode(&maps.in[b], tmap_type(in_t), 4, gaddr4, gdim4, gstr4, box4, estr4,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r4 != CUDA_SUCCESS) {
+        *err = "cuTensorMapEncodeTiled(input, swizzle 32B) failed: " + std::to_string(static_cast<int>(r4));
+        return WF_CUDA_ERROR;
+      }
+      continue;
+    }
     cuuint64_t gdim[5] = {static_cast<cuuint64_t>(16 / es), static_cast<cuuint64_t>(p.wf), rows_b,
                           static_cast<cuuint64_t>(Q), static_cast<cuuint64_t>(d.n)};
     cuuint64_t gstr[4] = {pix, rowpitch * S.s, 16, rowpitch * d.h};

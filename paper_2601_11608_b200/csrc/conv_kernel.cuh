@@ -55,6 +55,10 @@ struct ConvArgs {
   int nt_entry0[kMaxNTiles], nt_entries[kMaxNTiles], nt_col0[kMaxNTiles], nt_cols[kMaxNTiles];
   int nt_split[kMaxNTiles];       // lower-half MMAs of the N-tile (-1: no accumulator half-split)
   int num_units, unit_stride;     // M-tile units (pairs of M tiles in cta_group::2 mode) and the CTA stride
+  unsigned a_desc_hi;             // A descriptor bits 32..63: SBO, version, layout (no swizzle / SWIZZLE_32B)
+  int sw32, nq, qregion_bytes;    // SWIZZLE_32B A: one 32-byte-piece box per in-pixel offset
+  int qcoord[4];                  // sw32: element coordinate (in the pixel) of each region's box
+  int qbyte[4];                   // sw32: the same offset in bytes
   int nt_bbytes[kMaxNTiles];
   long long nt_bsrc[kMaxNTiles];  // device address of the N-tile's packed B
   long long row_bytes;            // bytes of one folded output row = r*Cout*out_elem
@@ -166,6 +170,7 @@ struct RowProd {
   long long in_img_bytes, total_px;
   int rb, pix, prod, Wbox, lw, Q, Qr, c0, lbo, region_bytes, s, H, n_img, ohb, OHt, OH, OW, U, sw, pw, ph;
   int rows_per_stage, ksplit, kh_count, raw_slots, raw_slot_bytes;
+  int sw32, qregion_bytes;  // SWIZZLE_32B A layout (plan.hpp Schedule::sw32)
   uint32_t row_tab;  // shared address of the folded stage-row table: b | i << 8 | a << 16
 };
 
@@ -214,6 +219,8 @@ __device__ __forceinline__ RowProd row_prod(const ConvArgs& a, uint32_t row_tab)
   p.kh_count = opq(a.kh_count);
   p.raw_slots = a.raw_slots;
   p.raw_slot_bytes = opq(a.raw_slot_bytes);
+  p.sw32 = opq(a.sw32);
+  p.qregion_bytes = opq(a.qregion_bytes);
   p.row_tab = row_tab;
   return p;
 }
@@ -320,18 +327,30 @@ struct FoldChunks {
   int src[4], dst[4];
 };
 
-__device__ __forceinline__ FoldChunks fold_chunks(const RowProd& p, int lane) {
-  // (only meaningful for the folded layout; harmless otherwise)
+// Per-lane chunk map. Legacy layout: 16-byte core column q' of folded column
+// w'' -> region q' (the shift region q' = Q holds core column 0 of w''+1).
+// SWIZZLE_32B layout: 16-byte half h of the 32-byte K-step at in-pixel offset
+// qs[qi] -> region qi, logical byte (w'' * 32 + h * 16) of the row (the
+// row-dependent swizzle is applied per row in transpose_row).
+__device__ __forceinline__ FoldChunks fold_chunks(const RowProd& p, const ConvArgs& a, int lane) {
   FoldChunks fc;
-  const int nck = p.Qr << p.lw;
+  const int nck = p.sw32 ? (a.nq * 2) << p.lw : p.Qr << p.lw;
   fc.n = (nck <= 128) ? (nck - lane + 31) / 32 : 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int c = lane + 32 * k;
-    const int qq = c >> p.lw;
-    const int w2 = c & (p.Wbox - 1);
-    fc.src[k] = (p.c0 + w2) * p.pix + ((qq == p.Q) ? p.pix : qq * 16);
-    fc.dst[k] = qq * p.lbo + w2 * 16;
+    if (p.sw32) {
+      const int w2 = c & (p.Wbox - 1);
+      const int qh = c >> p.lw;  // qi * 2 + h
+      const int qi = qh >> 1, h = qh & 1;
+      fc.src[k] = (p.c0 + w2) * p.pix + a.qbyte[qi & 3] + h * 16;
+      fc.dst[k] = qi * p.qregion_bytes + w2 * 32 + h * 16;
+    } else {
+      const int qq = c >> p.lw;
+      const int w2 = c & (p.Wbox - 1);
+      fc.src[k] = (p.c0 + w2) * p.pix + ((qq == p.Q) ? p.pix : qq * 16);
+      fc.dst[k] = qq * p.lbo + w2 * 16;
+    }
   }
   return fc;
 }
@@ -344,7 +363,10 @@ __device__ __forceinline__ void transpose_row(const RowProd& p, const FoldChunks
   const uint4 z = make_uint4(0u, 0u, 0u, 0u);
   if (kProd == 1 && fc.n > 0) {
     const uint32_t e = ptx::ld_shared_u32(p.row_tab + 4 * r);
-    const uint32_t rbase = dst + (e & 0xFF) * p.region_bytes + ((e >> 8) & 0xFF) * p.Wbox * 16;
+    // legacy: region row i at i * Wbox * 16; sw32: logical row offset i * Wbox * 32, then
+    // the SWIZZLE_32B XOR (16-byte half ^= address bit 7) on the 1024-aligned region
+    const uint32_t rbase = dst + (e & 0xFF) * p.region_bytes + (p.sw32 ? 0u : ((e >> 8) & 0xFF) * p.Wbox * 16);
+    const uint32_t rlog = p.sw32 ? ((e >> 8) & 0xFF) * p.Wbox * 32 : 0u;
     const bool fast = sh == 0 && (pix & 15) == 0 && (rb & 15) == 0;
     uint4 v[4];
 #pragma unroll
@@ -360,8 +382,16 @@ __device__ __forceinline__ void transpose_row(const RowProd& p, const FoldChunks
       }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (k < fc.n) ptx::st_shared_v4(rbase + fc.dst[k], v[k].x, v[k].y, v[k].z, v[k].w);
+    for (int k = 0; k < 4; ++k) {
+      if (k >= fc.n) continue;
+      uint32_t o = fc.dst[k];
+      if (p.sw32) {  // region offset + swizzled in-region address
+        const uint32_t qoff = (o / p.qregion_bytes) * p.qregion_bytes;
+        const uint32_t L = rlog + (o - qoff);
+        o = qoff + (L ^ (((L >> 7) & 1u) << 4));
+      }
+      ptx::st_shared_v4(rbase + o, v[k].x, v[k].y, v[k].z, v[k].w);
+    }
   } else if (kProd == 1) {
     // regions q' of residue b, region row i: chunk (q', w'') = folded pixel
     // c0 + w'' (+1 for the shift region q' = Q), core column q' % Q
@@ -521,7 +551,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // the slot ring; warps 10..12: transpose staged rows into the A stages.
     const uint32_t ring = base + a.off_raw;
     const RowProd rp = row_prod(a, base + 768);
-    const FoldChunks fc = fold_chunks(rp, lane);
+    const FoldChunks fc = fold_chunks(rp, a, lane);
     if (warp == 0) {
       if (elect_one()) {
         const uint8_t* gb = reinterpret_cast<const uint8_t*>(a.nt_bsrc[ntile]);
@@ -636,6 +666,19 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
               txs += a.box_bytes + (dbg_noshift ? 0 : a.shift_box_bytes);
         }
         if (rank == 0) mbar_arrive_expect_tx(bar_full + 8 * stage, txs * kPair);
+        if (a.sw32) {  // one SWIZZLE_32B box of 32-byte K-step pieces per (residue, in-pixel offset)
+          for (int b = 0; b < a.s; ++b) {
+            if (!((a.res_mask >> b) & 1u)) continue;
+            for (int qi = 0; qi < a.nq; ++qi) {
+              const uint32_t dq = dst + b * a.region_bytes + qi * a.qregion_bytes;
+              if constexpr (kPair == 2)
+                tma_load_4d_pair(dq, &maps.in[b], a.qcoord[qi], a.c0, oh0 + a.amin[b], n, fbar);
+              else
+                tma_load_4d(dq, &maps.in[b], a.qcoord[qi], a.c0, oh0 + a.amin[b], n, fbar);
+            }
+          }
+          continue;
+        }
         for (int b = 0; b < a.s; ++b) {
           if (!((a.res_mask >> b) & 1u)) continue;
           if (dbg_oneres && b != __ffs(a.res_mask) - 1) continue;
@@ -660,6 +703,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // uniform registers straight from the constant bank; one lane issues.
     const bool skip_mma = (a.epi_flags & 0x100) != 0;  // profiling switch
     const uint32_t b_lo = (base + a.off_b) >> 4;
+    const uint32_t a_hi = a.a_desc_hi;
     const bool leader = elect_one() && rank == 0;  // pair: the leader CTA issues for both SMs
     if (kPair == 2 && rank != 0) goto mma_done;
     mbar_wait(bar_b, 0);
@@ -693,7 +737,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
           if (split > 0) {  // lower half first, then wait for the epilogue to drain the upper half
             for (; i < split; ++i) {
               const uint4 e = a.table[e0 + i];
-              const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
+              const uint64_t adesc = (static_cast<uint64_t>(a_hi) << 32) | (e.x + a_lo);
               const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
               if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
             }
@@ -706,14 +750,14 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const uint4 e = a.table[e0 + i + j];
-              const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
+              const uint64_t adesc = (static_cast<uint64_t>(a_hi) << 32) | (e.x + a_lo);
               const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
               if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
             }
           }
           for (; i < entries; ++i) {
             const uint4 e = a.table[e0 + i];
-            const uint64_t adesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.x + a_lo);
+            const uint64_t adesc = (static_cast<uint64_t>(a_hi) << 32) | (e.x + a_lo);
             const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
             if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
           }

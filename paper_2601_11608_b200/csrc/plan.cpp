@@ -297,8 +297,27 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
     for (int64_t st : U[g])
       if (st % Q == Q - 1) S.need_shift = true;
   S.units = U;
-  S.lbo_a = static_cast<int>(NR * Wbox * 16);
-  S.region_bytes = static_cast<int>((((Q + (S.need_shift ? 1 : 0)) * S.lbo_a) + 127) / 128 * 128);
+  // A layout. Without straddling K-steps (and 2-byte inputs), every K-step is
+  // 32 contiguous bytes inside one folded pixel: the A tile is kept as one
+  // SWIZZLE_32B region per in-pixel offset q used ([row][folded col][32 B],
+  // one 32-byte TMA piece per K-step; row-shifted views verified in
+  // tools/probes/sw32_probe.cu). Otherwise the canonical no-swizzle layout of
+  // 16-byte core columns ([q][row][folded col][16 B], + the shift region).
+  S.sw32 = !S.need_shift && Q >= 2 && in_dtype != WF_TF32;
+  if (S.sw32) {
+    S.qs.clear();
+    for (int64_t g = 0; g < G; ++g)
+      for (int64_t st : U[g])
+        if (std::find(S.qs.begin(), S.qs.end(), static_cast<int>(st % Q)) == S.qs.end())
+          S.qs.push_back(static_cast<int>(st % Q));
+    std::sort(S.qs.begin(), S.qs.end());
+    S.lbo_a = 16;  // unused by SWIZZLE_32B K-major descriptors
+    S.qregion_bytes = static_cast<int>((NR * Wbox * 32 + 1023) / 1024 * 1024);
+    S.region_bytes = static_cast<int>(S.qs.size()) * S.qregion_bytes;
+  } else {
+    S.lbo_a = static_cast<int>(NR * Wbox * 16);
+    S.region_bytes = static_cast<int>((((Q + (S.need_shift ? 1 : 0)) * S.lbo_a) + 127) / 128 * 128);
+  }
   S.stage_bytes = static_cast<int>(sh) * S.region_bytes;
   const int64_t block_bytes = static_cast<int64_t>(S.Ng) * 32;  // 2 core cols x Ng rows x 16 B
   auto group_b_bytes = [&](int64_t g) { return d.kh * n_units(g) * block_bytes; };
@@ -461,7 +480,12 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
         const int64_t u = rn.u;  // first core column of the pair
         const int64_t kp = u / Q, q = u % Q;
         MmaEntry e{};
-        e.a_off = static_cast<uint32_t>(b * S.region_bytes + ((a - S.amin[b]) * Wbox + kp) * 16 + q * S.lbo_a);
+        if (S.sw32) {
+          const int qi = static_cast<int>(std::find(S.qs.begin(), S.qs.end(), static_cast<int>(q)) - S.qs.begin());
+          e.a_off = static_cast<uint32_t>(b * S.region_bytes + qi * S.qregion_bytes + ((a - S.amin[b]) * Wbox + kp) * 32);
+        } else {
+          e.a_off = static_cast<uint32_t>(b * S.region_bytes + ((a - S.amin[b]) * Wbox + kp) * 16 + q * S.lbo_a);
+        }
         e.b_off = boff;
         const int64_t n = static_cast<int64_t>(rn.len) * S.Ng;
         boff += static_cast<uint32_t>(n * 32);

@@ -91,6 +91,9 @@ struct Schedule {
   int E = 16;                    // elements per 32-byte unit
   int Q = 2;                     // 16-byte core columns per folded pixel
   bool need_shift = false;       // some unit pairs (Q-1, next pixel's 0)
+  bool sw32 = false;             // A tile as SWIZZLE_32B regions of 32-byte K-steps
+  std::vector<int> qs;           // sw32: in-pixel core-column offsets with a region each
+  int qregion_bytes = 0;         // sw32: bytes of one such region (1024-aligned)
   int Ng = 64;                   // accumulator columns per group
   int CH = 64;                   // epilogue chunk (columns per 16x256b TMEM read)
   int prod = 0;                  // A producer: 0 TMA boxes, 1 row gather (folded), 2 row gather
