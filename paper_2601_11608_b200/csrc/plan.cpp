@@ -285,7 +285,11 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
           while (k < ng && ++idx[k] == cand[k].size()) idx[k++] = 0;
           if (k == ng) break;
         }
-        if (best <= legacy_cost)
+        // accept up to `slack` percent more MMA cost: dropping the shift region
+        // saves TMA pieces and A-operand reads the MMA cost model does not see
+        int64_t slack = 0;
+        if (const char* env = std::getenv("WF_COVER_SLACK")) slack = std::atoll(env);
+        if (best * 100 <= legacy_cost * (100 + slack))
           for (int64_t k = 0; k < ng; ++k) U[g0 + k] = best_us[k];
       }
       g0 = g1;
