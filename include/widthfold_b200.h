@@ -119,7 +119,8 @@ typedef struct {
                               3 re-pitch x into the workspace, then TMA boxes */
   int32_t cta_pair;        /* 2: the conv runs on CTA pairs (cta_group::2, M = 256
                               per MMA), each SM holding half of every B block */
-  int32_t reserved0;
+  int32_t stage_tiles;     /* M tiles fed by one A stage: 2 when two consecutive
+                              output-row bands share their input-row halo */
   int64_t pitched_w;       /* producer 3: workspace row width (>= W, % f == 0) */
   int64_t workspace_bytes; /* device scratch wf_conv_fold_fwd_ws needs (0: none) */
   uint64_t useful_macs;    /* count_macs of the original conv */

@@ -51,7 +51,7 @@ class FoldPlan(ctypes.Structure):
         ("units_per_px", c_int64), ("group_size", c_int64), ("n_groups", c_int64),
         ("n_tiles", c_int64), ("tile_rows", c_int64), ("wbox", c_int64), ("nrows", c_int64),
         ("mma_entries", c_int64), ("table_bytes", c_int64), ("packed_bytes", c_int64), ("epi_chunk", c_int64), ("variant", c_int32), ("producer", c_int32), ("cta_pair", c_int32),
-        ("reserved0", c_int32),
+        ("stage_tiles", c_int32),
         ("pitched_w", c_int64), ("workspace_bytes", c_int64),
         ("useful_macs", c_uint64), ("issued_macs", c_uint64),
     ]

@@ -149,8 +149,15 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   }
   a.ctas_per_ntile = std::max(1, std::min<int>(num_sms / a.n_tiles, a.num_mtiles));
   if (S.pair == 2) a.ctas_per_ntile = std::max(2, a.ctas_per_ntile & ~1);  // whole CTA pairs
-  a.num_units = static_cast<int>((a.num_mtiles + S.pair - 1) / S.pair);
+  a.tps = S.tps;
+  a.uph = static_cast<int>((S.ohb + S.tps - 1) / S.tps);
+  a.tile_shift = S.tile_shift;
+  a.num_units = (S.tps == 2) ? static_cast<int>(d.n) * a.uph : static_cast<int>((a.num_mtiles + S.pair - 1) / S.pair);
   a.unit_stride = a.ctas_per_ntile / S.pair;
+  if (S.tps == 2 && S.pair != 1) {
+    *err = "two-tile stages run single-CTA";
+    return WF_UNSUPPORTED;
+  }
   a.row_bytes = p.cout_f * oes;
   a.acc_stride = pow2ceil(max_cols);
   a.tmem_cols = 2 * a.acc_stride;
@@ -182,7 +189,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   while ((1 << a.log_wbox) < a.Wbox) ++a.log_wbox;
   for (int b = 0; b < S.s && prod == 1; ++b) {  // folded raw rows of one stage (row producer)
     if (!S.has_res[b]) continue;
-    const int rows = S.amax[b] - S.amin[b] + static_cast<int>(p.tile_rows);
+    const int rows = S.amax[b] - S.amin[b] + static_cast<int>(p.tile_rows) * S.tps;
     for (int i = 0; i < rows; ++i) {
       if (a.rows_per_stage >= kMaxStageRows) {
         *err = "too many raw rows per stage for the row producer";

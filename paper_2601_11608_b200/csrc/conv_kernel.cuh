@@ -56,6 +56,7 @@ struct ConvArgs {
   int nt_split[kMaxNTiles];       // lower-half MMAs of the N-tile (-1: no accumulator half-split)
   int num_units, unit_stride;     // M-tile units (pairs of M tiles in cta_group::2 mode) and the CTA stride
   unsigned a_desc_hi;             // A descriptor bits 32..63: SBO, version, layout (no swizzle / SWIZZLE_32B)
+  int tps, uph, tile_shift;       // M tiles per A stage, stage units per image (tps 2), A bytes between tiles
   int sw32, nq, qregion_bytes;    // SWIZZLE_32B A: one 32-byte-piece box per in-pixel offset
   int qcoord[4];                  // sw32: element coordinate (in the pixel) of each region's box
   int qbyte[4];                   // sw32: the same offset in bytes
@@ -225,6 +226,19 @@ __device__ __forceinline__ RowProd row_prod(const ConvArgs& a, uint32_t row_tab)
   return p;
 }
 
+// Image and first output row of M tile k of stage unit u (this CTA's tile in pair mode).
+template <int kPair>
+__device__ __forceinline__ void tile_origin(const ConvArgs& a, int u, int k, uint32_t rank, int& n, int& oh0) {
+  if (a.tps == 2) {
+    n = u / a.uph;
+    oh0 = ((u - n * a.uph) * 2 + k) * a.OHt;
+  } else {
+    const int mt = u * kPair + static_cast<int>(rank);
+    n = mt / a.ohb;
+    oh0 = (mt - n * a.ohb) * a.OHt;
+  }
+}
+
 // Raw rows of one A stage, enumerated identically by the loader and the
 // transposers. Folded: row r = (residue b, region row i), input row
 // (oh0 + a) * s + b with a = amin[b] + i. im2col: row r = (output row t of the
@@ -239,9 +253,8 @@ struct StageRows {
 template <int kProd>
 __device__ __forceinline__ StageRows stage_rows(const ConvArgs& a, const RowProd& p, int mt, int ks) {
   StageRows sr;
-  if constexpr (kProd == 1) {
-    sr.n0 = mt / p.ohb;
-    sr.oh0 = (mt - sr.n0 * p.ohb) * p.OHt;
+  if constexpr (kProd == 1) {  // `mt` is the stage unit here (tps M tiles from tile_origin)
+    tile_origin<1>(a, mt, 0, 0u, sr.n0, sr.oh0);
     sr.count = p.rows_per_stage;
     sr.g0 = 0;
     sr.kh0 = 0;
@@ -561,7 +574,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
           bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
         int slot_it = 0;
         const bool no_loads = (a.epi_flags & 0x1000) != 0;
-        for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile)
+        for (int mt = local; mt < a.num_units; mt += a.unit_stride)  // stage units (= M tiles unless tps 2)
           for (int ks = 0; ks < rp.ksplit; ++ks) {
             const StageRows sr = stage_rows<kProd>(a, rp, mt, ks);
             for (int r = 0; r < sr.count; ++r) {  // every row takes a slot; padding rows carry no bytes
@@ -593,7 +606,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       const bool no_loads = (a.epi_flags & 0x1000) != 0;
       const int nstages = a.stages, stage_bytes = a.stage_bytes;
       const uint32_t a_base = base + a.off_a;
-      for (int mt = local; mt < a.num_mtiles; mt += a.ctas_per_ntile) {
+      for (int mt = local; mt < a.num_units; mt += a.unit_stride) {  // stage units
         for (int ks = 0; ks < rp.ksplit; ++ks, ++it) {
           const int stage = it % nstages;
           const uint32_t round = static_cast<uint32_t>(it / nstages);
@@ -643,14 +656,13 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       const uint32_t tx = static_cast<uint32_t>((a.box_bytes + a.shift_box_bytes) * __popc(a.res_mask));
       int it = 0;
       for (int u = local; u < a.num_units; u += a.unit_stride, ++it) {
-        const int mt = u * kPair + static_cast<int>(rank);
         const int stage = it % a.stages;
         const uint32_t round = static_cast<uint32_t>(it / a.stages);
         mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
         // pair: both CTAs' boxes complete on the leader's full barrier
         const uint32_t fbar = (kPair == 2) ? mapa(bar_full + 8 * stage, 0) : bar_full + 8 * stage;
-        const int n = mt / a.ohb;
-        const int oh0 = (mt - n * a.ohb) * a.OHt;
+        int n, oh0;
+        tile_origin<kPair>(a, u, 0, rank, n, oh0);  // the stage covers tiles 0..tps-1 from here
         const uint32_t dst = base + a.off_a + stage * a.stage_bytes;
         if (a.epi_flags & 0x1000) {  // profiling: no A loads (stage contents stale)
           if (rank == 0) mbar_arrive(bar_full + 8 * stage);
@@ -712,9 +724,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // profiling (0x80000, CTA 0): cycles the issuer waits on the accumulator / the A stage
     const bool dbg = (a.epi_flags & 0x80000) && blockIdx.x == 0;
     long long w_acc = 0, w_full = 0, w_hi = 0, t_all = dbg ? clock64() : 0;
-    int it = 0;  // A stages consumed (ksplit per M tile)
+    int it0 = 0;  // first A stage of the unit (ksplit sub-stages per unit)
     int tile = 0;
-    for (int u = local; u < a.num_units; u += a.unit_stride, ++tile) {
+    for (int u = local; u < a.num_units; u += a.unit_stride, it0 += a.ksplit) {
+     for (int k = 0; k < a.tps; ++k, ++tile) {  // tps M tiles share the unit's A stage
       const int acc = tile & 1;
       const uint32_t acc_round = static_cast<uint32_t>(tile >> 1);
       const int split = (a.ksplit == 1) ? a.nt_split[ntile] : -1;
@@ -723,15 +736,16 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       if (split < 0) mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
       if (dbg) { const long long t1 = clock64(); w_acc += t1 - t0; t0 = t1; }
       const uint32_t d_base = tmem_base + acc * a.acc_stride;
-      for (int ks = 0; ks < a.ksplit; ++ks, ++it) {
+      for (int ks = 0; ks < a.ksplit; ++ks) {
+        const int it = it0 + ks;
         const int stage = it % a.stages;
         const uint32_t round = static_cast<uint32_t>(it / a.stages);
         const int e0 = (a.ksplit == 1) ? a.nt_entry0[ntile] : a.ks_entry0[ks];
         const int entries = (a.ksplit == 1) ? a.nt_entries[ntile] : a.ks_entries[ks];
-        mbar_wait(bar_full + 8 * stage, round & 1u);
+        if (k == 0) mbar_wait(bar_full + 8 * stage, round & 1u);
         if (dbg) { const long long t1 = clock64(); w_full += t1 - t0; t0 = t1; }
         tc_fence_after();
-        const uint32_t a_lo = (base + a.off_a + stage * a.stage_bytes) >> 4;
+        const uint32_t a_lo = (base + a.off_a + stage * a.stage_bytes + k * a.tile_shift) >> 4;
         if (!skip_mma) {
           int i = 0;
           if (split > 0) {  // lower half first, then wait for the epilogue to drain the upper half
@@ -765,10 +779,11 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         else if (split > 0) {
           mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
         }
-        if (leader) commit_to<kPair>(bar_empty + 8 * stage);
+        if (leader && k == a.tps - 1) commit_to<kPair>(bar_empty + 8 * stage);  // last tile frees the stage
       }
       if (leader) commit_to<kPair>(bar_tfull + 8 * acc);
       __syncwarp();
+     }
     }
     if (dbg && leader)
       printf("mma issuer cta0: %d tiles, %lld cycles: wait accumulator %lld (upper half %lld), wait A stage %lld\n",
@@ -828,12 +843,14 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // pair: arrivals go to the leader's accumulator-free barriers
     const uint32_t te_lo = (kPair == 2) ? mapa(bar_tempty, 0) : bar_tempty;
     const uint32_t te_hi = (kPair == 2) ? mapa(bar_tempty_hi, 0) : bar_tempty_hi;
-    for (int u = local; u < a.num_units; u += a.unit_stride, ++it_tile) {
-      const int mt = u * kPair + static_cast<int>(rank);
+    for (int ut = local * a.tps; ut < a.num_units * a.tps; ++it_tile) {
+      const int u = ut / a.tps, k = ut - u * a.tps;  // tile k of stage unit u
+      ut = (k + 1 < a.tps) ? ut + 1 : (u + a.unit_stride) * a.tps;
       const int acc = it_tile & 1;
       const uint32_t acc_round = static_cast<uint32_t>(it_tile >> 1);
-      const int n = mt / a.ohb;
-      const int oh0 = (mt - n * a.ohb) * a.OHt;
+      const int mt = u * kPair + static_cast<int>(rank);  // (im2col rows; tps == 1 there)
+      int n, oh0;
+      tile_origin<kPair>(a, u, k, rank, n, oh0);
       mbar_wait(bar_tfull + 8 * acc, acc_round & 1u);
       tc_fence_after();
       if (dbg_skip_epi || n_it == 0) {

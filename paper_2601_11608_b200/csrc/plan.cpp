@@ -59,8 +59,39 @@ wf_status validate_desc(const wf_conv_desc& d, std::string* err) {
   return WF_OK;
 }
 
-wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
-                        wf_dtype in_dtype, Schedule* out, std::string* err) {
+namespace {
+wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, int tps,
+                            Schedule* out, std::string* err);
+}  // namespace
+
+// Two M tiles per A stage (their input-row halo loaded once) when it fits as
+// well as one tile per stage does and the batch is large; WF_TPS=1 forces one.
+wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, Schedule* out,
+                        std::string* err) {
+  Schedule s1;
+  wf_status st = make_schedule_tps(d, f_req, gs_req, in_dtype, 1, &s1, err);
+  if (st != WF_OK || s1.plan.status != WF_FOLD_APPLY || f_req == 0) {
+    *out = std::move(s1);
+    return st;
+  }
+  const char* env = std::getenv("WF_TPS");
+  if (!(env && env[0] == '1') && (s1.prod == 0 || s1.prod == 3) && s1.pair == 1 && s1.ohb >= 2 &&
+      d.n * s1.ohb >= 8 * 148) {  // keep >= 4 stage units per B200 SM: small batches keep the parallelism
+    Schedule s2;
+    std::string e2;
+    if (make_schedule_tps(d, f_req, gs_req, in_dtype, 2, &s2, &e2) == WF_OK && s2.plan.status == WF_FOLD_APPLY &&
+        s2.stages >= 2 && s2.ntiles.size() == s1.ntiles.size()) {
+      *out = std::move(s2);
+      return WF_OK;
+    }
+  }
+  *out = std::move(s1);
+  return WF_OK;
+}
+
+namespace {
+wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, int tps,
+                            Schedule* out, std::string* err) {
   wf_status st = validate_desc(d, err);
   if (st != WF_OK) return st;
   if (in_dtype != WF_BF16 && in_dtype != WF_F16 && in_dtype != WF_TF32) {
@@ -157,9 +188,10 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
     S.amin[b] = std::min(S.amin[b], a);
     S.amax[b] = std::max(S.amax[b], a);
   }
-  int64_t NR = 0;
+  S.tps = tps;
+  int64_t NR = 0;  // input rows per residue region: tps tiles of OHt output rows + the kh spread
   for (int b = 0; b < sh; ++b)
-    if (S.has_res[b]) NR = std::max<int64_t>(NR, OHt + S.amax[b] - S.amin[b]);
+    if (S.has_res[b]) NR = std::max<int64_t>(NR, tps * OHt + S.amax[b] - S.amin[b]);
   // every core-column region (and the shifted one) must start 128-byte aligned
   // for the TMA destination: pad rows so NR*Wbox*16 % 128 == 0
   while ((NR * Wbox) % 8 != 0) ++NR;
@@ -323,6 +355,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
     S.region_bytes = static_cast<int>((((Q + (S.need_shift ? 1 : 0)) * S.lbo_a) + 127) / 128 * 128);
   }
   S.stage_bytes = static_cast<int>(sh) * S.region_bytes;
+  S.tile_shift = static_cast<int>(OHt * Wbox * (S.sw32 ? 32 : 16));  // A bytes between the stage's tiles
   const int64_t block_bytes = static_cast<int64_t>(S.Ng) * 32;  // 2 core cols x Ng rows x 16 B
   auto group_b_bytes = [&](int64_t g) { return d.kh * n_units(g) * block_bytes; };
 
@@ -586,7 +619,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   {
     const char* env = std::getenv("WF_CTA_PAIR");
     bool pair = env != nullptr && env[0] == '1';
-    pair = pair && in_dtype != WF_TF32 && (S.prod == 0 || S.prod == 3) && S.num_mtiles >= 2;
+    pair = pair && in_dtype != WF_TF32 && (S.prod == 0 || S.prod == 3) && S.num_mtiles >= 2 && S.tps == 1;
     for (const MmaEntry& e : S.entries) pair = pair && (((e.meta >> 22) & 0x1FFu) * 8) % 16 == 0;
     if (pair) {
       int64_t max_b = 0;
@@ -598,6 +631,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
         if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { S.stages = st2; break; }
     }
     p.cta_pair = S.pair;
+    p.stage_tiles = S.tps;
   }
   p.useful_macs = static_cast<uint64_t>(d.n) * OH * OW * d.cout * d.kh * d.kw * d.c;
   uint64_t issued_per_tile = 0;
@@ -606,6 +640,8 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req,
   *out = std::move(S);
   return WF_OK;
 }
+
+}  // namespace
 
 wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Schedule* out, std::string* err) {
   wf_status st = validate_desc(d, err);
@@ -724,6 +760,7 @@ wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Sched
   p.variant = WF_VARIANT_UNFOLDED;
   p.producer = 2;
   p.cta_pair = 1;
+  p.stage_tiles = 1;
   const int64_t total = d.n * OH * OW;
   S.num_mtiles = ceil_div(total, kTileM);
   S.ohb = 1;

@@ -100,6 +100,8 @@ struct Schedule {
                                  // (im2col), 3 re-pitch into the workspace + TMA boxes
   int64_t Wp = 0;                // input width the TMA view uses (re-pitched when != W)
   int pair = 1;                  // 2: CTA-pair (cta_group::2) MMAs, B blocks split across the pair
+  int tps = 1;                   // M tiles per A stage (2: consecutive tiles share their input rows)
+  int tile_shift = 0;            // bytes of A between the stage's tiles
   int U = 0;                     // im2col: 32-byte K-steps per kh
   int ksplit = 1;                // A stages per M tile (im2col: kh ranges)
   int raw_slots = 0, raw_slot_bytes = 0;  // staged-row ring of the row producer (prod 1/2)
