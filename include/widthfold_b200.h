@@ -121,6 +121,9 @@ typedef struct {
                               per MMA), each SM holding half of every B block */
   int32_t stage_tiles;     /* M tiles fed by one A stage: 2 when two consecutive
                               output-row bands share their input-row halo */
+  int32_t kstep_mode;      /* MMA K-steps: 0 32-byte covers of each kh row's
+                              window, 1 cross-kh pairs of 16-byte core columns */
+  int32_t reserved0;
   int64_t pitched_w;       /* producer 3: workspace row width (>= W, % f == 0) */
   int64_t workspace_bytes; /* device scratch wf_conv_fold_fwd_ws needs (0: none) */
   uint64_t useful_macs;    /* count_macs of the original conv */
@@ -192,6 +195,15 @@ wf_status wf_replicate_bias(const float* b, int64_t cout, int64_t r, float* out,
  * Synchronizes `stream`. Returns WF_NOT_BLOCK_DIAGONAL when one is found. */
 wf_status wf_check_block_diagonal(const float* w_dense, int64_t kh, int64_t kw, int64_t cif, int64_t cof,
                                   int64_t groups, void* scratch, int64_t* first_bad, void* stream);
+
+/* Diagnostic: the tcgen05 schedule make_schedule builds for (desc, f,
+ * group_size, in_dtype) as one JSON object (A-stage layout, per-MMA
+ * descriptor offsets, per-core-column (kh, c, slot mask) words, slot order) in
+ * buf (cap bytes, NUL-terminated). Lets a host-side simulator replay the MMAs
+ * against the oracle without a GPU. Host-only. WF_INVALID_ARGUMENT if cap is
+ * too small or the plan falls back. No reference counterpart. */
+wf_status wf_schedule_describe(const wf_conv_desc* desc, int64_t f, int64_t group_size, wf_dtype in_dtype,
+                               char* buf, size_t cap);
 
 /* Number of SMs the conv kernel assumes (persistent grid); 0 = device value. */
 void wf_set_num_sms(int num_sms);

@@ -33,6 +33,7 @@ REASONS = [
 EXPORTED = [
     "wf_plan_fold", "wf_plan_unfolded", "wf_packed_filter_bytes", "wf_expand_filter_pack", "wf_expand_filter_dense",
     "wf_conv_fold_fwd", "wf_conv_fold_fwd_ws", "wf_set_num_sms", "wf_last_error", "wf_abi_version",
+    "wf_schedule_describe",
 ]
 
 
@@ -51,7 +52,7 @@ class FoldPlan(ctypes.Structure):
         ("units_per_px", c_int64), ("group_size", c_int64), ("n_groups", c_int64),
         ("n_tiles", c_int64), ("tile_rows", c_int64), ("wbox", c_int64), ("nrows", c_int64),
         ("mma_entries", c_int64), ("table_bytes", c_int64), ("packed_bytes", c_int64), ("epi_chunk", c_int64), ("variant", c_int32), ("producer", c_int32), ("cta_pair", c_int32),
-        ("stage_tiles", c_int32),
+        ("stage_tiles", c_int32), ("kstep_mode", c_int32), ("reserved0", c_int32),
         ("pitched_w", c_int64), ("workspace_bytes", c_int64),
         ("useful_macs", c_uint64), ("issued_macs", c_uint64),
     ]
@@ -104,6 +105,8 @@ def lib() -> ctypes.CDLL:
         L.wf_last_error.restype = c_char_p
         L.wf_abi_version.argtypes = []
         L.wf_abi_version.restype = c_int
+        L.wf_schedule_describe.argtypes = [POINTER(ConvDesc), c_int64, c_int64, c_int, ctypes.c_char_p, c_size_t]
+        L.wf_schedule_describe.restype = c_int
         _lib = L
     return _lib
 
@@ -128,3 +131,11 @@ def plan_fold(desc: ConvDesc, f: int = 0, group_size: int = 0, in_dtype: int = W
     p = FoldPlan()
     check(lib().wf_plan_fold(byref(desc), f, group_size, in_dtype, byref(p)))
     return p
+
+
+def schedule_describe(desc: ConvDesc, f: int = 0, group_size: int = 0, in_dtype: int = WF_BF16) -> dict:
+    """The tcgen05 schedule of a plan (diagnostic; tests replay it on the CPU)."""
+    import json
+    buf = ctypes.create_string_buffer(1 << 20)
+    check(lib().wf_schedule_describe(byref(desc), f, group_size, in_dtype, buf, len(buf)))
+    return json.loads(buf.value.decode())

@@ -66,7 +66,7 @@ wf_status fail(wf_status st, const std::string& msg) {
 
 extern "C" {
 
-int wf_abi_version(void) { return 5; }
+int wf_abi_version(void) { return 6; }
 
 const char* wf_last_error(void) { return g_last_error.c_str(); }
 
@@ -90,6 +90,48 @@ wf_status wf_plan_unfolded(const wf_conv_desc* desc, wf_dtype in_dtype, wf_fold_
   wf_status st = wfb::make_schedule_unfolded(*desc, in_dtype, &S, &err);
   if (st != WF_OK) return fail(st, err);
   *plan = S.plan;
+  return WF_OK;
+}
+
+wf_status wf_schedule_describe(const wf_conv_desc* desc, int64_t f, int64_t group_size, wf_dtype in_dtype,
+                               char* buf, size_t cap) {
+  if (!desc || !buf) return fail(WF_INVALID_ARGUMENT, "null argument");
+  wfb::Schedule S;
+  std::string err;
+  wf_status st = wfb::make_schedule(*desc, f, group_size, in_dtype, &S, &err);
+  if (st != WF_OK) return fail(st, err);
+  if (S.plan.status != WF_FOLD_APPLY) return fail(WF_INVALID_ARGUMENT, "plan falls back: nothing to describe");
+  std::string j = "{";
+  auto kv = [&](const char* k, long long v) { j += "\"" + std::string(k) + "\": " + std::to_string(v) + ", "; };
+  auto arr = [&](const char* k, const std::vector<long long>& v) {
+    j += "\"" + std::string(k) + "\": [";
+    for (size_t i = 0; i < v.size(); ++i) j += (i ? ", " : "") + std::to_string(v[i]);
+    j += "], ";
+  };
+  kv("f", S.plan.f); kv("r", S.plan.r); kv("c0", S.plan.c0); kv("kw_f", S.plan.kw_f); kv("s", S.s);
+  kv("ph", S.ph); kv("pw", S.pw); kv("esize", S.esize); kv("Q", S.Q); kv("Ng", S.Ng); kv("CH", S.CH);
+  kv("wbox", S.plan.wbox); kv("tile_rows", S.plan.tile_rows); kv("nrows", S.plan.nrows); kv("tps", S.tps);
+  kv("tile_shift", S.tile_shift); kv("sw32", S.sw32); kv("kpair", S.kpair); kv("need_shift", S.need_shift);
+  kv("region_bytes", S.region_bytes); kv("qregion_bytes", S.qregion_bytes); kv("lbo_a", S.lbo_a);
+  kv("stage_bytes", S.stage_bytes); kv("stages", S.stages); kv("smem_bytes", S.smem_bytes);
+  std::vector<long long> v;
+  for (int b = 0; b < S.s; ++b) v.push_back(S.has_res[b] ? S.amin[b] : -999);
+  arr("amin", v);
+  arr("qs", std::vector<long long>(S.qs.begin(), S.qs.end()));
+  arr("order", std::vector<long long>(S.order.begin(), S.order.end()));
+  v.clear();
+  for (const auto& t : S.ntiles) { v.push_back(t.col0); v.push_back(t.cols); v.push_back(t.entry0); v.push_back(t.entries); v.push_back(t.g0); v.push_back(t.split); }
+  arr("ntiles", v);
+  v.clear();
+  for (size_t i = 0; i < S.entries.size(); ++i) {
+    const auto& e = S.entries[i];
+    v.push_back(e.a_off); v.push_back(S.entry_lbo[i]); v.push_back(e.b_off); v.push_back(e.meta);
+    v.push_back(e.tmem_col); v.push_back(S.entry_cc0[i]); v.push_back(S.entry_cc1[i]);
+  }
+  arr("entries", v);
+  j += "\"mma_entries\": " + std::to_string(S.entries.size()) + "}";
+  if (j.size() + 1 > cap) return fail(WF_INVALID_ARGUMENT, "buffer too small: need " + std::to_string(j.size() + 1));
+  std::memcpy(buf, j.c_str(), j.size() + 1);
   return WF_OK;
 }
 

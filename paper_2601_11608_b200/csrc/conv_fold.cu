@@ -129,7 +129,8 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     const MmaEntry& e = S.entries[i];
     const uint32_t n8 = (e.meta >> 22) & 0x1FFu;  // N / 8 of this MMA
     const uint32_t lbo_b = n8 * 8u * 16u;         // B: [core col][N rows][16 B]
-    a.table[i].x = (e.a_off >> 4) | ((static_cast<uint32_t>(S.lbo_a) >> 4) << 16);
+    const uint32_t lbo_a = S.entry_lbo.empty() ? static_cast<uint32_t>(S.lbo_a) : S.entry_lbo[i];
+    a.table[i].x = (e.a_off >> 4) | ((lbo_a >> 4) << 16);
     a.table[i].y = ((e.b_off / S.pair) >> 4) | (((lbo_b / S.pair) >> 4) << 16);
     a.table[i].z = idesc_base | (n8 << 17) | (e.meta & 0x80000000u);
     a.table[i].w = e.tmem_col;

@@ -51,7 +51,7 @@ py::dict raw_dict(const wf_fold_plan& p) {
   d["packed_bytes"] = p.packed_bytes; d["epi_chunk"] = p.epi_chunk;
   d["variant"] = p.variant == WF_VARIANT_UNFOLDED ? "unfolded" : "fold";
   d["producer"] = p.producer == 0 ? "tma" : (p.producer == 1 ? "gather" : (p.producer == 2 ? "im2col" : "repitch+tma"));
-  d["pitched_w"] = p.pitched_w; d["workspace_bytes"] = p.workspace_bytes; d["cta_pair"] = p.cta_pair; d["stage_tiles"] = p.stage_tiles; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
+  d["pitched_w"] = p.pitched_w; d["workspace_bytes"] = p.workspace_bytes; d["cta_pair"] = p.cta_pair; d["stage_tiles"] = p.stage_tiles; d["kstep_mode"] = p.kstep_mode; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
   return d;
 }
 

@@ -10,10 +10,13 @@
 //   kw = (c0 + kw')*f + fi - j*s + pw   if 0 <= kw < KW, else exactly 0,
 // and replicate_bias (src/fold.cpp:213-226) is b'[j*Cout + co] = b[co].
 //
-// Packed B layout, per schedule entry (kh, group g, unit u): a K-major,
-// no-swizzle block [core col cc in {0,1}][n row (j,co) of the group][8 elems]
-// (Ng*32 bytes), i.e. exactly the smem descriptor layout the MMA reads
-// (LBO = Ng*16, SBO = 128). Only the units a group's windows touch are stored.
+// Packed B layout, per schedule entry: a K-major, no-swizzle block
+// [core col cc in {0,1}][n row (j,co) of the run][8 elems] (N*16 bytes per
+// core column), i.e. exactly the smem descriptor layout the MMA reads
+// (LBO = N*16, SBO = 128). Core column cc of the entry is the window-row core
+// column c of filter row kh, nonzero for the accumulator slots in its mask
+// (header words, plan.hpp Schedule::entry_cc0/1). Only the core columns a
+// group's windows touch are stored.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -25,9 +28,6 @@
 
 namespace wfb {
 
-constexpr int kPackMaxGroups = 32;
-constexpr int kPackMaxUnits = 12;
-
 struct PackArgs {
   int KH, KW, C, Cout, f, s, pw, c0, gs, Ng, E, esize, CH;
   int entries;
@@ -37,11 +37,7 @@ struct PackArgs {
   long long nt_boff[kMaxNTiles];
   long long nt_bbytes[kMaxNTiles];
   int pair;  // 2: rows [0, N/2) of every block go to the first half of the N-tile's B, [N/2, N) to the second
-  // per group: its K-step starts (a K column covered by two steps of a group is
-  // kept in the lower one and zeroed in the upper one)
   int n_groups;
-  int n_units[kPackMaxGroups];
-  unsigned char units[kPackMaxGroups][kPackMaxUnits];
   long long table_bytes;
   int round_tf32;
 };
@@ -52,17 +48,17 @@ template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
 template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
 template <> __device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
 
-// One CTA per schedule entry (kh, unit u, run of accumulator slots); threads
-// walk its 2 core cols x N rows x (E/2) elements. Row nrow of the block is
-// accumulator column slot0*Ng + nrow: group order[g0 + slot], output column
-// chunk_perm(nrow % Ng) of that group.
+// One CTA per schedule entry (run of accumulator slots, two core columns);
+// threads walk its 2 core cols x N rows x (E/2) elements. Row nrow of the
+// block is accumulator column slot0*Ng + nrow: group order[g0 + slot], output
+// column chunk_perm(nrow % Ng) of that group.
 template <typename T>
 __global__ void pack_b_kernel(const T* __restrict__ w, uint8_t* __restrict__ packed, PackArgs a) {
   const int ei = blockIdx.x;
   const uint4 e = reinterpret_cast<const uint4*>(packed)[ei];
   const int* order = reinterpret_cast<const int*>(packed + 16LL * a.entries);
-  const int kh = e.z & 0xff;
-  const int u = (e.z >> 8) & 0xff;  // first core column of the pair
+  const uint32_t* ccw = reinterpret_cast<const uint32_t*>(packed + 16LL * a.entries + 4LL * a.n_groups);
+  const uint32_t cw[2] = {ccw[2 * ei], ccw[2 * ei + 1]};
   const int slot0 = (e.z >> 16) & 0x3f;
   const int N = static_cast<int>((e.z >> 22) & 0x1ffu) * 8;
   int nt = 0;
@@ -74,7 +70,8 @@ __global__ void pack_b_kernel(const T* __restrict__ w, uint8_t* __restrict__ pac
     int rem = idx - cc * N * half;
     const int nrow = rem / half;
     const int e8 = rem - nrow * half;
-    const int widx = (u + cc) * half + e8;  // element of the KW'*f*C window row
+    const int kh = static_cast<int>(cw[cc] & 0xff);
+    const int widx = static_cast<int>((cw[cc] >> 8) & 0xff) * half + e8;  // element of the KW'*f*C window row
     const int kp = widx / (a.f * a.C);
     const int r2 = widx - kp * a.f * a.C;
     const int fi = r2 / a.C;
@@ -84,12 +81,9 @@ __global__ void pack_b_kernel(const T* __restrict__ w, uint8_t* __restrict__ pac
     const int j = g * a.gs + ncol / a.Cout;
     const int co = ncol - (ncol / a.Cout) * a.Cout;
     const int kw = (a.c0 + kp) * a.f + fi - j * a.s + a.pw;
-    // core column u of this step is owned by the group's step at u-1 if it has one
-    bool dup = false;
-    if (cc == 0 && g < a.n_groups)
-      for (int k = 0; k < a.n_units[g]; ++k) dup = dup || (a.units[g][k] + 1 == u);
+    const bool member = (cw[cc] >> (16 + nrow / a.Ng)) & 1u;  // this core column feeds the row's slot
     T val = T(0.0f);
-    if (!dup && kw >= 0 && kw < a.KW) val = w[((static_cast<long long>(kh) * a.KW + kw) * a.C + c) * a.Cout + co];
+    if (member && kw >= 0 && kw < a.KW) val = w[((static_cast<long long>(kh) * a.KW + kw) * a.C + c) * a.Cout + co];
     uint8_t* dst;
     if (a.pair == 2) {  // CTA r of the pair loads [nt_boff + r * b_bytes / 2, ...): its half of every block
       const int h = nrow / (N / 2), rr = nrow - h * (N / 2);
@@ -144,6 +138,18 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
   std::vector<uint8_t> header(static_cast<size_t>(p.table_bytes), 0);
   std::memcpy(header.data(), S.entries.data(), S.entries.size() * sizeof(MmaEntry));
   std::memcpy(header.data() + S.entries.size() * sizeof(MmaEntry), S.order.data(), S.order.size() * sizeof(int));
+  if (S.entry_cc0.size() != S.entries.size() || S.entry_cc1.size() != S.entries.size()) {
+    *err = "pack: schedule has no core-column words";
+    return WF_INVALID_ARGUMENT;
+  }
+  {
+    uint32_t* ccw = reinterpret_cast<uint32_t*>(header.data() + S.entries.size() * sizeof(MmaEntry) +
+                                                S.order.size() * sizeof(int));
+    for (size_t i = 0; i < S.entries.size(); ++i) {
+      ccw[2 * i] = S.entry_cc0[i];
+      ccw[2 * i + 1] = S.entry_cc1[i];
+    }
+  }
   cudaError_t e = cudaMemsetAsync(packed, 0, static_cast<size_t>(p.packed_bytes), st);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(packed, header.data(), header.size(), cudaMemcpyHostToDevice, st);
@@ -166,19 +172,7 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
   a.esize = S.esize;
   a.CH = S.CH;
   a.pair = S.pair;
-  a.n_groups = static_cast<int>(std::min<size_t>(S.units.size(), kPackMaxGroups));
-  for (int g = 0; g < a.n_groups; ++g) {
-    if (S.units[g].size() > static_cast<size_t>(kPackMaxUnits)) {
-      *err = "pack: too many K-steps per group";
-      return WF_UNSUPPORTED;
-    }
-    a.n_units[g] = static_cast<int>(S.units[g].size());
-    for (size_t k = 0; k < S.units[g].size(); ++k) a.units[g][k] = static_cast<unsigned char>(S.units[g][k]);
-  }
-  if (S.units.size() > static_cast<size_t>(kPackMaxGroups)) {
-    *err = "pack: too many output groups";
-    return WF_UNSUPPORTED;
-  }
+  a.n_groups = static_cast<int>(S.order.size());
   a.entries = static_cast<int>(S.entries.size());
   a.n_tiles = static_cast<int>(S.ntiles.size());
   for (int i = 0; i < a.n_tiles; ++i) {

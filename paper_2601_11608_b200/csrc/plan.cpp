@@ -61,15 +61,153 @@ wf_status validate_desc(const wf_conv_desc& d, std::string* err) {
 
 namespace {
 wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, int tps,
-                            Schedule* out, std::string* err);
+                            Schedule* out, std::string* err, int kpair_req = -1);
+
+int64_t mma_cost(int64_t n) { return std::max<int64_t>(n / 2, 32 + n / 4); }
+
+// One kpair MMA: accumulator slots [slot0, slot0 + len) of the N-tile; core
+// column k in {0, 1} is (kh[k], c[k]) and feeds the slots in mask[k] (bit i =
+// slot slot0 + i; the other rows of its B half-block are zero).
+struct PMma {
+  int slot0, len;
+  int kh[2], c[2];
+  uint32_t mask[2];
+};
+
+// kpair MMAs of one N-tile. ord[slot] = group; group g's window covers core
+// columns [lo[g], hi[g]] of every kh row. Items (kh, c) with the same
+// accumulator run pair up among themselves ((c, kh) order: mostly (kh, c) with
+// (kh+1, c)); the odd ones out are matched by a min-cost DP over their runs'
+// hulls, a last single one pairs with a zero (mask 0) neighbour column.
+std::vector<PMma> build_kpair(const std::vector<int>& ord, const std::vector<int64_t>& lo,
+                              const std::vector<int64_t>& hi, int KH, int Ng) {
+  const int ns = static_cast<int>(ord.size());
+  int64_t cmin = INT64_MAX, cmax = -1;
+  for (int g : ord) { cmin = std::min(cmin, lo[g]); cmax = std::max(cmax, hi[g]); }
+  struct Run { int s0, len; };
+  std::vector<std::pair<Run, std::vector<std::pair<int, int>>>> groups;  // run -> items (kh, c)
+  for (int64_t c = cmin; c <= cmax; ++c) {
+    for (int s = 0; s < ns;) {
+      if (!(lo[ord[s]] <= c && c <= hi[ord[s]])) { ++s; continue; }
+      int e = s;
+      while (e < ns && lo[ord[e]] <= c && c <= hi[ord[e]]) ++e;
+      size_t k = 0;
+      while (k < groups.size() && !(groups[k].first.s0 == s && groups[k].first.len == e - s)) ++k;
+      if (k == groups.size()) groups.push_back({Run{s, e - s}, {}});
+      for (int kh = 0; kh < KH; ++kh) groups[k].second.push_back({kh, static_cast<int>(c)});
+      s = e;
+    }
+  }
+  std::vector<PMma> out;
+  struct Left { Run run; int kh, c; };
+  std::vector<Left> left;
+  for (auto& gr : groups) {
+    auto& it = gr.second;
+    std::sort(it.begin(), it.end(), [](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+      return x.second != y.second ? x.second < y.second : x.first < y.first;
+    });
+    const uint32_t full = (1u << gr.first.len) - 1u;
+    size_t i = 0;
+    for (; i + 1 < it.size(); i += 2)
+      out.push_back({gr.first.s0, gr.first.len, {it[i].first, it[i + 1].first}, {it[i].second, it[i + 1].second},
+                     {full, full}});
+    if (i < it.size()) left.push_back({gr.first, it[i].first, it[i].second});
+  }
+  // leftovers: min-cost matching (hull of the two runs) by DP over subsets
+  const int L = static_cast<int>(left.size());
+  auto hull_cost = [&](int i, int j) {
+    const int a0 = std::min(left[i].run.s0, left[j].run.s0);
+    const int a1 = std::max(left[i].run.s0 + left[i].run.len, left[j].run.s0 + left[j].run.len);
+    return mma_cost(static_cast<int64_t>(a1 - a0) * Ng);
+  };
+  std::vector<std::pair<int, int>> match;  // (i, j), j == -1: paired with a zero column
+  if (L <= 16) {
+    std::vector<int64_t> best(static_cast<size_t>(1) << L, INT64_MAX);
+    std::vector<int> pick(static_cast<size_t>(1) << L, -2);
+    best[0] = 0;
+    for (uint32_t m = 1; m < (1u << L); ++m) {
+      const int i = __builtin_ctz(m);
+      const uint32_t r = m & ~(1u << i);
+      if (best[r] != INT64_MAX) {
+        const int64_t c = best[r] + mma_cost(static_cast<int64_t>(left[i].run.len) * Ng);
+        if (c < best[m]) { best[m] = c; pick[m] = -1; }
+      }
+      for (int j = i + 1; j < L; ++j) {
+        if (!((r >> j) & 1u) || best[r & ~(1u << j)] == INT64_MAX) continue;
+        const int64_t c = best[r & ~(1u << j)] + hull_cost(i, j);
+        if (c < best[m]) { best[m] = c; pick[m] = j; }
+      }
+    }
+    for (uint32_t m = (1u << L) - 1u; m;) {
+      const int i = __builtin_ctz(m);
+      const int j = pick[m];
+      match.push_back({i, j});
+      m &= ~(1u << i);
+      if (j >= 0) m &= ~(1u << j);
+    }
+  } else {
+    int i = 0;
+    for (; i + 1 < L; i += 2) match.push_back({i, i + 1});
+    if (i < L) match.push_back({i, -1});
+  }
+  for (const auto& pr : match) {
+    const Left& x = left[pr.first];
+    if (pr.second < 0) {  // partner: a neighbouring core column of the same row (finite data), B zero
+      const int c2 = x.c > 0 ? x.c - 1 : x.c + 1;
+      out.push_back({x.run.s0, x.run.len, {x.kh, x.kh}, {x.c, c2}, {(1u << x.run.len) - 1u, 0u}});
+      continue;
+    }
+    const Left& y = left[pr.second];
+    const int s0 = std::min(x.run.s0, y.run.s0);
+    const int s1 = std::max(x.run.s0 + x.run.len, y.run.s0 + y.run.len);
+    out.push_back({s0, s1 - s0, {x.kh, y.kh}, {x.c, y.c},
+                   {((1u << x.run.len) - 1u) << (x.run.s0 - s0), ((1u << y.run.len) - 1u) << (y.run.s0 - s0)}});
+  }
+  return out;
+}
+
+// Order runs (slot0, len) so each one meets only untouched accumulator slots
+// (its MMA zero-initialises them) or only touched ones. Backtracking, widest
+// first; false when no such order exists.
+bool zero_init_order(const std::vector<std::pair<int, int>>& runs, int nslots, std::vector<int>* seq_out) {
+  std::vector<int> idx(runs.size());
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return runs[x].second > runs[y].second; });
+  std::vector<char> used(runs.size(), 0), tch(static_cast<size_t>(nslots), 0);
+  std::vector<int> seq;
+  int budget = 100000;
+  std::function<bool()> place = [&]() -> bool {
+    if (seq.size() == runs.size()) return true;
+    if (--budget < 0) return false;
+    for (int k : idx) {
+      if (used[k]) continue;
+      int nt = 0;
+      for (int q = 0; q < runs[k].second; ++q) nt += tch[runs[k].first + q];
+      if (nt != 0 && nt != runs[k].second) continue;
+      std::vector<char> saved = tch;
+      for (int q = 0; q < runs[k].second; ++q) tch[runs[k].first + q] = 1;
+      used[k] = 1;
+      seq.push_back(k);
+      if (place()) return true;
+      seq.pop_back();
+      used[k] = 0;
+      tch = saved;
+      if (nt != 0) break;  // an all-touched run fits anywhere: no other choice is better here
+    }
+    return false;
+  };
+  if (!place()) return false;
+  *seq_out = seq;
+  return true;
+}
 }  // namespace
 
 // Two M tiles per A stage (their input-row halo loaded once) when it fits as
 // well as one tile per stage does and the batch is large; WF_TPS=1 forces one.
 wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, Schedule* out,
-                        std::string* err) {
+                        std::string* err, int kpair_req) {
   Schedule s1;
-  wf_status st = make_schedule_tps(d, f_req, gs_req, in_dtype, 1, &s1, err);
+  wf_status st = make_schedule_tps(d, f_req, gs_req, in_dtype, 1, &s1, err, kpair_req);
   if (st != WF_OK || s1.plan.status != WF_FOLD_APPLY || f_req == 0) {
     *out = std::move(s1);
     return st;
@@ -79,7 +217,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf
       d.n * s1.ohb >= 8 * 148) {  // keep >= 4 stage units per B200 SM: small batches keep the parallelism
     Schedule s2;
     std::string e2;
-    if (make_schedule_tps(d, f_req, gs_req, in_dtype, 2, &s2, &e2) == WF_OK && s2.plan.status == WF_FOLD_APPLY &&
+    if (make_schedule_tps(d, f_req, gs_req, in_dtype, 2, &s2, &e2, kpair_req) == WF_OK && s2.plan.status == WF_FOLD_APPLY &&
         s2.stages >= 2 && s2.ntiles.size() == s1.ntiles.size()) {
       *out = std::move(s2);
       return WF_OK;
@@ -91,7 +229,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf
 
 namespace {
 wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, int tps,
-                            Schedule* out, std::string* err) {
+                            Schedule* out, std::string* err, int kpair_req) {
   wf_status st = validate_desc(d, err);
   if (st != WF_OK) return st;
   if (in_dtype != WF_BF16 && in_dtype != WF_F16 && in_dtype != WF_TF32) {
@@ -126,7 +264,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     for (int64_t cand = base; cand <= d.w; cand += base) {
       Schedule tmp;
       std::string e2;
-      wf_status s2 = make_schedule(d, cand, gs_req, in_dtype, &tmp, &e2);
+      wf_status s2 = make_schedule(d, cand, gs_req, in_dtype, &tmp, &e2, kpair_req);
       if (s2 != WF_OK) {
         *err = e2;
         return s2;
@@ -328,10 +466,65 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     }
   }
   auto n_units = [&](int64_t g) { return static_cast<int64_t>(U[g].size()); };
+  // ---- cross-kh core-column pairing (kpair) ---------------------------------
+  // Every (kh, core column c) a group's window touches is one 16-byte core
+  // column of A; the legacy cover rounds each kh row's window out to 32-byte
+  // K-steps. kpair instead pairs two single core columns that feed the same
+  // accumulator run -- (kh, c) with (kh', c), or any two leftovers -- into one
+  // K=16 MMA whose descriptor LBO is the distance between them. Chosen when the
+  // measured-cycle cost model says it is cheaper (WF_KPAIR=0/1 forces it).
+  const int64_t KHn = d.kh;
+  auto kpair_mmas = [&](const std::vector<int>& ord) {  // ord: slot -> group
+    return build_kpair(ord, lo, hi, static_cast<int>(KHn), S.Ng);
+  };
+  auto kpair_cost = [&](const std::vector<int>& ord) {
+    int64_t c = 0;
+    for (const PMma& m : kpair_mmas(ord)) c += mma_cost(static_cast<int64_t>(m.len) * S.Ng);
+    return c;
+  };
+  auto best_kpair_order = [&](std::vector<int> ord, int64_t* cost) {
+    std::vector<int> best_ord = ord;
+    int64_t best = kpair_cost(ord);
+    if (ord.size() <= 6) {
+      std::sort(ord.begin(), ord.end());
+      do {
+        const int64_t c = kpair_cost(ord);
+        if (c < best) { best = c; best_ord = ord; }
+      } while (std::next_permutation(ord.begin(), ord.end()));
+    }
+    *cost = best;
+    return best_ord;
+  };
+  {
+    const char* env = std::getenv("WF_KPAIR");
+    bool use = false;
+    if (kpair_req >= 0) {
+      use = kpair_req == 1;
+    } else if (env && env[0] == '1') {
+      use = true;
+    } else if (!(env && env[0] == '0')) {
+      int64_t legacy = 0, kp = 0;
+      for (int64_t g0 = 0; g0 < G;) {  // column tiles of <= 256 accumulator columns, as above
+        int64_t g1 = g0;
+        while (g1 < G && (g1 - g0 + 1) * S.Ng <= kMaxAccCols) ++g1;
+        std::vector<std::vector<int64_t>> us(U.begin() + g0, U.begin() + g1);
+        legacy += KHn * best_order_cost(us);
+        std::vector<int> ord(static_cast<size_t>(g1 - g0));
+        std::iota(ord.begin(), ord.end(), static_cast<int>(g0));
+        int64_t c = 0;
+        best_kpair_order(ord, &c);
+        kp += c;
+        g0 = g1;
+      }
+      use = kp < legacy;
+    }
+    S.kpair = use;
+  }
   S.need_shift = false;
-  for (int64_t g = 0; g < G; ++g)
-    for (int64_t st : U[g])
-      if (st % Q == Q - 1) S.need_shift = true;
+  if (!S.kpair)
+    for (int64_t g = 0; g < G; ++g)
+      for (int64_t st : U[g])
+        if (st % Q == Q - 1) S.need_shift = true;
   S.units = U;
   // A layout. Without straddling K-steps (and 2-byte inputs), every K-step is
   // 32 contiguous bytes inside one folded pixel: the A tile is kept as one
@@ -339,7 +532,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // one 32-byte TMA piece per K-step; row-shifted views verified in
   // tools/probes/sw32_probe.cu). Otherwise the canonical no-swizzle layout of
   // 16-byte core columns ([q][row][folded col][16 B], + the shift region).
-  S.sw32 = !S.need_shift && Q >= 2 && in_dtype != WF_TF32;
+  S.sw32 = !S.kpair && !S.need_shift && Q >= 2 && in_dtype != WF_TF32;
   if (S.sw32) {
     S.qs.clear();
     for (int64_t g = 0; g < G; ++g)
@@ -358,12 +551,37 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   S.tile_shift = static_cast<int>(OHt * Wbox * (S.sw32 ? 32 : 16));  // A bytes between the stage's tiles
   const int64_t block_bytes = static_cast<int64_t>(S.Ng) * 32;  // 2 core cols x Ng rows x 16 B
   auto group_b_bytes = [&](int64_t g) { return d.kh * n_units(g) * block_bytes; };
+  // B bytes of the N-tile holding groups [g0, g1) (kpair: as built in slot order g0, g0+1, ...)
+  auto tile_b_bytes = [&](int64_t g0, int64_t g1) {
+    int64_t bytes = 0;
+    if (S.kpair) {
+      std::vector<int> ord(static_cast<size_t>(g1 - g0));
+      std::iota(ord.begin(), ord.end(), static_cast<int>(g0));
+      for (const PMma& m : kpair_mmas(ord)) bytes += static_cast<int64_t>(m.len) * S.Ng * 32;
+    } else {
+      for (int64_t g = g0; g < g1; ++g) bytes += group_b_bytes(g);
+    }
+    return bytes;
+  };
 
   // ---- N-tiles and shared-memory budget ------------------------------------
   const int ctrl_bytes = 1024;
   const int staging = kStagingBytes;   // 4 epilogue warps x 2 x 2 KB
   const int a_pad = kTileM * 16;
   const int bias_bytes = kMaxAccCols * 4;
+  const int64_t ring = (S.prod == 1 || S.prod == 2) ? static_cast<int64_t>(kRawSlots) * raw_slot_bytes_for(d.w * d.c * S.esize) : 0;
+  // A stages that fit beside a resident B of max_b bytes (>= 2, else false)
+  auto fit_stages = [&](int64_t max_b) {
+    const int64_t fixed = ctrl_bytes + staging + a_pad + 128 + (max_b + 127) / 128 * 128 + bias_bytes + ring + 1024;
+    int stages = 0;
+    for (int st2 = 4; st2 >= 2; --st2)
+      if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { stages = st2; break; }
+    if (stages < 2) return false;
+    S.stages = stages;
+    S.b_smem_bytes = static_cast<int>((max_b + 127) / 128 * 128);
+    S.smem_bytes = static_cast<int>(fixed + static_cast<int64_t>(stages) * S.stage_bytes);
+    return true;
+  };
   int64_t b_budget = 128 * 1024;
   for (int attempt = 0; attempt < 8; ++attempt) {
     S.ntiles.clear();
@@ -373,10 +591,10 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
       NTile t{};
       t.g0 = static_cast<int>(g);
       int64_t cols = 0, bytes = 0;
-      while (g < G && cols + S.Ng <= kMaxAccCols && bytes + group_b_bytes(g) <= b_budget) {
+      while (g < G && cols + S.Ng <= kMaxAccCols && tile_b_bytes(t.g0, g + 1) <= b_budget) {
         cols += S.Ng;
-        bytes += group_b_bytes(g);
         ++g;
+        bytes = tile_b_bytes(t.g0, g);
       }
       if (g == t.g0) { ok = false; break; }
       t.g1 = static_cast<int>(g);
@@ -390,27 +608,9 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
       *out = S;
       return WF_OK;
     }
-    int64_t max_b = 0, max_entries = 0;
-    for (auto& t : S.ntiles) {
-      max_b = std::max(max_b, t.b_bytes);
-      int64_t e = 0;
-      for (int gg = t.g0; gg < t.g1; ++gg) e += d.kh * n_units(gg);
-      max_entries = std::max(max_entries, e);
-    }
-    const int64_t table_b = max_entries * 16;
-    (void)table_b;  // the schedule lives in the kernel's constant bank
-    const int64_t ring = (S.prod == 1 || S.prod == 2) ? static_cast<int64_t>(kRawSlots) * raw_slot_bytes_for(d.w * d.c * S.esize) : 0;
-    const int64_t fixed = ctrl_bytes + staging + a_pad + 128 + (max_b + 127) / 128 * 128 + bias_bytes + ring + 1024;
-    int stages = 0;
-    for (int st2 = 4; st2 >= 2; --st2)
-      if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { stages = st2; break; }
-    if (stages >= 2) {
-      S.stages = stages;
-      S.b_smem_bytes = static_cast<int>((max_b + 127) / 128 * 128);
-      S.table_smem_bytes = static_cast<int>(table_b);
-      S.smem_bytes = static_cast<int>(fixed + static_cast<int64_t>(stages) * S.stage_bytes);
-      break;
-    }
+    int64_t max_b = 0;
+    for (auto& t : S.ntiles) max_b = std::max(max_b, t.b_bytes);
+    if (fit_stages(max_b)) break;
     b_budget /= 2;
     if (attempt == 7 || b_budget < block_bytes) {
       S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
@@ -460,91 +660,134 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     return c;
   };
   S.entries.clear();
+  S.entry_cc0.clear();
+  S.entry_cc1.clear();
+  S.entry_lbo.clear();
   S.order.assign(static_cast<size_t>(G), 0);
+  // byte offset of core column c of kh's window row inside an A stage (no-swizzle layout)
+  auto cc_addr = [&](int64_t kh, int64_t c) {
+    const int64_t delta = kh - d.pad_h;
+    const int b = static_cast<int>(pos_mod(delta, sh));
+    const int a = static_cast<int>((delta - b) / sh);
+    return static_cast<uint32_t>(b * S.region_bytes + ((a - S.amin[b]) * Wbox + c / Q) * 16 + (c % Q) * S.lbo_a);
+  };
+  auto cc_word = [](int64_t kh, int64_t c, uint32_t mask) {
+    return static_cast<uint32_t>(kh) | (static_cast<uint32_t>(c) << 8) | (mask << 16);
+  };
   int64_t b_cursor = 0;
   for (auto& t : S.ntiles) {
     std::vector<int> order;
     for (int g = t.g0; g < t.g1; ++g) order.push_back(g);
-    if (t.g1 - t.g0 <= 8) {  // exhaustive over slot orders (<= 40320)
-      std::vector<int> cand = order;
-      int64_t best = order_cost(t, order);
-      while (std::next_permutation(cand.begin(), cand.end())) {
-        const int64_t c = order_cost(t, cand);
-        if (c < best) { best = c; order = cand; }
-      }
-    }
-    for (size_t sidx = 0; sidx < order.size(); ++sidx) S.order[t.g0 + sidx] = order[sidx];
-    const std::vector<Run> runs = runs_for(t, order);
-    // zero-init: at kh == 0 every group's first MMA must not accumulate, so the
-    // kh == 0 runs are ordered such that each one meets either only untouched
-    // groups (accumulate = 0) or only touched ones (backtracking, few runs)
-    std::vector<Run> first;
-    {
-      std::vector<Run> pool = runs;
-      std::stable_sort(pool.begin(), pool.end(), [](const Run& x, const Run& y) { return x.len > y.len; });
-      std::vector<char> used(pool.size(), 0), tch(order.size(), 0);
-      std::vector<Run> seq;
-      std::function<bool()> place = [&]() -> bool {
-        if (seq.size() == pool.size()) return true;
-        for (size_t k = 0; k < pool.size(); ++k) {
-          if (used[k]) continue;
-          int nt = 0;
-          for (int q = 0; q < pool[k].len; ++q) nt += tch[pool[k].slot0 + q];
-          if (nt != 0 && nt != pool[k].len) continue;
-          std::vector<char> saved = tch;
-          for (int q = 0; q < pool[k].len; ++q) tch[pool[k].slot0 + q] = 1;
-          used[k] = 1;
-          seq.push_back(pool[k]);
-          if (place()) return true;
-          seq.pop_back();
-          used[k] = 0;
-          tch = saved;
-        }
-        return false;
-      };
-      first = place() ? seq : pool;  // no valid order: the check below falls back
-    }
     t.entry0 = static_cast<int>(S.entries.size());
     t.b_off = b_cursor;
     uint32_t boff = 0;
-    bool ok_init = true;
-    for (int64_t kh = 0; kh < d.kh; ++kh) {
-      const int64_t delta = kh - d.pad_h;
-      const int b = static_cast<int>(pos_mod(delta, sh));
-      const int a = static_cast<int>((delta - b) / sh);
+    if (S.kpair) {
+      int64_t cst = 0;
+      order = best_kpair_order(order, &cst);
+      for (size_t sidx = 0; sidx < order.size(); ++sidx) S.order[t.g0 + sidx] = order[sidx];
+      const std::vector<PMma> mm = kpair_mmas(order);
+      std::vector<std::pair<int, int>> rr;
+      for (const PMma& m : mm) rr.push_back({m.slot0, m.len});
+      std::vector<int> seq;
+      if (!zero_init_order(rr, static_cast<int>(order.size()), &seq))
+        return make_schedule_tps(d, f_req, gs_req, in_dtype, tps, out, err, 0);
       std::vector<char> touched(order.size(), 0);
-      for (const Run& rn : (kh == 0 ? first : runs)) {
-        const int64_t u = rn.u;  // first core column of the pair
-        const int64_t kp = u / Q, q = u % Q;
+      for (int k : seq) {
+        const PMma& m = mm[k];
+        int i0 = 0, i1 = 1;  // core column 0 of the K-step = the lower shared-memory address
+        if (cc_addr(m.kh[1], m.c[1]) < cc_addr(m.kh[0], m.c[0])) std::swap(i0, i1);
+        const uint32_t a0 = cc_addr(m.kh[i0], m.c[i0]), a1 = cc_addr(m.kh[i1], m.c[i1]);
         MmaEntry e{};
-        if (S.sw32) {
-          const int qi = static_cast<int>(std::find(S.qs.begin(), S.qs.end(), static_cast<int>(q)) - S.qs.begin());
-          e.a_off = static_cast<uint32_t>(b * S.region_bytes + qi * S.qregion_bytes + ((a - S.amin[b]) * Wbox + kp) * 32);
-        } else {
-          e.a_off = static_cast<uint32_t>(b * S.region_bytes + ((a - S.amin[b]) * Wbox + kp) * 16 + q * S.lbo_a);
-        }
+        e.a_off = a0;
         e.b_off = boff;
-        const int64_t n = static_cast<int64_t>(rn.len) * S.Ng;
+        const int64_t n = static_cast<int64_t>(m.len) * S.Ng;
         boff += static_cast<uint32_t>(n * 32);
-        bool acc = true;
-        if (kh == 0) {
-          int nt = 0;
-          for (int k = 0; k < rn.len; ++k) nt += touched[rn.slot0 + k];
-          if (nt != 0 && nt != rn.len) ok_init = false;
-          acc = (nt != 0);
-          for (int k = 0; k < rn.len; ++k) touched[rn.slot0 + k] = 1;
-        }
-        e.meta = static_cast<uint32_t>(kh) | (static_cast<uint32_t>(u) << 8) |
-                 (static_cast<uint32_t>(rn.slot0) << 16) | (static_cast<uint32_t>(n >> 3) << 22) |
+        const bool acc = touched[m.slot0] != 0;  // zero_init_order: all or none of the run touched
+        for (int q = 0; q < m.len; ++q) touched[m.slot0 + q] = 1;
+        e.meta = static_cast<uint32_t>(m.kh[i0]) | (static_cast<uint32_t>(m.c[i0]) << 8) |
+                 (static_cast<uint32_t>(m.slot0) << 16) | (static_cast<uint32_t>(n >> 3) << 22) |
                  (acc ? 0x80000000u : 0u);
-        e.tmem_col = static_cast<uint32_t>(rn.slot0 * S.Ng);
+        e.tmem_col = static_cast<uint32_t>(m.slot0 * S.Ng);
         S.entries.push_back(e);
+        S.entry_cc0.push_back(cc_word(m.kh[i0], m.c[i0], m.mask[i0]));
+        S.entry_cc1.push_back(cc_word(m.kh[i1], m.c[i1], m.mask[i1]));
+        S.entry_lbo.push_back(a1 - a0);
       }
-    }
-    if (!ok_init) {  // cannot happen with disjoint per-group units; keep the planner total
-      S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
-      *out = S;
-      return WF_OK;
+      t.b_bytes = boff;
+    } else {
+      if (t.g1 - t.g0 <= 8) {  // exhaustive over slot orders (<= 40320)
+        std::vector<int> cand = order;
+        int64_t best = order_cost(t, order);
+        while (std::next_permutation(cand.begin(), cand.end())) {
+          const int64_t c = order_cost(t, cand);
+          if (c < best) { best = c; order = cand; }
+        }
+      }
+      for (size_t sidx = 0; sidx < order.size(); ++sidx) S.order[t.g0 + sidx] = order[sidx];
+      const std::vector<Run> runs = runs_for(t, order);
+      // zero-init: at kh == 0 every group's first MMA must not accumulate, so the
+      // kh == 0 runs are ordered such that each one meets either only untouched
+      // groups (accumulate = 0) or only touched ones (backtracking, few runs)
+      std::vector<Run> first = runs;
+      {
+        std::vector<std::pair<int, int>> rr;
+        for (const Run& rn : runs) rr.push_back({rn.slot0, rn.len});
+        std::vector<int> seq;
+        if (zero_init_order(rr, static_cast<int>(order.size()), &seq))
+          for (size_t k = 0; k < seq.size(); ++k) first[k] = runs[seq[k]];
+      }
+      bool ok_init = true;
+      for (int64_t kh = 0; kh < d.kh; ++kh) {
+        const int64_t delta = kh - d.pad_h;
+        const int b = static_cast<int>(pos_mod(delta, sh));
+        const int a = static_cast<int>((delta - b) / sh);
+        std::vector<char> touched(order.size(), 0);
+        for (const Run& rn : (kh == 0 ? first : runs)) {
+          const int64_t u = rn.u;  // first core column of the pair
+          const int64_t kp = u / Q, q = u % Q;
+          MmaEntry e{};
+          if (S.sw32) {
+            const int qi = static_cast<int>(std::find(S.qs.begin(), S.qs.end(), static_cast<int>(q)) - S.qs.begin());
+            e.a_off = static_cast<uint32_t>(b * S.region_bytes + qi * S.qregion_bytes + ((a - S.amin[b]) * Wbox + kp) * 32);
+          } else {
+            e.a_off = static_cast<uint32_t>(b * S.region_bytes + ((a - S.amin[b]) * Wbox + kp) * 16 + q * S.lbo_a);
+          }
+          e.b_off = boff;
+          const int64_t n = static_cast<int64_t>(rn.len) * S.Ng;
+          boff += static_cast<uint32_t>(n * 32);
+          bool acc = true;
+          if (kh == 0) {
+            int nt = 0;
+            for (int k = 0; k < rn.len; ++k) nt += touched[rn.slot0 + k];
+            if (nt != 0 && nt != rn.len) ok_init = false;
+            acc = (nt != 0);
+            for (int k = 0; k < rn.len; ++k) touched[rn.slot0 + k] = 1;
+          }
+          e.meta = static_cast<uint32_t>(kh) | (static_cast<uint32_t>(u) << 8) |
+                   (static_cast<uint32_t>(rn.slot0) << 16) | (static_cast<uint32_t>(n >> 3) << 22) |
+                   (acc ? 0x80000000u : 0u);
+          e.tmem_col = static_cast<uint32_t>(rn.slot0 * S.Ng);
+          S.entries.push_back(e);
+          // core column u of a step is owned by the group's step at u - 1 if it has one
+          uint32_t mask0 = 0;
+          for (int k = 0; k < rn.len; ++k) {
+            const auto& ug = U[order[rn.slot0 + k]];
+            if (std::find(ug.begin(), ug.end(), u - 1) == ug.end()) mask0 |= 1u << k;
+          }
+          S.entry_cc0.push_back(cc_word(kh, u, mask0));
+          S.entry_cc1.push_back(cc_word(kh, u + 1, (1u << rn.len) - 1u));
+          S.entry_lbo.push_back(static_cast<uint32_t>(S.lbo_a));
+        }
+      }
+      if (!ok_init) {  // cannot happen with disjoint per-group units; keep the planner total
+        S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
+        *out = S;
+        return WF_OK;
+      }
+      if (static_cast<int64_t>(boff) != t.b_bytes) {
+        *err = "internal: B operand bytes of a merged schedule differ from the plan";
+        return WF_INVALID_ARGUMENT;
+      }
     }
     t.entries = static_cast<int>(S.entries.size()) - t.entry0;
     // Half-split accumulator release: MMAs writing only the lower half of the
@@ -553,25 +796,34 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     {
       const int mid = t.cols / 2;
       bool clean = (t.cols / S.CH) % 2 == 0 && mid % S.CH == 0;
-      std::vector<MmaEntry> lo_e, hi_e;
+      std::vector<int> lo_i, hi_i;
       for (int i = t.entry0; i < t.entry0 + t.entries && clean; ++i) {
         const MmaEntry& e = S.entries[i];
         const int c0e = static_cast<int>(e.tmem_col), ne = static_cast<int>((e.meta >> 22) & 0x1FFu) * 8;
-        if (c0e + ne <= mid) lo_e.push_back(e);
-        else if (c0e >= mid) hi_e.push_back(e);
+        if (c0e + ne <= mid) lo_i.push_back(i);
+        else if (c0e >= mid) hi_i.push_back(i);
         else clean = false;
       }
-      if (clean && !lo_e.empty() && !hi_e.empty()) {
-        std::copy(lo_e.begin(), lo_e.end(), S.entries.begin() + t.entry0);
-        std::copy(hi_e.begin(), hi_e.end(), S.entries.begin() + t.entry0 + lo_e.size());
-        t.split = static_cast<int>(lo_e.size());
+      if (clean && !lo_i.empty() && !hi_i.empty()) {
+        std::vector<int> perm = lo_i;
+        perm.insert(perm.end(), hi_i.begin(), hi_i.end());
+        auto permute = [&](auto& v) {
+          auto old = v;
+          for (size_t k = 0; k < perm.size(); ++k) v[t.entry0 + k] = old[perm[k]];
+        };
+        permute(S.entries);
+        permute(S.entry_cc0);
+        permute(S.entry_cc1);
+        permute(S.entry_lbo);
+        t.split = static_cast<int>(lo_i.size());
       }
     }
-    if (static_cast<int64_t>(boff) != t.b_bytes) {
-      *err = "internal: B operand bytes of a merged schedule differ from the plan";
-      return WF_INVALID_ARGUMENT;
-    }
     b_cursor += t.b_bytes;
+  }
+  if (S.kpair) {  // exact B sizes: the A stages must still fit beside the largest
+    int64_t max_b = 0;
+    for (const auto& t : S.ntiles) max_b = std::max(max_b, t.b_bytes);
+    if (!fit_stages(max_b)) return make_schedule_tps(d, f_req, gs_req, in_dtype, tps, out, err, 0);
   }
 
   // ---- plan facts -----------------------------------------------------------
@@ -599,8 +851,9 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   p.wbox = Wbox;
   p.nrows = NR;
   p.mma_entries = static_cast<int64_t>(S.entries.size());
-  // packed header: schedule table, then the slot -> group order (int32 each)
-  p.table_bytes = (p.mma_entries * 16 + G * 4 + 127) / 128 * 128;
+  // packed header: schedule table, the slot -> group order (int32 each), then
+  // the (core column 0, core column 1) words of every entry
+  p.table_bytes = (p.mma_entries * 24 + G * 4 + 127) / 128 * 128;
   p.packed_bytes = p.table_bytes + b_cursor;
   p.epi_chunk = S.CH;
   S.raw_slots = kRawSlots;
@@ -632,6 +885,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     }
     p.cta_pair = S.pair;
     p.stage_tiles = S.tps;
+    p.kstep_mode = S.kpair ? 1 : 0;
   }
   p.useful_macs = static_cast<uint64_t>(d.n) * OH * OW * d.cout * d.kh * d.kw * d.c;
   uint64_t issued_per_tile = 0;
@@ -713,6 +967,9 @@ wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Sched
                (static_cast<uint32_t>(d.cout >> 3) << 22) | (acc ? 0x80000000u : 0u);
       e.tmem_col = 0;
       S.entries.push_back(e);
+      S.entry_cc0.push_back(static_cast<uint32_t>(kh) | (static_cast<uint32_t>(2 * u) << 8) | (1u << 16));
+      S.entry_cc1.push_back(static_cast<uint32_t>(kh) | (static_cast<uint32_t>(2 * u + 1) << 8) | (1u << 16));
+      S.entry_lbo.push_back(static_cast<uint32_t>(S.lbo_a));
     }
   }
   for (size_t k = 0; k < S.ks_entry0.size(); ++k)
@@ -754,7 +1011,7 @@ wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Sched
   p.wbox = 0;
   p.nrows = 0;
   p.mma_entries = static_cast<int64_t>(S.entries.size());
-  p.table_bytes = (p.mma_entries * 16 + 4 + 127) / 128 * 128;
+  p.table_bytes = (p.mma_entries * 24 + 4 + 127) / 128 * 128;
   p.packed_bytes = p.table_bytes + t.b_bytes;
   p.epi_chunk = S.CH;
   p.variant = WF_VARIANT_UNFOLDED;
@@ -778,7 +1035,8 @@ wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
   }
   wf_status st = (p.variant == WF_VARIANT_UNFOLDED)
                      ? make_schedule_unfolded(d, static_cast<wf_dtype>(p.in_dtype), out, err)
-                     : make_schedule(d, p.f, p.group_size, static_cast<wf_dtype>(p.in_dtype), out, err);
+                     : make_schedule(d, p.f, p.group_size, static_cast<wf_dtype>(p.in_dtype), out, err,
+                                     p.kstep_mode);
   if (st != WF_OK) return st;
   if (out->plan.status != WF_FOLD_APPLY || out->plan.packed_bytes != p.packed_bytes ||
       out->plan.mma_entries != p.mma_entries) {

@@ -71,7 +71,7 @@ struct MmaEntry {          // 16 bytes, lives in the packed buffer and in smem
   uint32_t a_off;          // byte offset of the A view inside an A stage
   uint32_t b_off;          // byte offset of the B block inside the N-tile's B
   uint32_t meta;           // kh | u << 8 | slot << 16 | (N/8) << 22 | accumulate << 31
-                           // (u: first core column; slot: first accumulator slot)
+                           // (kh, u: position of core column 0; slot: first accumulator slot)
   uint32_t tmem_col;       // accumulator column of the group
 };
 
@@ -114,6 +114,16 @@ struct Schedule {
   int smem_bytes = 0, b_smem_bytes = 0, table_smem_bytes = 0;
   int64_t num_mtiles = 0, ohb = 0;
   std::vector<MmaEntry> entries;
+  // Per entry, what each of its two 16-byte core columns holds:
+  // kh | c << 8 | mask << 16 (c: core column of the KW'*f*C window row; mask:
+  // the run's accumulator slots whose B rows are nonzero for it). Packed into
+  // the header after the slot order; the pack kernel builds B from it.
+  std::vector<uint32_t> entry_cc0, entry_cc1;
+  std::vector<uint32_t> entry_lbo;  // per entry: A bytes from core column 0 to core column 1
+  // Cross-kh core-column pairing: every MMA K-step is two single core columns
+  // (8 bf16 / 4 tf32 elements) of any (kh, c) positions with the same output
+  // groups -- K granularity 8 elements instead of 16 (no-swizzle A only).
+  bool kpair = false;
   std::vector<NTile> ntiles;
   std::vector<int> order;        // accumulator slot (g0 + s of its N-tile) -> group
   std::vector<std::vector<int64_t>> units;  // per group: the first core columns of its K-steps
@@ -125,8 +135,10 @@ wf_status validate_desc(const wf_conv_desc& d, std::string* err);
 
 // Full planner. Returns WF_OK with plan.status == APPLY or FALLBACK (reason),
 // or an error status (shape problems, bad arguments).
+// kpair_req: -1 choose the K-step mode (cost model; WF_KPAIR=0/1 overrides),
+// 0 / 1 force 32-byte covers / cross-kh core-column pairs.
 wf_status make_schedule(const wf_conv_desc& d, int64_t f, int64_t group_size,
-                        wf_dtype in_dtype, Schedule* out, std::string* err);
+                        wf_dtype in_dtype, Schedule* out, std::string* err, int kpair_req = -1);
 
 // The unfolded Cin=C variant of the same kernel (explicit im2col A tiles):
 // the fold-vs-unfolded comparison of the north star.

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version_and_error_channel():
-    assert A.lib().wf_abi_version() == 5
+    assert A.lib().wf_abi_version() == 6
     d = A.make_desc(1, 8, 8, 3, 3, 3, 4, 1, 1, 0, 0)
     p = A.FoldPlan()
     # bad dtype -> WF_INVALID_ARGUMENT with a message

@@ -11,6 +11,7 @@ import pytest
 import torch
 
 import paper_2601_11608_b200 as wf
+from paper_2601_11608_b200 import _abi as A
 from tests.test_oracle import CONFIG_GEOM
 
 pytestmark = pytest.mark.gpu
@@ -114,53 +115,62 @@ def test_tensor_core_conv_configs_within_tolerance(golden_configs, name):
     assert err <= TOL[dt], f"{name}: normwise rel {err:.3e} > {TOL[dt]} (plan {conv.device_plan})"
 
 
+@pytest.mark.parametrize("kpair", ["0", "1"])
 @pytest.mark.parametrize("name", list(CONFIG_GEOM))
-def test_tensor_core_conv_integer_data_exact(golden_configs, name):
-    y, ref, dt, _ = _config_run(golden_configs, name, "i", out_dtype=torch.float32)
-    np.testing.assert_array_equal(y, ref, err_msg=name)
+def test_tensor_core_conv_integer_data_exact(golden_configs, name, kpair, monkeypatch):
+    """Both K-step schedules (32-byte covers / cross-kh core-column pairs) are exact on integers."""
+    monkeypatch.setenv("WF_KPAIR", kpair)
+    y, ref, dt, conv = _config_run(golden_configs, name, "i", out_dtype=torch.float32)
+    np.testing.assert_array_equal(y, ref, err_msg=f"{name} plan {conv.device_plan}")
 
 
-def test_packed_operand_unpacks_to_the_expansion(oracle):
-    """The once-packed tcgen05 B operand holds exactly W'(kh, kw', fi*C+c, j*Co+co).
+def _unpack_and_check(conv, w, s, p, oracle):
+    """Rebuild W'(kh, kw', fi*C+c, j*Co+co) from the packed operand; every
+    nonzero of the expansion must be stored exactly once.
 
     Packed header: per MMA a 16-byte entry (a_off, b_off, meta, tmem_col),
-    meta = kh | u << 8 | slot << 16 | (N/8) << 22 | acc << 31, then the
-    accumulator-slot -> group order (int32). B block of an entry:
-    [core col 0..1][N rows][8 elements]; row n is accumulator column
-    slot*Ng + n = group order[slot + n // Ng], output column chunk_perm(n % Ng).
+    meta = kh | u << 8 | slot << 16 | (N/8) << 22 | acc << 31, the
+    accumulator-slot -> group order (int32), then per entry two words
+    kh | c << 8 | mask << 16 naming the window-row core column c of filter row
+    kh that the entry's core column 0 / 1 holds, for the slots in mask. B block
+    of an entry: [core col 0..1][N rows][8 elements]; row n is accumulator
+    column slot*Ng + n = group order[slot + n // Ng], output column
+    chunk_perm(n % Ng).
     """
-    rng = np.random.default_rng(5)
-    KH, KW, C, Co, s, p = 7, 7, 3, 64, 2, 3
-    w = rng.integers(-8, 9, (KH, KW, C, Co)).astype(np.float32)
-    conv = wf.FoldedConv2d(cuda(w, torch.bfloat16), None, (2, 64, 64, 3), stride=s, padding=p,
-                           dtype=torch.bfloat16)
+    KH, KW, C, Co = w.shape
     d = conv.device_plan
     f, gs, ch = d["f"], d["group_size"], d["epi_chunk"]
     Ng = gs * Co
     G = d["n_groups"]
-    assert d["n_tiles"] == 1
     wexp = oracle.expand_filter_folded(w, f, s, p)  # (KH, KW', f*C, r*Co)
+    kwf = wexp.shape[1]
+    E2 = 8  # 2-byte elements per 16-byte core column
     raw = conv.packed.cpu().numpy()
     n_ent = d["mma_entries"]
     table = raw[: n_ent * 16].view(np.uint32).reshape(n_ent, 4)
     order = raw[n_ent * 16: n_ent * 16 + 4 * G].view(np.int32)
+    ccw = raw[n_ent * 16 + 4 * G: n_ent * 24 + 4 * G].view(np.uint32).reshape(n_ent, 2)
     assert sorted(order.tolist()) == list(range(G))
-    base = (n_ent * 16 + 4 * G + 127) // 128 * 128
+    base = (n_ent * 24 + 4 * G + 127) // 128 * 128
     pair = d["cta_pair"]
     b_total = len(raw) - base
-    checked = 0
-    covered = np.zeros((KH, G), np.int64)
-    # each group's K-step starts; a core column covered by two steps of a group
-    # lives in the lower one (zero in the upper one's B rows)
-    starts = {g: set() for g in range(G)}
-    for (a_off, b_off, meta, col) in table:
-        u, slot, N = (meta >> 8) & 0xFF, (meta >> 16) & 0x3F, ((meta >> 22) & 0x1FF) * 8
-        for k in range(N // Ng):
-            starts[int(order[slot + k])].add(int(u))
-    for (a_off, b_off, meta, col) in table:
-        kh, u, slot = meta & 0xFF, (meta >> 8) & 0xFF, (meta >> 16) & 0x3F
+    recon = np.zeros((KH, kwf * f * C + 2 * E2, wexp.shape[3]), np.float64)
+    # N-tile of every entry (first group, B base = the B bytes of the tiles before it)
+    nts = np.array(A.schedule_describe(A.make_desc(*conv.input_shape, KH, KW, Co, s, s, p, p), 0, 0,
+                                       A.WF_BF16)["ntiles"]).reshape(-1, 6)
+    assert len(nts) == d["n_tiles"]
+    tile_g0, tile_b0, bcur = np.zeros(n_ent, np.int64), np.zeros(n_ent, np.int64), 0
+    for (_, _, e0, ne, g0, _) in nts:
+        tile_g0[e0:e0 + ne] = g0
+        tile_b0[e0:e0 + ne] = bcur
+        bcur += int(sum(((table[i][2] >> 22) & 0x1FF) * 8 * 32 for i in range(e0, e0 + ne)))
+    assert bcur == b_total
+    for ei, ((a_off, b_off, meta, col), words) in enumerate(zip(table, ccw)):
+        slot = tile_g0[ei] + ((meta >> 16) & 0x3F)
         N = ((meta >> 22) & 0x1FF) * 8
-        assert col == slot * Ng
+        b_off = b_off + tile_b0[ei]
+        assert col == (slot - tile_g0[ei]) * Ng
+        assert (words[0] & 0xFF, (words[0] >> 8) & 0xFF) == (meta & 0xFF, (meta >> 8) & 0xFF)
         if pair == 2:  # CTA r of the pair holds rows [r*N/2, (r+1)*N/2) of every block
             halves = []
             for r in range(2):
@@ -170,20 +180,30 @@ def test_packed_operand_unpacks_to_the_expansion(oracle):
         else:
             blk = raw[base + b_off: base + b_off + N * 32].view(np.uint16).reshape(2, N, 8)
         vals = (blk.astype(np.uint32) << 16).view(np.float32)
-        for n in range(N):
-            g = order[slot + n // Ng]
-            covered[kh, g] += n % Ng == 0
-            ocol = g * Ng + chunk_perm(n % Ng, ch)
-            for cc in range(2):
-                widx = (u + cc) * 8 + np.arange(8)
-                kp, k = widx // (f * C), widx % (f * C)
-                want = wexp[kh, kp, k, ocol]
-                if cc == 0 and (u - 1) in starts[g]:
-                    want = np.zeros_like(want)
-                np.testing.assert_array_equal(vals[cc, n], want)
-                checked += 1
-    assert checked > 1000
-    assert (covered >= 1).all()  # every group gets MMAs at every kh
+        for cc in range(2):
+            kh, c, mask = words[cc] & 0xFF, (words[cc] >> 8) & 0xFF, words[cc] >> 16
+            for n in range(N):
+                if not (mask >> (n // Ng)) & 1:
+                    assert not vals[cc, n].any()
+                    continue
+                ocol = order[slot + n // Ng] * Ng + chunk_perm(n % Ng, ch)
+                recon[kh, c * E2: c * E2 + E2, ocol] += vals[cc, n]
+    assert not recon[:, kwf * f * C:].any()
+    np.testing.assert_array_equal(recon[:, : kwf * f * C].reshape(wexp.shape[0], kwf, f * C, -1), wexp)
+
+
+@pytest.mark.parametrize("kpair", ["0", "1"])
+def test_packed_operand_unpacks_to_the_expansion(oracle, monkeypatch, kpair):
+    """The once-packed tcgen05 B operand holds exactly W'(kh, kw', fi*C+c, j*Co+co),
+    with the legacy 32-byte K-step cover and with cross-kh core-column pairs."""
+    monkeypatch.setenv("WF_KPAIR", kpair)
+    rng = np.random.default_rng(5)
+    for (KH, KW, C, Co, s, p, hw) in [(7, 7, 3, 64, 2, 3, 64), (3, 3, 3, 64, 1, 1, 32), (11, 11, 3, 96, 4, 0, 67),
+                                      (3, 3, 3, 32, 2, 1, 32)]:
+        w = rng.integers(-8, 9, (KH, KW, C, Co)).astype(np.float32)
+        conv = wf.FoldedConv2d(cuda(w, torch.bfloat16), None, (2, hw, hw, 3), stride=s, padding=p,
+                               dtype=torch.bfloat16)
+        _unpack_and_check(conv, w, s, p, oracle)
 
 
 @pytest.mark.parametrize("batch,h,w", [(3, 36, 48), (1, 224, 224), (5, 20, 32), (2, 9, 16)])
@@ -286,9 +306,11 @@ def test_unfolded_variant_configs(golden_configs, name):
     np.testing.assert_array_equal(y, ref, err_msg=name)
 
 
+@pytest.mark.parametrize("kpair", ["0", "1"])
 @pytest.mark.parametrize("name", [n for n in CONFIG_GEOM if n != "r50_b1"])
-def test_gather_producer_matches_tma_bitwise(golden_configs, name):
+def test_gather_producer_matches_tma_bitwise(golden_configs, name, kpair, monkeypatch):
     """The software-gather producer builds the same shared-memory A image as the TMA boxes."""
+    monkeypatch.setenv("WF_KPAIR", kpair)
     y0, _, _, conv = _config_run(golden_configs, name, "")
     assert conv.device_plan["producer"] in ("tma", "repitch+tma")
     y1, _, _, _ = _config_run(golden_configs, name, "", flags=0x4000)

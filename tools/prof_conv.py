@@ -8,6 +8,7 @@ CFG = {  # n, h, w, c, kh, kw, cout, s, p, dtype, relu
     "r50": (8192, 224, 224, 3, 7, 7, 64, 2, 3, torch.bfloat16, False),
     "vgg": (256, 224, 224, 3, 3, 3, 64, 1, 1, torch.bfloat16, False),
     "mnv2": (1024, 224, 224, 3, 3, 3, 32, 2, 1, torch.float16, True),
+    "alex": (512, 227, 227, 3, 11, 11, 96, 4, 0, torch.bfloat16, False),
     "r50zp": (8192, 224, 224, 8, 7, 7, 64, 2, 3, torch.bfloat16, False),
 }
 name = sys.argv[1]
