@@ -61,7 +61,7 @@ wf_status validate_desc(const wf_conv_desc& d, std::string* err) {
 
 namespace {
 wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, int tps,
-                            Schedule* out, std::string* err, int kpair_req = -1);
+                            Schedule* out, std::string* err, int kpair_req = -1, int pair_req = 0);
 
 int64_t mma_cost(int64_t n) { return std::max<int64_t>(n / 2, 32 + n / 4); }
 
@@ -202,23 +202,37 @@ bool zero_init_order(const std::vector<std::pair<int, int>>& runs, int nslots, s
 }
 }  // namespace
 
-// Two M tiles per A stage (their input-row halo loaded once) when it fits as
-// well as one tile per stage does and the batch is large; WF_TPS=1 forces one.
+// Variant selection over one planner core (make_schedule_tps):
+//  * CTA pairs (cta_group::2, each SM holding half of every B block, so a B
+//    that needs two N-tiles on one CTA fits in one) only on request
+//    (WF_CTA_PAIR=1): measured slower on B200 even for AlexNet (B = 173 KB,
+//    0.290 vs 0.278 ms with two N-tiles);
+//  * else two M tiles per A stage (their input-row halo loaded once) when it
+//    fits as well as one tile per stage does and the batch is large; WF_TPS=1
+//    forces one.
+// kpair_req / pair_req / tps_req >= 0 pin a choice (schedule_from_plan).
 wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, Schedule* out,
-                        std::string* err, int kpair_req) {
+                        std::string* err, int kpair_req, int pair_req, int tps_req) {
+  if (pair_req < 0) {
+    const char* env = std::getenv("WF_CTA_PAIR");
+    if (env && (env[0] == '0' || env[0] == '1')) pair_req = env[0] - '0';
+  }
+  if (f_req == 0) return make_schedule_tps(d, f_req, gs_req, in_dtype, 1, out, err, kpair_req, pair_req < 0 ? -1 : pair_req);
+  if (pair_req == 1) return make_schedule_tps(d, f_req, gs_req, in_dtype, 1, out, err, kpair_req, 1);
   Schedule s1;
-  wf_status st = make_schedule_tps(d, f_req, gs_req, in_dtype, 1, &s1, err, kpair_req);
-  if (st != WF_OK || s1.plan.status != WF_FOLD_APPLY || f_req == 0) {
+  wf_status st = make_schedule_tps(d, f_req, gs_req, in_dtype, 1, &s1, err, kpair_req, 0);
+  if (st != WF_OK || s1.plan.status != WF_FOLD_APPLY) {
     *out = std::move(s1);
     return st;
   }
   const char* env = std::getenv("WF_TPS");
-  if (!(env && env[0] == '1') && (s1.prod == 0 || s1.prod == 3) && s1.pair == 1 && s1.ohb >= 2 &&
-      d.n * s1.ohb >= 8 * 148) {  // keep >= 4 stage units per B200 SM: small batches keep the parallelism
+  const bool try2 = tps_req == 2 || (tps_req < 0 && !(env && env[0] == '1') && s1.ohb >= 2 &&
+                                     d.n * s1.ohb >= 8 * 148);  // keep >= 4 stage units per B200 SM
+  if (try2 && (s1.prod == 0 || s1.prod == 3) && s1.pair == 1) {
     Schedule s2;
     std::string e2;
-    if (make_schedule_tps(d, f_req, gs_req, in_dtype, 2, &s2, &e2, kpair_req) == WF_OK && s2.plan.status == WF_FOLD_APPLY &&
-        s2.stages >= 2 && s2.ntiles.size() == s1.ntiles.size()) {
+    if (make_schedule_tps(d, f_req, gs_req, in_dtype, 2, &s2, &e2, kpair_req, 0) == WF_OK &&
+        s2.plan.status == WF_FOLD_APPLY && s2.stages >= 2 && s2.ntiles.size() == s1.ntiles.size()) {
       *out = std::move(s2);
       return WF_OK;
     }
@@ -229,7 +243,7 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf
 
 namespace {
 wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, int tps,
-                            Schedule* out, std::string* err, int kpair_req) {
+                            Schedule* out, std::string* err, int kpair_req, int pair_req) {
   wf_status st = validate_desc(d, err);
   if (st != WF_OK) return st;
   if (in_dtype != WF_BF16 && in_dtype != WF_F16 && in_dtype != WF_TF32) {
@@ -264,7 +278,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     for (int64_t cand = base; cand <= d.w; cand += base) {
       Schedule tmp;
       std::string e2;
-      wf_status s2 = make_schedule(d, cand, gs_req, in_dtype, &tmp, &e2, kpair_req);
+      wf_status s2 = make_schedule(d, cand, gs_req, in_dtype, &tmp, &e2, kpair_req, pair_req);
       if (s2 != WF_OK) {
         *err = e2;
         return s2;
@@ -582,7 +596,8 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     S.smem_bytes = static_cast<int>(fixed + static_cast<int64_t>(stages) * S.stage_bytes);
     return true;
   };
-  int64_t b_budget = 128 * 1024;
+  const int pr = (pair_req == 1) ? 2 : 1;  // CTA pairs: each SM holds half of every B block
+  int64_t b_budget = 128 * 1024 * pr;
   for (int attempt = 0; attempt < 8; ++attempt) {
     S.ntiles.clear();
     bool ok = true;
@@ -610,7 +625,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     }
     int64_t max_b = 0;
     for (auto& t : S.ntiles) max_b = std::max(max_b, t.b_bytes);
-    if (fit_stages(max_b)) break;
+    if (fit_stages((max_b + pr - 1) / pr)) break;
     b_budget /= 2;
     if (attempt == 7 || b_budget < block_bytes) {
       S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
@@ -690,7 +705,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
       for (const PMma& m : mm) rr.push_back({m.slot0, m.len});
       std::vector<int> seq;
       if (!zero_init_order(rr, static_cast<int>(order.size()), &seq))
-        return make_schedule_tps(d, f_req, gs_req, in_dtype, tps, out, err, 0);
+        return make_schedule_tps(d, f_req, gs_req, in_dtype, tps, out, err, 0, pair_req);
       std::vector<char> touched(order.size(), 0);
       for (int k : seq) {
         const PMma& m = mm[k];
@@ -823,7 +838,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   if (S.kpair) {  // exact B sizes: the A stages must still fit beside the largest
     int64_t max_b = 0;
     for (const auto& t : S.ntiles) max_b = std::max(max_b, t.b_bytes);
-    if (!fit_stages(max_b)) return make_schedule_tps(d, f_req, gs_req, in_dtype, tps, out, err, 0);
+    if (!fit_stages((max_b + pr - 1) / pr)) return make_schedule_tps(d, f_req, gs_req, in_dtype, tps, out, err, 0, pair_req);
   }
 
   // ---- plan facts -----------------------------------------------------------
@@ -866,14 +881,14 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   S.num_mtiles = d.n * S.ohb;
   // CTA pairs (cta_group::2, M = 256): each SM holds and reads half of every
   // B block. bf16/fp16 TMA plans with N a multiple of 16; more A stages fit.
-  // Opt-in (WF_CTA_PAIR=1): measured slower on B200 for these shapes -- the
-  // pair MMA saves only ~10% at N=64 and nothing at N>=128
-  // (tools/probes/pair_probe.cu) while the pair synchronisation costs more.
+  // Opt-in (pair_req 1): the pair MMA saves only ~10% at N=64 and nothing at
+  // N>=128 (tools/probes/pair_probe.cu) while the pair synchronisation costs
+  // more; halving B per SM did not pay for AlexNet either.
   {
-    const char* env = std::getenv("WF_CTA_PAIR");
-    bool pair = env != nullptr && env[0] == '1';
+    bool pair = pair_req == 1;
     pair = pair && in_dtype != WF_TF32 && (S.prod == 0 || S.prod == 3) && S.num_mtiles >= 2 && S.tps == 1;
     for (const MmaEntry& e : S.entries) pair = pair && (((e.meta >> 22) & 0x1FFu) * 8) % 16 == 0;
+    if (pair_req == 1 && !pair) return make_schedule_tps(d, f_req, gs_req, in_dtype, tps, out, err, kpair_req, 0);
     if (pair) {
       int64_t max_b = 0;
       for (const auto& t : S.ntiles) max_b = std::max(max_b, t.b_bytes / 2);
@@ -1036,7 +1051,7 @@ wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
   wf_status st = (p.variant == WF_VARIANT_UNFOLDED)
                      ? make_schedule_unfolded(d, static_cast<wf_dtype>(p.in_dtype), out, err)
                      : make_schedule(d, p.f, p.group_size, static_cast<wf_dtype>(p.in_dtype), out, err,
-                                     p.kstep_mode);
+                                     p.kstep_mode, p.cta_pair == 2 ? 1 : 0, p.stage_tiles);
   if (st != WF_OK) return st;
   if (out->plan.status != WF_FOLD_APPLY || out->plan.packed_bytes != p.packed_bytes ||
       out->plan.mma_entries != p.mma_entries) {

@@ -136,9 +136,11 @@ wf_status validate_desc(const wf_conv_desc& d, std::string* err);
 // Full planner. Returns WF_OK with plan.status == APPLY or FALLBACK (reason),
 // or an error status (shape problems, bad arguments).
 // kpair_req: -1 choose the K-step mode (cost model; WF_KPAIR=0/1 overrides),
-// 0 / 1 force 32-byte covers / cross-kh core-column pairs.
+// 0 / 1 force 32-byte covers / cross-kh core-column pairs. pair_req: -1 no CTA
+// pairs unless WF_CTA_PAIR=1, 0 / 1 force. tps_req: -1 auto, 1 / 2 M tiles per A stage.
 wf_status make_schedule(const wf_conv_desc& d, int64_t f, int64_t group_size,
-                        wf_dtype in_dtype, Schedule* out, std::string* err, int kpair_req = -1);
+                        wf_dtype in_dtype, Schedule* out, std::string* err, int kpair_req = -1,
+                        int pair_req = -1, int tps_req = -1);
 
 // The unfolded Cin=C variant of the same kernel (explicit im2col A tiles):
 // the fold-vs-unfolded comparison of the north star.

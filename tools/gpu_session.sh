@@ -15,3 +15,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:conv_fold -s 1 -c 1 --csv --log-file gpurun_out/traffic_r50_n8192.csv \
    python tools/prof_conv.py r50 8192 0 0 1 > gpurun_out/ncu_traffic.log 2>&1
 ls -la gpurun_out
+WF_KPAIR=1 timeout 200 python tools/power_probe.py 8192 3 0,-1,0x1100,0x1200,0x300 > gpurun_out/power.log 2>&1
+timeout 600 python tools/bench_configs.py --out gpurun_out/configs.json > gpurun_out/configs.log 2>&1
