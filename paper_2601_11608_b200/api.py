@@ -481,22 +481,54 @@ def gemm_ref(a, b):
     return _ret(y.reshape(M, N), host)
 
 
-def gemm_as_conv1x1(a, b):
-    """GEMM as a 1x1 conv over a (1,1,M,K) tensor (src/gemm.cpp:43-49)."""
-    return gemm_ref(a, b)
-
-
-def fold_tall_skinny(a, b, factor: int):
-    """GEMM through a width-folded 1x1 conv (src/gemm.cpp:51-69)."""
-    _check_factor(factor)
-    at, host = _as_tensor(a, torch.float32)
-    bt, _ = _as_tensor(b, torch.float32)
+def _gemm_operands(a, b, precision):
+    dtype = torch.float32 if precision in (None, "exact") else _PREC_DTYPE[precision]
+    at, host = _as_tensor(a, dtype)
+    bt, _ = _as_tensor(b, dtype)
     if at.dim() != 2 or bt.dim() != 2 or at.shape[1] != bt.shape[0]:
         raise ShapeMismatchError(f"gemm shapes {tuple(at.shape)} x {tuple(bt.shape)} do not chain")
+    return at.contiguous(), bt.contiguous(), host, dtype
+
+
+def gemm_as_conv1x1(a, b, *, precision: str | None = None, out_dtype: torch.dtype | None = None):
+    """GEMM as a 1x1 conv over a (1,M,1,K) tensor (src/gemm.cpp:43-49).
+
+    ``precision=None`` is the reference's exact k-inner fp32 order (bitwise
+    gemm_ref). ``"bf16"``/``"f16"`` run the UNFOLDED variant of the tcgen05
+    kernel (M row = output pixel = GEMM row), the baseline fold_tall_skinny beats.
+    """
+    if precision in (None, "exact"):
+        return gemm_ref(a, b)
+    at, bt, host, dtype = _gemm_operands(a, b, precision)
+    M, K = at.shape
+    N = bt.shape[1]
+    fc = FoldedConv2d(bt.reshape(1, 1, K, N), None, (1, M, 1, K), dtype=dtype, variant="unfolded")
+    y = fc(at.reshape(1, M, 1, K), bias=False, out_dtype=out_dtype)
+    return _ret(y.reshape(M, N), host)
+
+
+def fold_tall_skinny(a, b, factor: int, *, precision: str | None = None, out_dtype: torch.dtype | None = None):
+    """GEMM through a width-folded 1x1 conv (src/gemm.cpp:51-69).
+
+    A (M,K) is read as (1, M/F, F, K) and width-folded into (1, M/F, 1, F*K)
+    -- one row-major reshape, zero-copy on the device -- against the
+    block-diagonal expansion of B; C is the reshaped folded output.
+    ``precision=None`` evaluates it with the reference's exact fp32 conv
+    (bitwise = gemm_ref); ``"bf16"``/``"f16"``/``"tf32"`` run the folded
+    tcgen05 kernel with fold factor F (the expansion is packed once; C is
+    written straight into (M, N) row-major). Raises IllegalFoldError if
+    M % F != 0 (src/gemm.cpp:56-60).
+    """
+    _check_factor(factor)
+    at, bt, host, dtype = _gemm_operands(a, b, precision)
     M, K = at.shape
     N = bt.shape[1]
     if M % factor:
         raise IllegalFoldError(f"rows {M} not divisible by {factor}")
+    if precision not in (None, "exact"):
+        fc = FoldedConv2d(bt.reshape(1, 1, K, N), None, (1, M // factor, factor, K), dtype=dtype, fold=factor)
+        y = fc(at.reshape(1, M // factor, factor, K), bias=False, out_dtype=out_dtype)
+        return _ret(y.reshape(M, N), host)
     x_f = at.reshape(1, M // factor, 1, K * factor)  # (M,K) as (1,M/F,F,K), width-folded: one reshape
     w_f = expand_filter_general(bt.reshape(1, 1, K, N), factor)
     y_f = conv2d(x_f, w_f, precision="exact")

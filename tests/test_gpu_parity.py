@@ -290,6 +290,32 @@ def test_conv1d_and_gemm_routes(oracle):
     np.testing.assert_array_equal(wf.fold_tall_skinny(a, bm, 8), want)
 
 
+@pytest.mark.parametrize("M,K,N,F,prec", [(8192, 3, 64, 8, "bf16"), (8000, 3, 64, 8, "bf16"), (4096, 4, 64, 4, "bf16"),
+                                           (2048, 8, 128, 2, "f16"), (4096, 3, 64, 4, "tf32"),
+                                           (4096, 3, 32, 8, "bf16"), (1024, 16, 96, 1, "bf16")])
+def test_tall_skinny_gemm_on_tensor_cores(M, K, N, F, prec):
+    """fold_tall_skinny through the folded tcgen05 kernel (SURVEY 8.F-3,
+    src/gemm.cpp:51-69): exact on integer data (fp32 out), within the
+    precision's tolerance on real data; gemm_as_conv1x1 through the unfolded
+    variant of the same kernel."""
+    rng = np.random.default_rng(M + K + N)
+    a = rng.integers(-4, 5, (M, K)).astype(np.float32)
+    b = rng.integers(-4, 5, (K, N)).astype(np.float32)
+    want = a.astype(np.float64) @ b.astype(np.float64)
+    got = wf.fold_tall_skinny(a, b, F, precision=prec, out_dtype=torch.float32)
+    np.testing.assert_array_equal(got, want)
+    a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    dt = {"bf16": torch.bfloat16, "f16": torch.float16, "tf32": torch.float32}[prec]
+    aq, bq = (torch.from_numpy(v).to(dt).float().numpy().astype(np.float64) for v in (a, b))
+    got = wf.fold_tall_skinny(cuda(a, dt), cuda(b, dt), F, precision=prec)
+    assert got.is_cuda and tuple(got.shape) == (M, N)
+    assert normrel(got.float().cpu().numpy(), aq @ bq) <= (1e-3 if prec == "tf32" else 1e-2)
+    if prec != "tf32" and N % 32 == 0:
+        got = wf.gemm_as_conv1x1(a, b, precision=prec, out_dtype=torch.float32)
+        assert normrel(got, aq @ bq) <= 1e-2
+
+
 def test_no_cpu_fallback_on_cpu_tensors():
     conv = wf.FoldedConv2d(torch.randn(3, 3, 3, 16, device="cuda").bfloat16(), None, (1, 32, 32, 3), padding=1)
     with pytest.raises(ValueError):

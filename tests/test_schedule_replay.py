@@ -129,11 +129,12 @@ GEOMS = [  # (KH, KW, Cout, stride, pad, H, W, dtype)
     (11, 11, 96, 4, 0, 27, 35, "bf16"),   # AlexNet conv1 (W % f != 0)
     (3, 3, 32, 2, 1, 16, 32, "f16"),      # MobileNetV2 stem
     (7, 7, 64, 2, 3, 16, 32, "tf32"),     # R50 conv1, TF32 (f = 4)
+    (1, 1, 64, 1, 0, 300, 8, "bf16"),     # tall-skinny GEMM (M=2400, K=3, N=64) as a folded 1x1 conv
 ]
 
 
 @pytest.mark.parametrize("kpair", ["0", "1"])
-@pytest.mark.parametrize("geom", GEOMS, ids=["r50", "vgg", "alexnet", "mnv2", "r50_tf32"])
+@pytest.mark.parametrize("geom", GEOMS, ids=["r50", "vgg", "alexnet", "mnv2", "r50_tf32", "gemm"])
 def test_schedule_replay_exact(oracle, monkeypatch, geom, kpair):
     monkeypatch.setenv("WF_KPAIR", kpair)
     KH, KW, Co, s, p, H, W, dt = geom

@@ -76,6 +76,54 @@ def time_conv(conv, x, y, relu, iters, flush):
     return tot / iters
 
 
+def bench_gemm(iters, hbm):
+    """tall-skinny C = A B (M = 2^24 rows, K = 3, N = 64, bf16)
+    three ways -- fold_tall_skinny on the folded tcgen05 kernel (F = 8, one
+    M row = 8 GEMM rows), the unfolded variant of the same kernel
+    (gemm_as_conv1x1), and cuBLAS (torch.matmul) -- on resident HBM data."""
+    dev = torch.device("cuda", 0)
+    M, K, N, F = 1 << 24, 3, 64, 8
+    g = torch.Generator(device=dev).manual_seed(1008)
+    a = (torch.rand((M, K), generator=g, device=dev) * 2 - 1).bfloat16()
+    b = (torch.rand((K, N), generator=g, device=dev) * 2 - 1).bfloat16()
+    c = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+    ref = (a[:4096].double() @ b.double()).float().cpu().numpy()
+    bytes_min = (M * K + M * N) * 2
+    out = {"shape": {"m": M, "k": K, "n": N, "factor": F, "dtype": "bfloat16"}, "min_bytes": bytes_min}
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    fold = wf.FoldedConv2d(b.reshape(1, 1, K, N), None, (1, M // F, F, K), fold=F)
+    unf = wf.FoldedConv2d(b.reshape(1, 1, K, N), None, (1, M, 1, K), variant="unfolded")
+    for name, fn in (("fold_tall_skinny", lambda: fold(a.reshape(1, M // F, F, K), bias=False, out=c.reshape(1, M // F, F, N))),
+                     ("unfolded_conv1x1", lambda: unf(a.reshape(1, M, 1, K), bias=False, out=c.reshape(1, M, 1, N))),
+                     ("cublas_matmul", lambda: torch.matmul(a, b, out=c))):
+        try:
+            ms = timed(fn)
+            err = float(np.max(np.abs(c[:4096].float().cpu().numpy() - ref)) / np.max(np.abs(ref)))
+            out[name] = {"ms": ms, "rows_per_s": M / (ms / 1e3), "hbm_gbs": bytes_min / (ms / 1e3) / 1e9,
+                         "hbm_frac": bytes_min / (ms / 1e3) / 1e9 / hbm, "normwise_rel_err": err}
+        except Exception as e:  # report, keep going
+            out[name] = {"error": f"{type(e).__name__}: {e}"}
+    if "ms" in out["fold_tall_skinny"] and "ms" in out["cublas_matmul"]:
+        out["fold_speedup_vs_cublas"] = out["cublas_matmul"]["ms"] / out["fold_tall_skinny"]["ms"]
+    if "ms" in out["fold_tall_skinny"] and "ms" in out["unfolded_conv1x1"]:
+        out["fold_speedup_vs_unfolded"] = out["unfolded_conv1x1"]["ms"] / out["fold_tall_skinny"]["ms"]
+    print("tall_skinny_gemm", json.dumps({k: (round(v["ms"], 4) if isinstance(v, dict) and "ms" in v else v)
+                                          for k, v in out.items() if k != "shape"}), flush=True)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
@@ -151,6 +199,8 @@ def main():
                                 for k, v in res.items() if k not in ("shape",)}), flush=True)
         del x, y
         torch.cuda.empty_cache()
+    if not args.only or "gemm" in args.only:
+        results["tall_skinny_gemm"] = bench_gemm(args.iters, hbm)
     results["_peaks"] = {"hbm_gbs": hbm, "bf16_tflops": tc, "source": "MEASURED_PEAKS.json"}
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(results, open(args.out, "w"), indent=1)
