@@ -26,53 +26,78 @@
 
 namespace wfb {
 
-// Out row r, 16-byte chunk k = in row r bytes [16k, 16k+16), zero past rb_in.
-// In rows are only element-aligned: two aligned 16-byte loads + funnel shift.
-__global__ void repitch_kernel(const uint8_t* __restrict__ x, uint8_t* __restrict__ y, long long rows, int rb_in,
-                               int rb_out) {
-  const int cpr = rb_out / 16;
-  const long long total = rows * cpr;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / cpr;
-    const int k = static_cast<int>(i - r * cpr);
-    const int o = 16 * k;
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
-    if (o < rb_in) {
-      const uintptr_t addr = reinterpret_cast<uintptr_t>(x) + r * rb_in + o;
-      const uint32_t sh = static_cast<uint32_t>(addr & 15u);
-      const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(addr - sh));
-      uint32_t q[8] = {v0.x, v0.y, v0.z, v0.w, 0u, 0u, 0u, 0u};
-      if (sh != 0 && o + 16 - static_cast<int>(sh) < rb_in) {
-        const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(addr - sh + 16));
-        q[4] = v1.x; q[5] = v1.y; q[6] = v1.z; q[7] = v1.w;
+// One warp per row (grid-stride over rows). Lane L of a round owns output
+// chunk k = base + L = input-row bytes [16k, 16k+16): it loads the aligned
+// 16-byte chunk k of the row's aligned superset once (coalesced, 512 B per
+// warp-round), takes chunk k+1 from lane L+1 by shuffle (lane 31 loads it),
+// and funnel-shifts the pair by the row's misalignment -- every input byte is
+// read once and every output byte written once. Bytes past rb_in are zero.
+__device__ __forceinline__ uint32_t pick8(const uint32_t (&q)[8], int i) {
+  uint32_t v = q[0];
+#pragma unroll
+  for (int t = 1; t < 8; ++t) v = (i == t) ? q[t] : v;  // selects, no local-memory indexing
+  return v;
+}
+
+__global__ void __launch_bounds__(256) repitch_kernel(const uint8_t* __restrict__ x, uint8_t* __restrict__ y,
+                                                      long long rows, int rb_in, int rb_out) {
+  constexpr int kRounds = 4;  // rounds of 32 chunks loaded before any is stored (memory-level parallelism)
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const int cpr = rb_out >> 4;
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  for (long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+    const uintptr_t src = reinterpret_cast<uintptr_t>(x) + r * rb_in;
+    const uint4* a0 = reinterpret_cast<const uint4*>(src & ~static_cast<uintptr_t>(15));
+    const int sh = static_cast<int>(src & 15u);
+    const int nin = (sh + rb_in + 15) >> 4;  // aligned chunks that hold the row
+    uint8_t* dst = y + r * rb_out;
+    for (int s0 = 0; s0 < cpr; s0 += 32 * kRounds) {
+      uint4 c[kRounds];
+#pragma unroll
+      for (int j = 0; j < kRounds; ++j) {
+        const int k = s0 + 32 * j + lane;
+        c[j] = (k < nin) ? __ldg(a0 + k) : z;
       }
-      const int ws = sh >> 2, bs = (sh & 3) * 8;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t lo = q[j + ws], hi = (j + ws + 1 < 8) ? q[j + ws + 1] : 0u;
-        w[j] = bs ? __funnelshift_r(lo, hi, bs) : lo;
-      }
-      if (o + 16 > rb_in) {  // zero the bytes past the input row
+      for (int j = 0; j < kRounds; ++j) {
+        const int k = s0 + 32 * j + lane;
+        uint4 n;
+        n.x = __shfl_down_sync(0xffffffffu, c[j].x, 1);
+        n.y = __shfl_down_sync(0xffffffffu, c[j].y, 1);
+        n.z = __shfl_down_sync(0xffffffffu, c[j].z, 1);
+        n.w = __shfl_down_sync(0xffffffffu, c[j].w, 1);
+        if (lane == 31) n = (k + 1 < nin) ? __ldg(a0 + k + 1) : z;
+        if (k >= cpr) continue;
+        const uint32_t q[8] = {c[j].x, c[j].y, c[j].z, c[j].w, n.x, n.y, n.z, n.w};
+        const int ws = sh >> 2, bs = (sh & 3) * 8;
+        uint32_t w[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint32_t m = 0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-            if (o + 4 * j + b < rb_in) m |= 0xFFu << (8 * b);
-          w[j] &= m;
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t lo = pick8(q, t + ws), hi = pick8(q, t + ws + 1);
+          w[t] = bs ? __funnelshift_r(lo, hi, bs) : lo;
         }
+        const int o = 16 * k;
+        if (o + 16 > rb_in) {  // zero the bytes past the input row
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            uint32_t m = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (o + 4 * t + b < rb_in) m |= 0xFFu << (8 * b);
+            w[t] &= m;
+          }
+        }
+        *reinterpret_cast<uint4*>(dst + o) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
-    *reinterpret_cast<uint4*>(y + r * rb_out + o) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
 wf_status launch_repitch(const void* x, void* ws, long long rows, int rb_in, int rb_out, cudaStream_t st,
                          std::string* err) {
-  const long long total = rows * (rb_out / 16);
-  const int threads = 256;
-  const int blocks = static_cast<int>(std::min<long long>((total + threads - 1) / threads, 148LL * 16));
+  const int threads = 256;  // 8 warps, one row each at a time
+  const int blocks = static_cast<int>(std::min<long long>((rows + 7) / 8, 148LL * 8));
   repitch_kernel<<<blocks, threads, 0, st>>>(static_cast<const uint8_t*>(x), static_cast<uint8_t*>(ws), rows, rb_in,
                                              rb_out);
   const cudaError_t e = cudaGetLastError();
