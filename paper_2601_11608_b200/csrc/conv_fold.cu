@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -161,7 +162,14 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   }
   a.row_bytes = p.cout_f * oes;
   a.acc_stride = pow2ceil(max_cols);
-  a.tmem_cols = 2 * a.acc_stride;
+  // as many accumulator buffers as fit in the 512 TMEM columns (<= 4): the
+  // MMAs run further ahead of the epilogue when an N-tile is narrow (MNv2 128)
+  a.n_acc = (a.acc_stride <= 128) ? 4 : 2;
+  a.acc_shift = (a.n_acc == 4) ? 2 : 1;
+  if (const char* env = std::getenv("WF_NACC")) {
+    if (env[0] == '2') { a.n_acc = 2; a.acc_shift = 1; }
+  }
+  a.tmem_cols = a.n_acc * a.acc_stride;
   a.epi_flags = static_cast<int>(epilogue);
   // shared-memory carve-up (offsets from the 1024-aligned base)
   a.off_a = 1024;

@@ -65,6 +65,7 @@ struct ConvArgs {
   long long row_bytes;            // bytes of one folded output row = r*Cout*out_elem
   int chunk_col[kMaxNTiles][kMaxAccCols / 32];  // output column of each epilogue chunk
   unsigned acc_stride, tmem_cols;
+  int n_acc, acc_shift;           // accumulator buffers in TMEM (2 or 4) and log2 of it
   int epi_flags;
   int off_a, off_b, off_bias;
   // software-gather producer (kProd 1: folded layout, 2: explicit im2col)
@@ -492,13 +493,13 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t bar_full = base;          // [stages] x 8 B
   const uint32_t bar_empty = base + 64;    // [stages] x 8 B
-  const uint32_t bar_tfull = base + 128;   // [2] x 8 B
-  const uint32_t bar_tempty = base + 144;     // [2] x 8 B: lower half of the accumulator drained
-  const uint32_t bar_tempty_hi = base + 168;  // [2] x 8 B: upper half drained
+  const uint32_t bar_tfull = base + 384;      // [n_acc <= 4] x 8 B: accumulator written
+  const uint32_t bar_tempty = base + 416;     // [n_acc] x 8 B: lower half of the accumulator drained
+  const uint32_t bar_tempty_hi = base + 448;  // [n_acc] x 8 B: upper half drained
   const uint32_t bar_bpeer = base + 184;      // pair: the peer's B half landed (leader's barrier)
   const uint32_t bar_b = base + 160;
-  const uint32_t bar_raw_full = base + 256;   // [raw_slots <= 32] x 8 B
-  const uint32_t bar_raw_empty = base + 512;  // [raw_slots <= 32] x 8 B
+  const uint32_t bar_raw_full = base + 256;   // [raw_slots <= 16] x 8 B
+  const uint32_t bar_raw_empty = base + 512;  // [raw_slots <= 16] x 8 B
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + 192);
 
   // warp index via shuffle so the compiler knows it is warp-uniform (keeps the
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       mbar_init(bar_full + 8 * i, kProd == 0 ? 1 : kGatherWarps);  // TMA: one expect_tx; rows: one arrive per transposer
       mbar_init(bar_empty + 8 * i, 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < a.n_acc; ++i) {
       mbar_init(bar_tfull + 8 * i, 1);
       // every epilogue thread arrives (pair: one arrive per warp of both CTAs, on the leader's)
       mbar_init(bar_tempty + 8 * i, kPair == 2 ? 16 : 256);
@@ -728,8 +729,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     int tile = 0;
     for (int u = local; u < a.num_units; u += a.unit_stride, it0 += a.ksplit) {
      for (int k = 0; k < a.tps; ++k, ++tile) {  // tps M tiles share the unit's A stage
-      const int acc = tile & 1;
-      const uint32_t acc_round = static_cast<uint32_t>(tile >> 1);
+      const int acc = tile & (a.n_acc - 1);
+      const uint32_t acc_round = static_cast<uint32_t>(tile >> a.acc_shift);
       const int split = (a.ksplit == 1) ? a.nt_split[ntile] : -1;
       long long t0 = dbg ? clock64() : 0;
       mbar_wait(bar_tempty + 8 * acc, (acc_round & 1u) ^ 1u);
@@ -846,8 +847,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     for (int ut = local * a.tps; ut < a.num_units * a.tps; ++it_tile) {
       const int u = ut / a.tps, k = ut - u * a.tps;  // tile k of stage unit u
       ut = (k + 1 < a.tps) ? ut + 1 : (u + a.unit_stride) * a.tps;
-      const int acc = it_tile & 1;
-      const uint32_t acc_round = static_cast<uint32_t>(it_tile >> 1);
+      const int acc = it_tile & (a.n_acc - 1);
+      const uint32_t acc_round = static_cast<uint32_t>(it_tile >> a.acc_shift);
       const int mt = u * kPair + static_cast<int>(rank);  // (im2col rows; tps == 1 there)
       int n, oh0;
       tile_origin<kPair>(a, u, k, rank, n, oh0);
