@@ -818,7 +818,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     const bool skip_ld = (a.epi_flags & 0x800) != 0;
     const bool stream_st = (a.epi_flags & 0x100000) != 0;  // experiment: streaming store hints
     const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
-    float breg[CPW][VPT];   // bias of this thread's channels in each of its chunks
+    int boff[CPW];          // shared-memory bias index of this thread's channels in each of its chunks
     long long coff[CPW];    // byte offset of each chunk's first output column in a row
     int jsub[CPW];          // output sub-column j of this thread's channels (OW % r tail mask)
 #pragma unroll
@@ -827,31 +827,55 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       const int ocol = (c < nchunks) ? a.chunk_col[ntile][c] : col0;  // slot order -> output column
       coff[cc] = static_cast<long long>(ocol + VPT * k4) * sizeof(OutT);
       jsub[cc] = (ocol + VPT * k4) / a.Cout;
-#pragma unroll
-      for (int v = 0; v < VPT; ++v) breg[cc][v] = (c < nchunks) ? sbias[ocol - col0 + VPT * k4 + v] : 0.0f;
+      boff[cc] = (c < nchunks) ? ocol - col0 + VPT * k4 : 0;
     }
-    // the four M rows this thread stores: (16-lane half h16, row group r8)
-    int row_t[2][2], row_w[2][2];
+    // the four M rows this thread stores: (16-lane half h16, row group r8).
+    // Everything about them that does not depend on the tile is computed once:
+    // output row t of the tile, byte offset from the tile's first output pixel,
+    // tile-independent validity, and per chunk the OW % r tail mask.
+    int row_t[2][2];
+    long long row_off[2][2];
+    bool row_ok[2][2];
+    unsigned row_cc[2][2];  // bit cc: this row's channels of chunk cc exist (ow < OW)
 #pragma unroll
     for (int h16 = 0; h16 < 2; ++h16)
 #pragma unroll
       for (int r8 = 0; r8 < 2; ++r8) {
         const int m = quarter * 32 + h16 * 16 + r8 * 8 + (lane >> 2);
-        row_t[h16][r8] = m / a.Wbox;
-        row_w[h16][r8] = m - row_t[h16][r8] * a.Wbox;
+        const int t = m / a.Wbox, wq = m - t * a.Wbox;
+        row_t[h16][r8] = t;
+        row_off[h16][r8] = (static_cast<long long>(t) * a.OW + wq * a.r) * a.Cout * static_cast<long long>(sizeof(OutT));
+        row_ok[h16][r8] = (wq < a.Wfo) && (t < a.OHt) && !dbg_skip_store;
+        unsigned bits = 0;
+#pragma unroll
+        for (int cc = 0; cc < CPW; ++cc) bits |= (wq * a.r + jsub[cc] < a.OW) ? (1u << cc) : 0u;
+        row_cc[h16][r8] = bits;
       }
+    const long long img_bytes = static_cast<long long>(a.OH) * a.OW * a.Cout * static_cast<long long>(sizeof(OutT));
+    const long long orow_bytes = static_cast<long long>(a.OW) * a.Cout * static_cast<long long>(sizeof(OutT));
+    // (image, first output row) of the current stage unit, advanced without
+    // divisions: v = u (two-tile stages, divisor = units per image) or the M
+    // tile u*kPair + rank (one tile per stage, divisor = M tiles per image)
+    const int vdiv = (a.tps == 2) ? a.uph : a.ohb;
+    const int vstep = (a.tps == 2) ? a.unit_stride : a.unit_stride * kPair;
+    const int vq = vstep / vdiv, vr = vstep - (vstep / vdiv) * vdiv;
+    const int v0 = (a.tps == 2) ? local : local * kPair + static_cast<int>(rank);
+    int vn = v0 / vdiv, vrem = v0 - (v0 / vdiv) * vdiv;
     int it_tile = 0;
     // pair: arrivals go to the leader's accumulator-free barriers
     const uint32_t te_lo = (kPair == 2) ? mapa(bar_tempty, 0) : bar_tempty;
     const uint32_t te_hi = (kPair == 2) ? mapa(bar_tempty_hi, 0) : bar_tempty_hi;
-    for (int ut = local * a.tps; ut < a.num_units * a.tps; ++it_tile) {
-      const int u = ut / a.tps, k = ut - u * a.tps;  // tile k of stage unit u
-      ut = (k + 1 < a.tps) ? ut + 1 : (u + a.unit_stride) * a.tps;
+    for (int u = local; u < a.num_units; u += a.unit_stride) {
+     const int vn_u = vn, vrem_u = vrem;
+     vn += vq;
+     vrem += vr;
+     if (vrem >= vdiv) { vrem -= vdiv; ++vn; }
+     for (int k = 0; k < a.tps; ++k, ++it_tile) {  // tile k of stage unit u
       const int acc = it_tile & (a.n_acc - 1);
       const uint32_t acc_round = static_cast<uint32_t>(it_tile >> a.acc_shift);
       const int mt = u * kPair + static_cast<int>(rank);  // (im2col rows; tps == 1 there)
-      int n, oh0;
-      tile_origin<kPair>(a, u, k, rank, n, oh0);
+      const int n = vn_u;
+      const int oh0 = (a.tps == 2) ? (vrem_u * 2 + k) * a.OHt : vrem_u * a.OHt;
       mbar_wait(bar_tfull + 8 * acc, acc_round & 1u);
       tc_fence_after();
       if (dbg_skip_epi || n_it == 0) {
@@ -862,7 +886,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       }
       uint8_t* rowp[2][2];  // first output pixel of the row (its j = 0 sub-column)
       bool rowv[2][2];
-      int roww[2][2];       // first output column ow of the row
+      unsigned rowc[2][2];
+      uint8_t* const tile_out = a.out + n * img_bytes + oh0 * orow_bytes;
 #pragma unroll
       for (int h16 = 0; h16 < 2; ++h16)
 #pragma unroll
@@ -871,14 +896,11 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
             const long long P = static_cast<long long>(mt) * 128 + quarter * 32 + h16 * 16 + r8 * 8 + (lane >> 2);
             rowv[h16][r8] = (P < a.total_px) && !dbg_skip_store;
             rowp[h16][r8] = a.out + P * a.row_bytes;
-            roww[h16][r8] = 0;
+            rowc[h16][r8] = ~0u;
           } else {
-            const int t = row_t[h16][r8], wq = row_w[h16][r8];
-            const int oh = oh0 + t;
-            rowv[h16][r8] = (wq < a.Wfo) && (t < a.OHt) && (oh < a.OH) && (n < a.n_img) && !dbg_skip_store;
-            roww[h16][r8] = wq * a.r;
-            rowp[h16][r8] = a.out + ((static_cast<long long>(n) * a.OH + oh) * a.OW + wq * a.r) * a.Cout *
-                                        static_cast<long long>(sizeof(OutT));
+            rowv[h16][r8] = row_ok[h16][r8] && (oh0 + row_t[h16][r8] < a.OH) && (n < a.n_img);
+            rowp[h16][r8] = tile_out + row_off[h16][r8];
+            rowc[h16][r8] = row_cc[h16][r8];
           }
         }
       const uint32_t tq = tmem_base + acc * a.acc_stride + (static_cast<uint32_t>(quarter * 32) << 16);
@@ -897,19 +919,25 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         if (it + 1 < n_it) tmem_ld_16x256b<NREG>(taddr(it + 1), buf[(it + 1) & 1], skip_ld);
         const int cc = it >> 1, h16 = it & 1;
         const uint32_t(&r)[NREG] = buf[it & 1];
+        float bb[VPT];  // bias of this thread's VPT channels (16-byte shared loads; registers are tight)
+#pragma unroll
+        for (int q = 0; q < VPT / 4; ++q) {
+          const float4 t4 = reinterpret_cast<const float4*>(sbias + boff[cc])[q];
+          bb[4 * q] = t4.x; bb[4 * q + 1] = t4.y; bb[4 * q + 2] = t4.z; bb[4 * q + 3] = t4.w;
+        }
 #pragma unroll
         for (int r8 = 0; r8 < 2; ++r8) {
           float v[VPT];
 #pragma unroll
           for (int i = 0; i < CH / 8; ++i) {
-            v[2 * i] = __uint_as_float(r[4 * i + 2 * r8]) + breg[cc][2 * i];
-            v[2 * i + 1] = __uint_as_float(r[4 * i + 2 * r8 + 1]) + breg[cc][2 * i + 1];
+            v[2 * i] = __uint_as_float(r[4 * i + 2 * r8]) + bb[2 * i];
+            v[2 * i + 1] = __uint_as_float(r[4 * i + 2 * r8 + 1]) + bb[2 * i + 1];
           }
           if (relu) {
 #pragma unroll
             for (int k = 0; k < VPT; ++k) v[k] = (v[k] < 0.0f) ? 0.0f : v[k];
           }
-          if (rowv[h16][r8] && roww[h16][r8] + jsub[cc] < a.OW) {
+          if (rowv[h16][r8] && ((rowc[h16][r8] >> cc) & 1u)) {
             if (stream_st) store_row<OutT, VPT, true>(rowp[h16][r8] + coff[cc], v);
             else store_row<OutT, VPT, false>(rowp[h16][r8] + coff[cc], v);
           }
@@ -921,6 +949,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       }
       tc_fence_before();
       arrive_at<kPair>(te_hi + 8 * acc);
+     }
     }
   }
 
