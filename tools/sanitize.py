@@ -1,5 +1,6 @@
 """Small shapes of every producer / epilogue variant, for compute-sanitizer
 (memcheck / racecheck / synccheck). Prints the normwise error vs torch's conv."""
+import os
 import sys
 import torch
 import torch.nn.functional as F
@@ -15,7 +16,8 @@ CASES = [  # n, h, w, kh, cout, s, p, dtype, relu, variant
     (2, 24, 32, 7, 64, 2, 3, torch.bfloat16, False, "unfolded"),   # row producer, im2col
     (2, 31, 31, 11, 96, 4, 0, torch.bfloat16, False, "unfolded"),
 ]
-for (n, h, w_, kh, co, s, p, dt, relu, var) in CASES:
+for kp, (n, h, w_, kh, co, s, p, dt, relu, var) in [(k, c) for k in ("0", "1") for c in CASES]:
+    os.environ["WF_KPAIR"] = kp  # both K-step schedules
     x = torch.randn(n, h, w_, 3, device="cuda").to(dt)
     w = (torch.randn(kh, kh, 3, co, device="cuda") * 0.1).to(dt)
     b = torch.randn(co, device="cuda")
@@ -31,7 +33,12 @@ for (n, h, w_, kh, co, s, p, dt, relu, var) in CASES:
         if relu:
             ref = ref.clamp_min(0)
         err = ((y - ref).abs().max() / ref.abs().max()).item()
-        print(f"{var:9s} {str(dt):14s} {kh}x{kh}/s{s}/p{p} flags={flags:#x} normwise err {err:.2e}", flush=True)
+        print(f"kpair={kp} {var:9s} {str(dt):14s} {kh}x{kh}/s{s}/p{p} flags={flags:#x} normwise err {err:.2e}", flush=True)
         assert err < 2e-2
+a = torch.randn(3000 * 8, 3, device="cuda").bfloat16()  # tall-skinny GEMM on the folded kernel
+bm = torch.randn(3, 64, device="cuda").bfloat16()
+c = wf.fold_tall_skinny(a, bm, 8, precision="bf16").float()
+ref = a.float() @ bm.float()
+assert ((c - ref).abs().max() / ref.abs().max()).item() < 2e-2
 torch.cuda.synchronize()
 print("sanitize cases ok")
