@@ -115,11 +115,20 @@ def test_tensor_core_conv_configs_within_tolerance(golden_configs, name):
     assert err <= TOL[dt], f"{name}: normwise rel {err:.3e} > {TOL[dt]} (plan {conv.device_plan})"
 
 
-@pytest.mark.parametrize("kpair", ["0", "1"])
+VARIANT_ENVS = [
+    {"WF_KPAIR": "0"}, {"WF_KPAIR": "1"},          # 32-byte covers / cross-kh core-column pairs
+    {"WF_CTA_PAIR": "1"},                           # cta_group::2 pairs (opt-in)
+    {"WF_TPS": "1"},                                # one M tile per A stage
+    {"WF_NACC": "2"},                               # two accumulator buffers
+]
+
+
+@pytest.mark.parametrize("env", VARIANT_ENVS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 @pytest.mark.parametrize("name", list(CONFIG_GEOM))
-def test_tensor_core_conv_integer_data_exact(golden_configs, name, kpair, monkeypatch):
-    """Both K-step schedules (32-byte covers / cross-kh core-column pairs) are exact on integers."""
-    monkeypatch.setenv("WF_KPAIR", kpair)
+def test_tensor_core_conv_integer_data_exact(golden_configs, name, env, monkeypatch):
+    """Every schedule / pipeline variant of the kernel is exact on integer data."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     y, ref, dt, conv = _config_run(golden_configs, name, "i", out_dtype=torch.float32)
     np.testing.assert_array_equal(y, ref, err_msg=f"{name} plan {conv.device_plan}")
 
