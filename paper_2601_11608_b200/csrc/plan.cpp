@@ -221,6 +221,18 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf
   if (pair_req == 1) return make_schedule_tps(d, f_req, gs_req, in_dtype, 1, out, err, kpair_req, 1);
   Schedule s1;
   wf_status st = make_schedule_tps(d, f_req, gs_req, in_dtype, 1, &s1, err, kpair_req, 0);
+  if (st == WF_OK && s1.plan.status != WF_FOLD_APPLY && s1.plan.reason == WF_REASON_NOT_PROFITABLE &&
+      pair_req < 0) {
+    // B too large for one SM's shared memory: CTA pairs hold half of it each
+    // (e.g. AlexNet zero-padded to Cin = 8, B = 270 KB)
+    Schedule sp;
+    std::string e2;
+    if (make_schedule_tps(d, f_req, gs_req, in_dtype, 1, &sp, &e2, kpair_req, 1) == WF_OK &&
+        sp.plan.status == WF_FOLD_APPLY && sp.pair == 2) {
+      *out = std::move(sp);
+      return WF_OK;
+    }
+  }
   if (st != WF_OK || s1.plan.status != WF_FOLD_APPLY) {
     *out = std::move(s1);
     return st;

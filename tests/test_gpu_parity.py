@@ -325,6 +325,27 @@ def test_tall_skinny_gemm_on_tensor_cores(M, K, N, F, prec):
         assert normrel(got, aq @ bq) <= 1e-2
 
 
+@pytest.mark.parametrize("geom", [(7, 64, 2, 3, 40), (3, 64, 1, 1, 32), (11, 96, 4, 0, 67), (3, 32, 2, 1, 32)],
+                         ids=["r50", "vgg", "alexnet", "mnv2"])
+def test_zero_padded_cin8_variant_exact(oracle, geom):
+    """The zero-pad Cin 3 -> 8 comparison variant (the north star's baseline)
+    equals the Cin = 3 oracle on integer data; AlexNet's (B = 190 KB) runs on
+    CTA pairs, each SM holding half of B."""
+    K, Co, s, p, hw = geom
+    rng = np.random.default_rng(K * 100 + Co)
+    x = rng.integers(-4, 5, (3, hw, hw, 3)).astype(np.float32)
+    w = rng.integers(-4, 5, (K, K, 3, Co)).astype(np.float32)
+    x8 = np.zeros((3, hw, hw, 8), np.float32)
+    x8[..., :3] = x
+    w8 = np.zeros((K, K, 8, Co), np.float32)
+    w8[:, :, :3] = w
+    conv = wf.FoldedConv2d(cuda(w8, torch.bfloat16), None, x8.shape, stride=s, padding=p, dtype=torch.bfloat16)
+    y = conv(cuda(x8, torch.bfloat16), out_dtype=torch.float32)
+    np.testing.assert_array_equal(y.cpu().numpy(), oracle.conv_padded(x, w, None, s, p))
+    if K == 11:
+        assert conv.device_plan["cta_pair"] == 2
+
+
 def test_no_cpu_fallback_on_cpu_tensors():
     conv = wf.FoldedConv2d(torch.randn(3, 3, 3, 16, device="cuda").bfloat16(), None, (1, 32, 32, 3), padding=1)
     with pytest.raises(ValueError):
