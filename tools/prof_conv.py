@@ -1,4 +1,5 @@
-"""Run one configured conv a few times (for ncu capture). Usage: prof_conv.py CONFIG [n] [f] [gs]"""
+"""Run one configured conv a few times (for ncu capture).
+Usage: prof_conv.py CONFIG [n] [f] [gs] [iters] [flags] [variant: fold|unfolded]"""
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -19,7 +20,8 @@ gs = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 x = torch.randn(n, h, w_, c, device="cuda").to(dt)
 w = (torch.randn(kh, kw, c, cout, device="cuda") * 0.1).to(dt)
 b = torch.randn(cout, device="cuda")
-ff = wf.FoldedConv2d(w, b, x.shape, stride=s, padding=p, fold=f, group_size=gs)
+variant = sys.argv[7] if len(sys.argv) > 7 else "fold"
+ff = wf.FoldedConv2d(w, b, x.shape, stride=s, padding=p, fold=f, group_size=gs, variant=variant)
 y = ff(x, relu=relu)
 iters = int(sys.argv[5]) if len(sys.argv) > 5 else 3
 flags = int(sys.argv[6], 0) if len(sys.argv) > 6 else 0
