@@ -542,7 +542,12 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
         kp += c;
         g0 = g1;
       }
-      use = kp < legacy;
+      // a legacy cover that straddles folded pixels needs the shifted A region
+      // (one more TMA box per residue, ~1/Q more pieces): charge it 10%
+      bool straddle = false;
+      for (int64_t g = 0; g < G; ++g)
+        for (int64_t st : U[g]) straddle = straddle || (st % Q == Q - 1);
+      use = kp * 10 < legacy * (straddle ? 11 : 10);
     }
     S.kpair = use;
   }
