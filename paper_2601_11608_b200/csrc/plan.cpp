@@ -614,6 +614,10 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     return true;
   };
   const int pr = (pair_req == 1) ? 2 : 1;  // CTA pairs: each SM holds half of every B block
+  // Latency-bound launches (fewer M tiles than half the SMs, e.g. batch 1):
+  // one group per N-tile multiplies the CTAs and shrinks the B each one loads.
+  const int64_t mtiles_est = d.n * ceil_div(OH, OHt);
+  const int64_t max_tile_cols = (mtiles_est * 2 <= 148 && G > 1) ? S.Ng : kMaxAccCols;
   int64_t b_budget = 128 * 1024 * pr;
   for (int attempt = 0; attempt < 8; ++attempt) {
     S.ntiles.clear();
@@ -623,7 +627,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
       NTile t{};
       t.g0 = static_cast<int>(g);
       int64_t cols = 0, bytes = 0;
-      while (g < G && cols + S.Ng <= kMaxAccCols && tile_b_bytes(t.g0, g + 1) <= b_budget) {
+      while (g < G && cols + S.Ng <= max_tile_cols && tile_b_bytes(t.g0, g + 1) <= b_budget) {
         cols += S.Ng;
         ++g;
         bytes = tile_b_bytes(t.g0, g);
