@@ -715,6 +715,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // The whole warp walks the (warp-uniform) schedule so descriptors live in
     // uniform registers straight from the constant bank; one lane issues.
     const bool skip_mma = (a.epi_flags & 0x100) != 0;  // profiling switch
+    const bool no_wait = (a.epi_flags & 0x200000) != 0;  // profiling: issue the schedule back to back (with 0x1200)
     const uint32_t b_lo = (base + a.off_b) >> 4;
     const uint32_t a_hi = a.a_desc_hi;
     const bool leader = elect_one() && rank == 0;  // pair: the leader CTA issues for both SMs
@@ -733,8 +734,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       const uint32_t acc_round = static_cast<uint32_t>(tile >> a.acc_shift);
       const int split = (a.ksplit == 1) ? a.nt_split[ntile] : -1;
       long long t0 = dbg ? clock64() : 0;
-      mbar_wait(bar_tempty + 8 * acc, (acc_round & 1u) ^ 1u);
-      if (split < 0) mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
+      if (!no_wait) {
+        mbar_wait(bar_tempty + 8 * acc, (acc_round & 1u) ^ 1u);
+        if (split < 0) mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
+      }
       if (dbg) { const long long t1 = clock64(); w_acc += t1 - t0; t0 = t1; }
       const uint32_t d_base = tmem_base + acc * a.acc_stride;
       for (int ks = 0; ks < a.ksplit; ++ks) {
@@ -743,7 +746,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         const uint32_t round = static_cast<uint32_t>(it / a.stages);
         const int e0 = (a.ksplit == 1) ? a.nt_entry0[ntile] : a.ks_entry0[ks];
         const int entries = (a.ksplit == 1) ? a.nt_entries[ntile] : a.ks_entries[ks];
-        if (k == 0) mbar_wait(bar_full + 8 * stage, round & 1u);
+        if (k == 0 && !no_wait) mbar_wait(bar_full + 8 * stage, round & 1u);
         if (dbg) { const long long t1 = clock64(); w_full += t1 - t0; t0 = t1; }
         tc_fence_after();
         const uint32_t a_lo = (base + a.off_a + stage * a.stage_bytes + k * a.tile_shift) >> 4;
@@ -757,7 +760,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
               if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
             }
             if (dbg) t0 = clock64();
-            mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
+            if (!no_wait) mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
             if (dbg) w_hi += clock64() - t0;
             tc_fence_after();
           }
