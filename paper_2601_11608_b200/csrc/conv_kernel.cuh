@@ -764,23 +764,20 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
             if (dbg) w_hi += clock64() - t0;
             tc_fence_after();
           }
-          // Groups of 8: a group's table words are all loaded (uniform
-          // constant loads; the last group's index clamped) before its first
-          // MMA, so each group exposes one constant-load latency -- a rolled
-          // tail exposed one per MMA.
-          for (; i < entries; i += 8) {
-            uint4 ev[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) ev[j] = a.table[e0 + min(i + j, entries - 1)];
+          for (; i + 8 <= entries; i += 8) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              if (i + j < entries) {
-                const uint64_t adesc = (static_cast<uint64_t>(a_hi) << 32) | (ev[j].x + a_lo);
-                const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (ev[j].y + b_lo);
-                if (leader)
-                  issue_mma<kKind, kPair>(d_base + ev[j].w, adesc, bdesc, ev[j].z & 0x7FFFFFFFu, ev[j].z >> 31);
-              }
+              const uint4 e = a.table[e0 + i + j];
+              const uint64_t adesc = (static_cast<uint64_t>(a_hi) << 32) | (e.x + a_lo);
+              const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
+              if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
             }
+          }
+          for (; i < entries; ++i) {
+            const uint4 e = a.table[e0 + i];
+            const uint64_t adesc = (static_cast<uint64_t>(a_hi) << 32) | (e.x + a_lo);
+            const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
+            if (leader) issue_mma<kKind, kPair>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
           }
         }
         else if (split > 0) {
