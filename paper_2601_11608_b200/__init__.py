@@ -6,7 +6,10 @@ re-designed for sm_100a (TMA + tcgen05 + TMEM). Same public names as
 /root/reference/proj/python/widthfold/__init__.py:5-49.
 """
 from .api import (  # noqa: F401
+    BlobSizeMismatchError,
     DegenerateOutputError,
+    IoFailureError,
+    ManifestParseError,
     FoldedConv2d,
     Graph,
     MissingInputError,
@@ -35,10 +38,14 @@ from .api import (  # noqa: F401
     interpret,
     mac_report,
     plan_fold,
+    read_bundle,
+    read_graph,
     reconstruct_output,
     replicate_bias,
     unfold_input_general,
     width_fold_pass,
+    write_bundle,
+    write_graph,
 )
 from .api import __all__  # noqa: F401
 

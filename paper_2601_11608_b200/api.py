@@ -580,6 +580,59 @@ def interpret(graph: Graph, inputs: dict, mode: str = "device") -> dict:
 ShapeInferenceFailureError = _core.ShapeInferenceFailureError
 MissingInputError = _core.MissingInputError
 
+
+# ------------------------------------------- model format: bundles + graph JSON (8.F-4)
+ManifestParseError = _core.ManifestParseError
+BlobSizeMismatchError = _core.BlobSizeMismatchError
+IoFailureError = _core.IoFailureError
+
+
+def read_bundle(manifest_path) -> dict:
+    """Tensor bundle (manifest + raw little-endian blobs, docs/model_format.md;
+    include/widthfold/bundle.hpp:32-36) -> {name: array} in manifest order.
+    ``f32``/``f16`` come back as numpy arrays, ``bf16`` as CPU torch tensors;
+    bit patterns (signed zeros, subnormals, NaN payloads) are preserved."""
+    out = {}
+    for name, shape, dtype, raw in _core.read_bundle(str(manifest_path)):
+        if dtype == "bf16":
+            bits = np.frombuffer(raw, dtype="<u2").astype(np.int16).reshape(shape)
+            out[name] = torch.from_numpy(bits.copy()).view(torch.bfloat16)
+        else:
+            out[name] = np.frombuffer(raw, dtype="<f4" if dtype == "f32" else "<f2").reshape(shape).copy()
+    return out
+
+
+def _bundle_entry(name, v):
+    if isinstance(v, torch.Tensor):
+        v = v.detach().cpu().contiguous()
+        if v.dtype == torch.bfloat16:
+            return (name, list(v.shape), "bf16", v.view(torch.int16).numpy().astype("<i2").tobytes())
+        v = v.numpy()
+    a = np.ascontiguousarray(v)
+    if a.dtype == np.float16:
+        return (name, list(a.shape), "f16", a.astype("<f2").tobytes())
+    if a.dtype != np.float32:
+        a = a.astype(np.float32)
+    return (name, list(a.shape), "f32", a.astype("<f4").tobytes())
+
+
+def write_bundle(manifest_path, tensors: dict) -> None:
+    """Write ``tensors`` ({name: array}; float32 / float16 numpy or torch, or
+    torch bfloat16) as a manifest plus ``<stem>.bin`` (bundle.hpp:38-40)."""
+    _core.write_bundle(str(manifest_path), [_bundle_entry(k, v) for k, v in tensors.items()])
+
+
+def read_graph(path) -> Graph:
+    """Graph JSON + its weights bundle (include/widthfold/graph.hpp:68-70); the
+    constants load as float32 graph values whatever their bundle dtype."""
+    nodes, weights = _core.read_graph(str(path))
+    return Graph(nodes, weights)
+
+
+def write_graph(graph: Graph, path) -> None:
+    """Graph JSON plus ``<stem>.weights.json``/``.bin`` beside it (src/graph.cpp:315-339)."""
+    _core.write_graph(graph.nodes, graph.weights, str(path))
+
 __all__ = [
     "apply_width_fold", "apply_width_fold_general", "bias_add", "check_legality", "choose_fold_factor",
     "conv1d_h", "conv2d", "count_macs", "expand_filter", "expand_filter_general", "fold_input",
@@ -589,4 +642,6 @@ __all__ = [
     "FoldedConv2d", "expand_filter_folded", "plan_fold", "ShapeMismatchError", "IllegalFoldError",
     "DegenerateOutputError", "NotBlockDiagonalError", "UnsupportedError",
     "Graph", "width_fold_pass", "interpret", "ShapeInferenceFailureError", "MissingInputError",
+    "read_bundle", "write_bundle", "read_graph", "write_graph", "ManifestParseError", "BlobSizeMismatchError",
+    "IoFailureError",
 ]

@@ -14,6 +14,7 @@
 #include <pybind11/numpy.h>
 
 #include "graph.hpp"
+#include "model_io.hpp"
 #include "widthfold.hpp"
 
 namespace py = pybind11;
@@ -262,6 +263,52 @@ PYBIND11_MODULE(_core, m) {
       },
       py::arg("w"), py::arg("dense_shape"), py::arg("groups"), py::arg("scratch"), py::arg("stream"));
 
+  // ---- model format: tensor bundles + graph JSON (model_io.hpp) ----
+  py::register_exception<wf::ManifestParse>(m, "ManifestParseError", PyExc_ValueError);
+  py::register_exception<wf::BlobSizeMismatch>(m, "BlobSizeMismatchError", PyExc_ValueError);
+  py::register_exception<wf::IoFailure>(m, "IoFailureError", PyExc_OSError);
+  m.def(
+      "read_bundle",
+      [](const std::string& path) {
+        const wf::TensorBundle b = wf::read_bundle(path);
+        py::list out;
+        for (const auto& [name, t] : b.entries())
+          out.append(py::make_tuple(name, t.shape, t.dtype,
+                                    py::bytes(reinterpret_cast<const char*>(t.bytes.data()), t.bytes.size())));
+        return out;
+      },
+      py::arg("manifest_path"), "[(name, shape, dtype, little-endian bytes)] in manifest order (bundle.hpp:32-36).");
+  m.def(
+      "write_bundle",
+      [](const std::string& path, const py::list& entries) {
+        wf::TensorBundle b;
+        for (auto h : entries) {
+          const py::tuple e = h.cast<py::tuple>();
+          wf::BundleTensor t;
+          t.shape = e[1].cast<wf::Shape>();
+          t.dtype = e[2].cast<std::string>();
+          const std::string raw = e[3].cast<std::string>();
+          t.bytes.assign(raw.begin(), raw.end());
+          b.add(e[0].cast<std::string>(), std::move(t));
+        }
+        wf::write_bundle(b, path);
+      },
+      py::arg("manifest_path"), py::arg("entries"), "Write a manifest + <stem>.bin blob (bundle.hpp:38-40).");
+  m.def(
+      "read_graph",
+      [](const std::string& path) {
+        const wf::Graph g = wf::read_graph(path);
+        py::dict w;
+        for (const auto& kv : g.weights) w[py::str(kv.first)] = to_array(kv.second);
+        return py::make_tuple(nodes_of(g), w);
+      },
+      py::arg("path"), "Graph JSON + its weights bundle (graph.hpp:68-70).");
+  m.def(
+      "write_graph",
+      [](const py::list& nodes, const py::dict& weights, const std::string& path) {
+        wf::write_graph(graph_of(nodes, weights), path);
+      },
+      py::arg("nodes"), py::arg("weights"), py::arg("path"));
   py::register_exception<wf::ShapeInferenceFailure>(m, "ShapeInferenceFailureError", PyExc_ValueError);
   py::register_exception<wf::MissingInput>(m, "MissingInputError", PyExc_ValueError);
 
