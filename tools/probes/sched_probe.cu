@@ -77,11 +77,16 @@ __global__ void __launch_bounds__(128, 1) probe_reg(const __grid_constant__ Tab 
                                                    unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tslot;
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar, bar2, bar3;
   const int warp = threadIdx.x >> 5;
   const uint32_t base = (smem_u32(smem) + 1023) & ~1023u;
   for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) ((uint32_t*)smem)[i] = 0x3c003c00u;
-  if (threadIdx.x == 0) { mbar_init(smem_u32(&bar), 1); fence_barrier_init(); }
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    mbar_init(smem_u32(&bar2), 1);
+    mbar_init(smem_u32(&bar3), 1);
+    fence_barrier_init();
+  }
   if (warp == 0) tmem_alloc(smem_u32(&tslot), 512);
   asm volatile("fence.proxy.async.shared::cta;");
   tc_fence_before(); __syncthreads(); tc_fence_after();
@@ -108,6 +113,8 @@ __global__ void __launch_bounds__(128, 1) probe_reg(const __grid_constant__ Tab 
 #pragma unroll
       for (int i = 0; i < NE; ++i)
         if (leader) mma<0>(tmem + dcol + col[i], ad[i], bd[i], id[i], 1u);
+      if (mode >= 5 && leader) mma_commit(smem_u32(&bar2));        // per-tile commit (nobody waits)
+      if (mode == 6 && leader && (it & 1)) mma_commit(smem_u32(&bar3));  // + a per-stage commit
     }
     if (leader) mma_commit(smem_u32(&bar));
     __syncwarp();
@@ -142,7 +149,7 @@ int main(int argc, char** argv) {
     printf("mode %d %-20s %8.1f cycles/tile (max over SMs)\n", mode, names[mode], (double)mx / iters);
   }
   if (t.n == 21 || t.n == 28) {
-    for (int mode : {0, 3}) {
+    for (int mode : {0, 3, 5, 6}) {
       if (t.n == 21) {
         cudaFuncSetAttribute(probe_reg<21>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
         probe_reg<21><<<148, 128, 210 * 1024>>>(t, mode, iters, d);
@@ -155,8 +162,8 @@ int main(int argc, char** argv) {
       std::vector<unsigned long long> h(148);
       cudaMemcpy(h.data(), d, 8 * 148, cudaMemcpyDeviceToHost);
       unsigned long long mx = 0; for (auto v : h) mx = v > mx ? v : mx;
-      printf("registers, mode %d %-14s %8.1f cycles/tile (max over SMs)\n", mode, mode ? "all N = 256" : "as planned",
-             (double)mx / iters);
+      const char* nm = mode == 0 ? "as planned" : mode == 3 ? "all N = 256" : mode == 5 ? "+commit/tile" : "+commit/tile+stage";
+      printf("registers, mode %d %-20s %8.1f cycles/tile (max over SMs)\n", mode, nm, (double)mx / iters);
     }
   }
   return 0;
