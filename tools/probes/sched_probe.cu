@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(128, 1) probe_reg(const __grid_constant__ Tab 
   if (wu == 1) {
     const uint32_t a0 = base, b0 = base + 96 * 1024;
     uint64_t ad[NE], bd[NE];
-    uint32_t id[NE], col[NE];
+    uint32_t id[NE], col[NE], accf[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       const Ent e = t.e[i];
@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(128, 1) probe_reg(const __grid_constant__ Tab 
       ad[i] = desc(a0 + e.a_off, e.lbo, 128);
       bd[i] = desc(b0 + e.b_off, n * 16, 128);
       col[i] = (mode == 3) ? 0u : e.col;
+      accf[i] = e.acc;
     }
     const bool leader = elect_one();
     __syncwarp();
@@ -111,9 +112,14 @@ __global__ void __launch_bounds__(128, 1) probe_reg(const __grid_constant__ Tab 
     for (int it = 0; it < iters; ++it) {
       const uint32_t dcol = (it & 1) * 256;
 #pragma unroll
-      for (int i = 0; i < NE; ++i)
-        if (leader) mma<0>(tmem + dcol + col[i], ad[i], bd[i], id[i], 1u);
-      if (mode >= 5 && leader) mma_commit(smem_u32(&bar2));        // per-tile commit (nobody waits)
+      for (int i = 0; i < NE; ++i) {
+        if (mode == 7) {  // accumulate flag from a runtime per-entry value (as the kernel's table carries it)
+          if (leader) mma<0>(tmem + dcol + col[i], ad[i], bd[i], id[i], accf[i] | static_cast<uint32_t>(it > 0));
+        } else {
+          if (leader) mma<0>(tmem + dcol + col[i], ad[i], bd[i], id[i], 1u);
+        }
+      }
+      if (mode == 5 || mode == 6) { if (leader) mma_commit(smem_u32(&bar2)); }  // per-tile commit (nobody waits)
       if (mode == 6 && leader && (it & 1)) mma_commit(smem_u32(&bar3));  // + a per-stage commit
     }
     if (leader) mma_commit(smem_u32(&bar));
@@ -149,7 +155,7 @@ int main(int argc, char** argv) {
     printf("mode %d %-20s %8.1f cycles/tile (max over SMs)\n", mode, names[mode], (double)mx / iters);
   }
   if (t.n == 21 || t.n == 28) {
-    for (int mode : {0, 3, 5, 6}) {
+    for (int mode : {0, 3, 5, 6, 7}) {
       if (t.n == 21) {
         cudaFuncSetAttribute(probe_reg<21>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
         probe_reg<21><<<148, 128, 210 * 1024>>>(t, mode, iters, d);
@@ -162,7 +168,7 @@ int main(int argc, char** argv) {
       std::vector<unsigned long long> h(148);
       cudaMemcpy(h.data(), d, 8 * 148, cudaMemcpyDeviceToHost);
       unsigned long long mx = 0; for (auto v : h) mx = v > mx ? v : mx;
-      const char* nm = mode == 0 ? "as planned" : mode == 3 ? "all N = 256" : mode == 5 ? "+commit/tile" : "+commit/tile+stage";
+      const char* nm = mode == 0 ? "as planned" : mode == 3 ? "all N = 256" : mode == 5 ? "+commit/tile" : mode == 6 ? "+commit/tile+stage" : "runtime acc flag";
       printf("registers, mode %d %-20s %8.1f cycles/tile (max over SMs)\n", mode, nm, (double)mx / iters);
     }
   }
