@@ -170,6 +170,10 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     if (env[0] == '2') { a.n_acc = 2; a.acc_shift = 1; }
   }
   a.tmem_cols = a.n_acc * a.acc_stride;
+  // epilogue ping-pong for a single narrow N-tile (MNv2: 128 columns, +3%);
+  // wider tiles lose with it (R50 -13%, VGG -25%). WF_EPI_PP=0/1 overrides.
+  a.epi_pp = (max_cols <= 128 && a.n_tiles == 1 && S.pair == 1) ? 1 : 0;
+  if (const char* env = std::getenv("WF_EPI_PP")) a.epi_pp = (env[0] == '1' && S.pair == 1) ? 1 : 0;
   a.epi_flags = static_cast<int>(epilogue);
   // shared-memory carve-up (offsets from the 1024-aligned base)
   a.off_a = 1024;

@@ -66,6 +66,7 @@ struct ConvArgs {
   int chunk_col[kMaxNTiles][kMaxAccCols / 32];  // output column of each epilogue chunk
   unsigned acc_stride, tmem_cols;
   int n_acc, acc_shift;           // accumulator buffers in TMEM (2 or 4) and log2 of it
+  int epi_pp;                     // epilogue ping-pong: warp groups alternate tiles
   int epi_flags;
   int off_a, off_b, off_bias;
   // software-gather producer (kProd 1: folded layout, 2: explicit im2col)
@@ -531,8 +532,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     for (int i = 0; i < a.n_acc; ++i) {
       mbar_init(bar_tfull + 8 * i, 1);
       // every epilogue thread arrives (pair: one arrive per warp of both CTAs, on the leader's)
-      mbar_init(bar_tempty + 8 * i, kPair == 2 ? 16 : 256);
-      mbar_init(bar_tempty_hi + 8 * i, kPair == 2 ? 16 : 256);
+      mbar_init(bar_tempty + 8 * i, kPair == 2 ? 16 : (a.epi_pp ? 128 : 256));  // ping-pong: one warp group per tile
+      mbar_init(bar_tempty_hi + 8 * i, kPair == 2 ? 16 : (a.epi_pp ? 128 : 256));
     }
     mbar_init(bar_b, 1);
     mbar_init(bar_bpeer, 1);
@@ -805,15 +806,21 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // row write whole 128-byte lines, 8 rows per store instruction.
     constexpr int VPT = CH / 4;    // consecutive output channels per thread and row
     constexpr int NREG = CH / 2;   // registers per 16x256b load (two rows)
-    constexpr int CPW = 128 / CH;  // chunks per warp at the maximum N-tile width (256)
+    constexpr int CPW = 256 / CH;  // chunks per warp at the maximum N-tile width (256), ping-pong mode
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const int nchunks = ncols / CH;
-    const int nc_w = (nchunks > half) ? (nchunks - half + 1) / 2 : 0;  // this warp's chunks
-    const int n_it = 2 * nc_w;                                          // x two 16-lane halves
+    // Two ways to share a tile among the 8 warps. Default: warps 2..5 take the
+    // even chunks, 6..9 the odd ones, of every tile. Ping-pong (a.epi_pp):
+    // warps 2..5 take every chunk of the even tiles, 6..9 of the odd ones, so
+    // two tiles drain at once (per-tile latency overlaps when N is narrow).
+    const bool pp = a.epi_pp != 0;
+    const int c_first = pp ? 0 : half, c_step = pp ? 1 : 2;
+    const int nc_w = pp ? nchunks : ((nchunks > half) ? (nchunks - half + 1) / 2 : 0);  // this warp's chunks
+    const int n_it = 2 * nc_w;                                                            // x two 16-lane halves
     // accumulator half-split: iterations [0, lo_it) read the lower half of the columns
     const bool split_acc = a.nt_split[ntile] > 0 && a.ksplit == 1;
-    const int lo_it = split_acc ? 2 * ((nchunks / 2 - half + 1) / 2) : n_it;
+    const int lo_it = split_acc ? (pp ? 2 * (nchunks / 2) : 2 * ((nchunks / 2 - half + 1) / 2)) : n_it;
     const int k4 = lane & 3;
     const bool relu = (a.epi_flags & WF_EPI_RELU) != 0;
     const bool dbg_skip_epi = (a.epi_flags & 0x200) != 0;
@@ -821,17 +828,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     const bool skip_ld = (a.epi_flags & 0x800) != 0;
     const bool stream_st = (a.epi_flags & 0x100000) != 0;  // experiment: streaming store hints
     const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
-    int boff[CPW];          // shared-memory bias index of this thread's channels in each of its chunks
-    long long coff[CPW];    // byte offset of each chunk's first output column in a row
-    int jsub[CPW];          // output sub-column j of this thread's channels (OW % r tail mask)
-#pragma unroll
-    for (int cc = 0; cc < CPW; ++cc) {
-      const int c = half + 2 * cc;
-      const int ocol = (c < nchunks) ? a.chunk_col[ntile][c] : col0;  // slot order -> output column
-      coff[cc] = static_cast<long long>(ocol + VPT * k4) * sizeof(OutT);
-      jsub[cc] = (ocol + VPT * k4) / a.Cout;
-      boff[cc] = (c < nchunks) ? ocol - col0 + VPT * k4 : 0;
-    }
+    // chunk cc of this warp is accumulator chunk c_first + c_step * cc; its output
+    // column comes from the slot order (chunk_col), read per iteration
     // the four M rows this thread stores: (16-lane half h16, row group r8).
     // Everything about them that does not depend on the tile is computed once:
     // output row t of the tile, byte offset from the tile's first output pixel,
@@ -850,8 +848,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         row_off[h16][r8] = (static_cast<long long>(t) * a.OW + wq * a.r) * a.Cout * static_cast<long long>(sizeof(OutT));
         row_ok[h16][r8] = (wq < a.Wfo) && (t < a.OHt) && !dbg_skip_store;
         unsigned bits = 0;
-#pragma unroll
-        for (int cc = 0; cc < CPW; ++cc) bits |= (wq * a.r + jsub[cc] < a.OW) ? (1u << cc) : 0u;
+        for (int cc = 0; cc < nc_w; ++cc) {
+          const int jsub = (a.chunk_col[ntile][c_first + c_step * cc] + VPT * k4) / a.Cout;  // output sub-column j
+          bits |= (wq * a.r + jsub < a.OW) ? (1u << cc) : 0u;
+        }
         row_cc[h16][r8] = bits;
       }
     const long long img_bytes = static_cast<long long>(a.OH) * a.OW * a.Cout * static_cast<long long>(sizeof(OutT));
@@ -874,6 +874,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
      vrem += vr;
      if (vrem >= vdiv) { vrem -= vdiv; ++vn; }
      for (int k = 0; k < a.tps; ++k, ++it_tile) {  // tile k of stage unit u
+      if (pp && (it_tile & 1) != half) continue;  // the other warp group drains this tile
       const int acc = it_tile & (a.n_acc - 1);
       const uint32_t acc_round = static_cast<uint32_t>(it_tile >> a.acc_shift);
       const int mt = u * kPair + static_cast<int>(rank);  // (im2col rows; tps == 1 there)
@@ -909,7 +910,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       const uint32_t tq = tmem_base + acc * a.acc_stride + (static_cast<uint32_t>(quarter * 32) << 16);
       // iteration it: chunk cc = it / 2 (c = half + 2cc), 16-lane half h16 = it % 2
       auto taddr = [&](int it) {
-        return tq + (static_cast<uint32_t>((it & 1) * 16) << 16) + static_cast<uint32_t>((half + 2 * (it >> 1)) * CH);
+        return tq + (static_cast<uint32_t>((it & 1) * 16) << 16) +
+               static_cast<uint32_t>((c_first + c_step * (it >> 1)) * CH);
       };
       if (lo_it == 0) arrive_at<kPair>(te_lo + 8 * acc);  // this warp reads no lower-half column
       uint32_t buf[2][NREG];
@@ -922,10 +924,12 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         if (it + 1 < n_it) tmem_ld_16x256b<NREG>(taddr(it + 1), buf[(it + 1) & 1], skip_ld);
         const int cc = it >> 1, h16 = it & 1;
         const uint32_t(&r)[NREG] = buf[it & 1];
+        const int ocol = a.chunk_col[ntile][c_first + c_step * cc];  // slot order -> output column
+        const long long coff = static_cast<long long>(ocol + VPT * k4) * sizeof(OutT);
         float bb[VPT];  // bias of this thread's VPT channels (16-byte shared loads; registers are tight)
 #pragma unroll
         for (int q = 0; q < VPT / 4; ++q) {
-          const float4 t4 = reinterpret_cast<const float4*>(sbias + boff[cc])[q];
+          const float4 t4 = reinterpret_cast<const float4*>(sbias + ocol - col0 + VPT * k4)[q];
           bb[4 * q] = t4.x; bb[4 * q + 1] = t4.y; bb[4 * q + 2] = t4.z; bb[4 * q + 3] = t4.w;
         }
 #pragma unroll
@@ -941,8 +945,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
             for (int k = 0; k < VPT; ++k) v[k] = (v[k] < 0.0f) ? 0.0f : v[k];
           }
           if (rowv[h16][r8] && ((rowc[h16][r8] >> cc) & 1u)) {
-            if (stream_st) store_row<OutT, VPT, true>(rowp[h16][r8] + coff[cc], v);
-            else store_row<OutT, VPT, false>(rowp[h16][r8] + coff[cc], v);
+            if (stream_st) store_row<OutT, VPT, true>(rowp[h16][r8] + coff, v);
+            else store_row<OutT, VPT, false>(rowp[h16][r8] + coff, v);
           }
         }
         if (it + 1 == lo_it) {  // lower half of the accumulator read (its wait::ld is done)

@@ -120,6 +120,7 @@ VARIANT_ENVS = [
     {"WF_CTA_PAIR": "1"},                           # cta_group::2 pairs (opt-in)
     {"WF_TPS": "1"},                                # one M tile per A stage
     {"WF_NACC": "2"},                               # two accumulator buffers
+    {"WF_EPI_PP": "1"}, {"WF_EPI_PP": "0"},         # epilogue warp groups alternate tiles / share each tile
 ]
 
 
