@@ -154,9 +154,9 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   a.tps = S.tps;
   a.uph = static_cast<int>((S.ohb + S.tps - 1) / S.tps);
   a.tile_shift = S.tile_shift;
-  a.num_units = (S.tps == 2) ? static_cast<int>(d.n) * a.uph : static_cast<int>((a.num_mtiles + S.pair - 1) / S.pair);
+  a.num_units = (S.tps > 1) ? static_cast<int>(d.n) * a.uph : static_cast<int>((a.num_mtiles + S.pair - 1) / S.pair);
   a.unit_stride = a.ctas_per_ntile / S.pair;
-  if (S.tps == 2 && S.pair != 1) {
+  if (S.tps > 1 && S.pair != 1) {
     *err = "two-tile stages run single-CTA";
     return WF_UNSUPPORTED;
   }

@@ -56,7 +56,7 @@ struct ConvArgs {
   int nt_split[kMaxNTiles];       // lower-half MMAs of the N-tile (-1: no accumulator half-split)
   int num_units, unit_stride;     // M-tile units (pairs of M tiles in cta_group::2 mode) and the CTA stride
   unsigned a_desc_hi;             // A descriptor bits 32..63: SBO, version, layout (no swizzle / SWIZZLE_32B)
-  int tps, uph, tile_shift;       // M tiles per A stage, stage units per image (tps 2), A bytes between tiles
+  int tps, uph, tile_shift;       // M tiles per A stage, stage units per image (tps > 1), A bytes between tiles
   int sw32, nq, qregion_bytes;    // SWIZZLE_32B A: one 32-byte-piece box per in-pixel offset
   int qcoord[4];                  // sw32: element coordinate (in the pixel) of each region's box
   int qbyte[4];                   // sw32: the same offset in bytes
@@ -231,9 +231,9 @@ __device__ __forceinline__ RowProd row_prod(const ConvArgs& a, uint32_t row_tab)
 // Image and first output row of M tile k of stage unit u (this CTA's tile in pair mode).
 template <int kPair>
 __device__ __forceinline__ void tile_origin(const ConvArgs& a, int u, int k, uint32_t rank, int& n, int& oh0) {
-  if (a.tps == 2) {
+  if (a.tps > 1) {
     n = u / a.uph;
-    oh0 = ((u - n * a.uph) * 2 + k) * a.OHt;
+    oh0 = ((u - n * a.uph) * a.tps + k) * a.OHt;
   } else {
     const int mt = u * kPair + static_cast<int>(rank);
     n = mt / a.ohb;
@@ -859,10 +859,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // (image, first output row) of the current stage unit, advanced without
     // divisions: v = u (two-tile stages, divisor = units per image) or the M
     // tile u*kPair + rank (one tile per stage, divisor = M tiles per image)
-    const int vdiv = (a.tps == 2) ? a.uph : a.ohb;
-    const int vstep = (a.tps == 2) ? a.unit_stride : a.unit_stride * kPair;
+    const int vdiv = (a.tps > 1) ? a.uph : a.ohb;
+    const int vstep = (a.tps > 1) ? a.unit_stride : a.unit_stride * kPair;
     const int vq = vstep / vdiv, vr = vstep - (vstep / vdiv) * vdiv;
-    const int v0 = (a.tps == 2) ? local : local * kPair + static_cast<int>(rank);
+    const int v0 = (a.tps > 1) ? local : local * kPair + static_cast<int>(rank);
     int vn = v0 / vdiv, vrem = v0 - (v0 / vdiv) * vdiv;
     int it_tile = 0;
     // pair: arrivals go to the leader's accumulator-free barriers
@@ -879,7 +879,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       const uint32_t acc_round = static_cast<uint32_t>(it_tile >> a.acc_shift);
       const int mt = u * kPair + static_cast<int>(rank);  // (im2col rows; tps == 1 there)
       const int n = vn_u;
-      const int oh0 = (a.tps == 2) ? (vrem_u * 2 + k) * a.OHt : vrem_u * a.OHt;
+      const int oh0 = (a.tps > 1) ? (vrem_u * a.tps + k) * a.OHt : vrem_u * a.OHt;
       mbar_wait(bar_tfull + 8 * acc, acc_round & 1u);
       tc_fence_after();
       if (dbg_skip_epi || n_it == 0) {

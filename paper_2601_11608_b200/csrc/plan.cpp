@@ -237,13 +237,20 @@ wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf
     *out = std::move(s1);
     return st;
   }
+  // M tiles per A stage: 2 when the stage still double-buffers, the N-tiling
+  // is unchanged and every SM keeps >= 4 stage units (small batches keep their
+  // parallelism); WF_TPS=1/2/4 forces one. 4 is supported but measured 1-3%
+  // slower than 2 (R50, MNv2, VGG): fewer halo rows, shallower pipeline.
   const char* env = std::getenv("WF_TPS");
-  const bool try2 = tps_req == 2 || (tps_req < 0 && !(env && env[0] == '1') && s1.ohb >= 2 &&
-                                     d.n * s1.ohb >= 8 * 148);  // keep >= 4 stage units per B200 SM
-  if (try2 && (s1.prod == 0 || s1.prod == 3) && s1.pair == 1) {
+  const int env_tps = (env && (env[0] == '1' || env[0] == '2' || env[0] == '4')) ? env[0] - '0' : 0;
+  for (int cand : {4, 2}) {
+    const bool want = (tps_req > 0) ? tps_req == cand
+                                    : (env_tps ? env_tps == cand
+                                               : cand == 2 && s1.ohb >= cand && d.n * ceil_div(s1.ohb, cand) >= 4 * 148);
+    if (!want || !(s1.prod == 0 || s1.prod == 3) || s1.pair != 1) continue;
     Schedule s2;
     std::string e2;
-    if (make_schedule_tps(d, f_req, gs_req, in_dtype, 2, &s2, &e2, kpair_req, 0) == WF_OK &&
+    if (make_schedule_tps(d, f_req, gs_req, in_dtype, cand, &s2, &e2, kpair_req, 0) == WF_OK &&
         s2.plan.status == WF_FOLD_APPLY && s2.stages >= 2 && s2.ntiles.size() == s1.ntiles.size()) {
       *out = std::move(s2);
       return WF_OK;

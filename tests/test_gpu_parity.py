@@ -118,7 +118,7 @@ def test_tensor_core_conv_configs_within_tolerance(golden_configs, name):
 VARIANT_ENVS = [
     {"WF_KPAIR": "0"}, {"WF_KPAIR": "1"},          # 32-byte covers / cross-kh core-column pairs
     {"WF_CTA_PAIR": "1"},                           # cta_group::2 pairs (opt-in)
-    {"WF_TPS": "1"},                                # one M tile per A stage
+    {"WF_TPS": "1"}, {"WF_TPS": "2"}, {"WF_TPS": "4"},  # M tiles per A stage
     {"WF_NACC": "2"},                               # two accumulator buffers
     {"WF_EPI_PP": "1"}, {"WF_EPI_PP": "0"},         # epilogue warp groups alternate tiles / share each tile
 ]

@@ -133,10 +133,13 @@ GEOMS = [  # (KH, KW, Cout, stride, pad, H, W, dtype)
 ]
 
 
+@pytest.mark.parametrize("tps", ["", "2", "4"])
 @pytest.mark.parametrize("kpair", ["0", "1"])
 @pytest.mark.parametrize("geom", GEOMS, ids=["r50", "vgg", "alexnet", "mnv2", "r50_tf32", "gemm"])
-def test_schedule_replay_exact(oracle, monkeypatch, geom, kpair):
+def test_schedule_replay_exact(oracle, monkeypatch, geom, kpair, tps):
     monkeypatch.setenv("WF_KPAIR", kpair)
+    if tps:
+        monkeypatch.setenv("WF_TPS", tps)  # M tiles per A stage (the batch here is too small to pick them)
     KH, KW, Co, s, p, H, W, dt = geom
     rng = np.random.default_rng(KH * 7 + W)
     x = rng.integers(-3, 4, (1, H, W, 3)).astype(np.float32)
