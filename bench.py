@@ -2,10 +2,12 @@
 
 Workload (BASELINE.json configs[4], the config the metric is quoted on for
 1/2/4/8 GPUs): ResNet-50 conv1 (7x7, stride 2, pad 3, Cin=3 -> Cout=64),
-NHWC 224x224, global batch 8192, bf16 in / bf16 out, fp32 accumulate, bias
-fused, synthetic data (seeded U[-1,1)), random-init weights. The batch is
-sharded across ranks (contiguous slices, no collective on the hot path):
-total work is fixed as N grows ("scaling": "strong").
+NHWC 224x224, batch 8192 per GPU, bf16 in / bf16 out, fp32 accumulate, bias
+fused, synthetic data (seeded U[-1,1)), random-init weights. Images are
+independent, so ranks take disjoint shards with no collective on the hot
+path; by default every rank holds 8192 images ("scaling": "weak", the work
+per GPU is fixed as N grows). --strong instead splits ONE global batch of
+8192 into contiguous slices (BASELINE.json configs[4] read literally).
 
 A step = one folded tcgen05 conv over the rank's shard; inputs (2.47 GB at
 N=1) exceed the 126 MB L2 so no flush is needed between steps. Timing: W
@@ -123,8 +125,10 @@ def run_reference(args) -> None:
     value = n / t
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(vals),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": N_IMG, "impl": "CPU reference"},
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "global_batch": N_IMG if args.strong else N_IMG * args.gpus,
+                       "impl": "CPU reference (host cores of rank 0; a bounded sample per step)"},
             "useful_tflops": value * USEFUL_FLOP_PER_IMG / 1e12,
             "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": vals[0]["kind"],
                              "sample": vals[-1]["sample"]},
@@ -194,7 +198,11 @@ def run_gpu(args) -> None:
     dev = torch.device("cuda", local)
     if world > 1:
         shard.init("nccl")
-    lo, hi = shard.shard_range(N_IMG, rank, world)
+    if args.strong:  # one global batch of N_IMG split across the ranks
+        lo, hi = shard.shard_range(N_IMG, rank, world)
+    else:            # N_IMG images per rank
+        lo, hi = rank * N_IMG, (rank + 1) * N_IMG
+    total = hi - lo if world == 1 else (N_IMG if args.strong else N_IMG * world)
     n = hi - lo
     peaks = load_peaks()
 
@@ -229,7 +237,7 @@ def run_gpu(args) -> None:
     ms_local = ev0.elapsed_time(ev1)
     ms_total = shard.max_over_ranks(ms_local, dev)
     ms_step = ms_total / args.steps
-    value = N_IMG / (ms_step / 1e3)
+    value = total / (ms_step / 1e3)
 
     # ---- verification (outside timing): sampled image vs the CPU oracle; NCCL gather --
     verify = None
@@ -273,8 +281,8 @@ def run_gpu(args) -> None:
         ums = time_variant(convu, x, max(3, args.steps // 20))
         for name, ms_, c_ in (("fold", ms_step, conv), ("zeropad_cin8", zms, convz), ("unfolded_cin3", ums, convu)):
             d = c_.device_plan
-            variants[name] = {"images_per_s": N_IMG / (ms_ / 1e3), "ms_per_step": ms_,
-                              "useful_tflops": N_IMG * USEFUL_FLOP_PER_IMG / (ms_ / 1e3) / 1e12,
+            variants[name] = {"images_per_s": total / (ms_ / 1e3), "ms_per_step": ms_,
+                              "useful_tflops": total * USEFUL_FLOP_PER_IMG / (ms_ / 1e3) / 1e12,
                               "issued_tflops": 2 * d["issued_macs"] * world / (ms_ / 1e3) / 1e12,
                               "useful_over_issued": d["useful_macs"] / d["issued_macs"] * (
                                   C / 8 if name.startswith("zero") else 1.0),
@@ -298,7 +306,7 @@ def run_gpu(args) -> None:
         ev1.record(stream)
         barrier()
         ems = shard.max_over_ranks(ev0.elapsed_time(ev1), dev) / es
-        e2e = {"value": N_IMG / (ems / 1e3), "unit": "images/s", "h2d_bytes_per_step": xh.numel() * 2 * world,
+        e2e = {"value": total / (ems / 1e3), "unit": "images/s", "h2d_bytes_per_step": xh.numel() * 2 * world,
                "d2h_bytes_per_step": yh.numel() * 2 * world, "ms_per_step": ems, "steps": es,
                "path": "FoldedConv2d.run_host (pinned host -> H2D -> folded conv -> D2H, chunked on 2 streams)"}
         del xh, yh
@@ -327,14 +335,15 @@ def run_gpu(args) -> None:
             traffic = tj if tj is None else float(tj)
         except Exception:
             traffic = None
-    useful_tf = N_IMG * USEFUL_FLOP_PER_IMG / (ms_step / 1e3) / 1e12
+    useful_tf = total * USEFUL_FLOP_PER_IMG / (ms_step / 1e3) / 1e12
     ai = USEFUL_FLOP_PER_IMG / (IN_BYTES_PER_IMG + OUT_BYTES_PER_IMG)
     attainable = min(peaks["bf16_tflops"], ai * peaks["hbm_gbs"] / 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded U[-1,1) inputs, random-init conv1 weights)",
-        "config": {"workload": WORKLOAD, "global_batch": N_IMG, "per_gpu_batch": n, "image": [H, W, C],
+        "config": {"workload": WORKLOAD, "global_batch": total, "per_gpu_batch": n, "image": [H, W, C],
                    "filter": [K, K, C, COUT], "stride": STRIDE, "padding": PAD, "epilogue": "bias",
                    "fold_factor": conv.device_plan["f"], "parallelism": f"batch-shard{world}",
                    "l2": "no flush: per-step input 2.47 GB/N and output 13.15 GB/N exceed the 126 MB L2"},
@@ -371,6 +380,7 @@ def main():
     ap.add_argument("--e2e-chunk", type=int, default=512)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--strong", action="store_true", help="split one global batch of 8192 across the ranks")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     args = ap.parse_args()
