@@ -401,3 +401,37 @@ def test_unfolded_full_size_sampled(oracle):
     y = wf.FoldedConv2d(w, b, x.shape, stride=2, padding=3, variant="unfolded")(x).float().cpu().numpy()
     ref = oracle.conv_padded(x[2:3].float().cpu().numpy(), w.float().cpu().numpy(), b.cpu().numpy(), 2, 3)
     assert normrel(y[2:3], ref) <= 1e-2
+
+
+def _random_device_geoms(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        s = int(rng.choice([1, 2, 4]))
+        k = int(rng.integers(1, 12))
+        p = int(rng.integers(0, min(4, k)))
+        cout = int(rng.choice([32, 64, 96, 128]))
+        dt = str(rng.choice(["bf16", "f16", "tf32"]))
+        h = int(rng.integers(max(k, 4), 72))
+        w = int(rng.integers(max(k, 8), 96))  # any width: W % f != 0 and odd pitches take the re-pitch path
+        if w + 2 * p < k or h + 2 * p < k:
+            continue
+        out.append((k, cout, s, p, h, w, dt, int(rng.integers(1, 4))))
+    return out
+
+
+@pytest.mark.parametrize("geom", _random_device_geoms(40, 7), ids=lambda g: "k{}c{}s{}p{}h{}w{}{}n{}".format(*g))
+def test_random_geometries_exact(oracle, geom):
+    """Random first-layer geometries through the device kernel: bit-exact on integer data (fp32 out)."""
+    K, Co, s, p, h, w, dt, n = geom
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16, "tf32": torch.float32}[dt]
+    rng = np.random.default_rng(K * 7919 + h * 31 + w)
+    x = rng.integers(-3, 4, (n, h, w, 3)).astype(np.float32)
+    wt = rng.integers(-3, 4, (K, K, 3, Co)).astype(np.float32)
+    try:
+        conv = wf.FoldedConv2d(cuda(wt, tdt), None, x.shape, stride=s, padding=p, dtype=tdt)
+    except wf.UnsupportedError as e:
+        pytest.skip(f"fold not applicable: {e}")
+    y = conv(cuda(x, tdt), out_dtype=torch.float32)
+    np.testing.assert_array_equal(y.cpu().numpy(), oracle.conv_padded(x, wt, None, s, p),
+                                  err_msg=str(conv.device_plan))

@@ -146,3 +146,37 @@ def test_schedule_replay_exact(oracle, monkeypatch, geom, kpair, tps):
     w = rng.integers(-3, 4, (KH, KW, 3, Co)).astype(np.float32)
     sc = replay(oracle, x, w, s, p, dt)
     assert bool(sc["kpair"]) == (kpair == "1")
+
+
+def _random_geoms(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        s = int(rng.choice([1, 2, 4]))
+        k = int(rng.integers(1, 12))
+        p = int(rng.integers(0, min(4, k)))
+        cout = int(rng.choice([32, 64, 96, 128]))
+        dt = str(rng.choice(["bf16", "f16", "tf32"]))
+        h = int(rng.integers(max(k, 4), 40))
+        w = int(rng.choice([8, 16, 24, 32, 48, 64]))
+        if w + 2 * p < k or h + 2 * p < k:
+            continue
+        out.append((k, k, cout, s, p, h, w, dt))
+    return out
+
+
+@pytest.mark.parametrize("geom", _random_geoms(24, 2024), ids=lambda g: "k{}s{}p{}c{}h{}w{}{}".format(
+    g[0], g[3], g[4], g[2], g[5], g[6], g[7]))
+def test_schedule_replay_random_geometries(oracle, geom):
+    """Random kernels / strides / paddings / widths / dtypes: whatever the
+    planner builds (or falls back from) replays exactly."""
+    KH, KW, Co, s, p, H, W, dt = geom
+    N, Hh, Ww = 1, H, W
+    d = A.make_desc(N, Hh, Ww, 3, KH, KW, Co, s, s, p, p)
+    plan = A.plan_fold(d, 0, 0, DT[dt])
+    if plan.status != A.WF_FOLD_APPLY:
+        pytest.skip(f"fold falls back: {A.REASONS[plan.reason]}")
+    rng = np.random.default_rng(KH * 1000 + W)
+    x = rng.integers(-3, 4, (N, Hh, Ww, 3)).astype(np.float32)
+    w = rng.integers(-3, 4, (KH, KW, 3, Co)).astype(np.float32)
+    replay(oracle, x, w, s, p, dt)
