@@ -347,6 +347,20 @@ def test_zero_padded_cin8_variant_exact(oracle, geom):
         assert conv.device_plan["cta_pair"] == 2
 
 
+def test_cuda_graph_replay_matches_eager():
+    """FoldedConv2d.graphed(): the captured launch replays on new input contents."""
+    torch.manual_seed(0)
+    w = (torch.randn(7, 7, 3, 64, device="cuda") * 0.1).bfloat16()
+    b = torch.randn(64, device="cuda")
+    x = torch.randn(2, 64, 64, 3, device="cuda").bfloat16()
+    conv = wf.FoldedConv2d(w, b, x.shape, stride=2, padding=3)
+    replay, out = conv.graphed(x)
+    for _ in range(2):
+        x.copy_(torch.randn_like(x, dtype=torch.float32).bfloat16())
+        replay()
+        torch.testing.assert_close(out, conv(x), rtol=0, atol=0)
+
+
 def test_no_cpu_fallback_on_cpu_tensors():
     conv = wf.FoldedConv2d(torch.randn(3, 3, 3, 16, device="cuda").bfloat16(), None, (1, 32, 32, 3), padding=1)
     with pytest.raises(ValueError):
