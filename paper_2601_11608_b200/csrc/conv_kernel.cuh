@@ -38,6 +38,10 @@
 namespace wfb {
 
 constexpr int kMaxTable = 384;  // schedule entries per launch (constant bank)
+#ifndef WFB_ISSUE_GROUP
+#define WFB_ISSUE_GROUP 8
+#endif
+constexpr int kIssueGroup = WFB_ISSUE_GROUP;  // MMAs whose table words are loaded together
 constexpr int kGatherWarps = 4;  // row-staged producer: transposer warps 10..13
 constexpr int kMaxKsplit = 8;    // A stages per M tile (im2col kh ranges)
 constexpr int kMaxStageRows = 64;  // folded raw rows per A stage (row producer)
@@ -717,40 +721,51 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // uniform registers straight from the constant bank; one lane issues.
     const bool skip_mma = (a.epi_flags & 0x100) != 0;  // profiling switch
     const bool no_wait = (a.epi_flags & 0x200000) != 0;  // profiling: issue the schedule back to back (with 0x1200)
-    const uint32_t b_lo = (base + a.off_b) >> 4;
-    const uint32_t a_hi = a.a_desc_hi;
+    const uint32_t b_lo = static_cast<uint32_t>(opq(static_cast<int>((base + a.off_b) >> 4)));
+    const uint32_t a_hi = static_cast<uint32_t>(opq(static_cast<int>(a.a_desc_hi)));
     const bool leader = elect_one() && rank == 0;  // pair: the leader CTA issues for both SMs
     if (kPair == 2 && rank != 0) goto mma_done;
     mbar_wait(bar_b, 0);
     if constexpr (kPair == 2) mbar_wait_cluster(bar_bpeer, 0);
     {
+    // Every per-tile scalar is laundered into a register once: each tcgen05 /
+    // mbarrier asm statement clobbers "memory", so a field read through `a`
+    // inside the loop is re-fetched from the (large) parameter constant bank
+    // after every MMA -- at the head of each tile's issue chain that latency
+    // made the issuer ~40% slower than the tensor pipe (tools/probes/issue_probe.cu).
+    const int ksplit = opq(a.ksplit), tps = opq(a.tps), stages = opq(a.stages), stage_bytes = opq(a.stage_bytes);
+    const int tile_shift = opq(a.tile_shift), n_acc = opq(a.n_acc), acc_shift = opq(a.acc_shift);
+    const int num_units = opq(a.num_units), unit_stride = opq(a.unit_stride);
+    const uint32_t acc_stride = static_cast<uint32_t>(opq(static_cast<int>(a.acc_stride)));
+    const uint32_t a_base = static_cast<uint32_t>(opq(static_cast<int>(base + a.off_a)));
+    const int nt_e0 = opq(a.nt_entry0[ntile]), nt_en = opq(a.nt_entries[ntile]), nt_sp = opq(a.nt_split[ntile]);
     // profiling (0x80000, CTA 0): cycles the issuer waits on the accumulator / the A stage
     const bool dbg = (a.epi_flags & 0x80000) && blockIdx.x == 0;
     long long w_acc = 0, w_full = 0, w_hi = 0, t_all = dbg ? clock64() : 0;
     int it0 = 0;  // first A stage of the unit (ksplit sub-stages per unit)
     int tile = 0;
-    for (int u = local; u < a.num_units; u += a.unit_stride, it0 += a.ksplit) {
-     for (int k = 0; k < a.tps; ++k, ++tile) {  // tps M tiles share the unit's A stage
-      const int acc = tile & (a.n_acc - 1);
-      const uint32_t acc_round = static_cast<uint32_t>(tile >> a.acc_shift);
-      const int split = (a.ksplit == 1) ? a.nt_split[ntile] : -1;
+    for (int u = local; u < num_units; u += unit_stride, it0 += ksplit) {
+     for (int k = 0; k < tps; ++k, ++tile) {  // tps M tiles share the unit's A stage
+      const int acc = tile & (n_acc - 1);
+      const uint32_t acc_round = static_cast<uint32_t>(tile >> acc_shift);
+      const int split = (ksplit == 1) ? nt_sp : -1;
       long long t0 = dbg ? clock64() : 0;
       if (!no_wait) {
         mbar_wait(bar_tempty + 8 * acc, (acc_round & 1u) ^ 1u);
         if (split < 0) mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
       }
       if (dbg) { const long long t1 = clock64(); w_acc += t1 - t0; t0 = t1; }
-      const uint32_t d_base = tmem_base + acc * a.acc_stride;
-      for (int ks = 0; ks < a.ksplit; ++ks) {
+      const uint32_t d_base = tmem_base + acc * acc_stride;
+      for (int ks = 0; ks < ksplit; ++ks) {
         const int it = it0 + ks;
-        const int stage = it % a.stages;
-        const uint32_t round = static_cast<uint32_t>(it / a.stages);
-        const int e0 = (a.ksplit == 1) ? a.nt_entry0[ntile] : a.ks_entry0[ks];
-        const int entries = (a.ksplit == 1) ? a.nt_entries[ntile] : a.ks_entries[ks];
+        const int stage = it % stages;
+        const uint32_t round = static_cast<uint32_t>(it / stages);
+        const int e0 = (ksplit == 1) ? nt_e0 : a.ks_entry0[ks];
+        const int entries = (ksplit == 1) ? nt_en : a.ks_entries[ks];
         if (k == 0 && !no_wait) mbar_wait(bar_full + 8 * stage, round & 1u);
         if (dbg) { const long long t1 = clock64(); w_full += t1 - t0; t0 = t1; }
         tc_fence_after();
-        const uint32_t a_lo = (base + a.off_a + stage * a.stage_bytes + k * a.tile_shift) >> 4;
+        const uint32_t a_lo = (a_base + stage * stage_bytes + k * tile_shift) >> 4;
         if (!skip_mma) {
           int i = 0;
           if (split > 0) {  // lower half first, then wait for the epilogue to drain the upper half
@@ -765,9 +780,9 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
             if (dbg) w_hi += clock64() - t0;
             tc_fence_after();
           }
-          for (; i + 8 <= entries; i += 8) {
+          for (; i + kIssueGroup <= entries; i += kIssueGroup) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < kIssueGroup; ++j) {
               const uint4 e = a.table[e0 + i + j];
               const uint64_t adesc = (static_cast<uint64_t>(a_hi) << 32) | (e.x + a_lo);
               const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
@@ -784,7 +799,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         else if (split > 0) {
           mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
         }
-        if (leader && k == a.tps - 1) commit_to<kPair>(bar_empty + 8 * stage);  // last tile frees the stage
+        if (leader && k == tps - 1) commit_to<kPair>(bar_empty + 8 * stage);  // last tile frees the stage
       }
       if (leader) commit_to<kPair>(bar_tfull + 8 * acc);
       __syncwarp();
@@ -868,7 +883,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // pair: arrivals go to the leader's accumulator-free barriers
     const uint32_t te_lo = (kPair == 2) ? mapa(bar_tempty, 0) : bar_tempty;
     const uint32_t te_hi = (kPair == 2) ? mapa(bar_tempty_hi, 0) : bar_tempty_hi;
-    for (int u = local; u < a.num_units; u += a.unit_stride) {
+    // profiling (0x400000, with 0x200000): the epilogue warps sit the launch out
+    for (int u = (a.epi_flags & 0x400000) ? a.num_units : local; u < a.num_units; u += a.unit_stride) {
      const int vn_u = vn, vrem_u = vrem;
      vn += vq;
      vrem += vr;
