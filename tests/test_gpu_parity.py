@@ -449,3 +449,28 @@ def test_random_geometries_exact(oracle, geom):
     y = conv(cuda(x, tdt), out_dtype=torch.float32)
     np.testing.assert_array_equal(y.cpu().numpy(), oracle.conv_padded(x, wt, None, s, p),
                                   err_msg=str(conv.device_plan))
+
+
+def test_reference_acceptance_sweep_on_device():
+    """The reference's oracle-equivalence sweep (tests/acceptance/acceptance_main.cpp:92-124):
+    F in {1,2,4,8}, K in {1,2,3}, H in [K,8], W in {F,2F}, Cout in {1,2}; every
+    case legal, apply_width_fold -> folded conv -> bias_add -> reconstruct on
+    the device equals the unfolded conv + bias exactly (integer data)."""
+    rng = np.random.default_rng(1002)
+    cases = 0
+    for F in (1, 2, 4, 8):
+        for K in (1, 2, 3):
+            for H in range(K, 9):
+                for W in (F, 2 * F):
+                    for Co in (1, 2):
+                        x = rng.integers(-4, 5, (1, H, W, 1)).astype(np.float32)
+                        w = rng.integers(-4, 5, (K, 1, 1, Co)).astype(np.float32)
+                        b = rng.integers(-4, 5, (Co,)).astype(np.float32)
+                        plan, x_f, w_f, b_f = wf.apply_width_fold(x, w, b, F)
+                        assert plan["status"] == "apply", plan
+                        y_f = wf.bias_add(wf.conv2d(x_f, w_f), b_f)
+                        got = wf.reconstruct_output(y_f, F)
+                        want = wf.bias_add(wf.conv2d(x, w), b)
+                        np.testing.assert_array_equal(got, want, err_msg=f"F={F} K={K} H={H} W={W} Co={Co}")
+                        cases += 1
+    assert cases == 336
