@@ -742,9 +742,12 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // profiling (0x80000, CTA 0): cycles the issuer waits on the accumulator / the A stage
     const bool dbg = (a.epi_flags & 0x80000) && blockIdx.x == 0;
     long long w_acc = 0, w_full = 0, w_hi = 0, t_all = dbg ? clock64() : 0;
-    int it0 = 0;  // first A stage of the unit (ksplit sub-stages per unit)
     int tile = 0;
-    for (int u = local; u < num_units; u += unit_stride, it0 += ksplit) {
+    int stage_c = 0;           // A stage of the next sub-stage (kept incrementally: no division per tile)
+    uint32_t round_c = 0;      // its fill round
+    for (int u = local; u < num_units; u += unit_stride) {
+     const int stage_u = stage_c;  // the unit's first sub-stage
+     const uint32_t round_u = round_c;
      for (int k = 0; k < tps; ++k, ++tile) {  // tps M tiles share the unit's A stage
       const int acc = tile & (n_acc - 1);
       const uint32_t acc_round = static_cast<uint32_t>(tile >> acc_shift);
@@ -756,10 +759,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       }
       if (dbg) { const long long t1 = clock64(); w_acc += t1 - t0; t0 = t1; }
       const uint32_t d_base = tmem_base + acc * acc_stride;
+      int stage = stage_u;
+      uint32_t round = round_u;
       for (int ks = 0; ks < ksplit; ++ks) {
-        const int it = it0 + ks;
-        const int stage = it % stages;
-        const uint32_t round = static_cast<uint32_t>(it / stages);
+        if (ks > 0 && ++stage == stages) { stage = 0; ++round; }
         const int e0 = (ksplit == 1) ? nt_e0 : a.ks_entry0[ks];
         const int entries = (ksplit == 1) ? nt_en : a.ks_entries[ks];
         if (k == 0 && !no_wait) mbar_wait(bar_full + 8 * stage, round & 1u);
@@ -804,6 +807,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       if (leader) commit_to<kPair>(bar_tfull + 8 * acc);
       __syncwarp();
      }
+     for (int ks = 0; ks < ksplit; ++ks)  // advance past the unit's sub-stages
+       if (++stage_c == stages) { stage_c = 0; ++round_c; }
     }
     if (dbg && leader)
       printf("mma issuer cta0: %d tiles, %lld cycles: wait accumulator %lld (upper half %lld), wait A stage %lld\n",
