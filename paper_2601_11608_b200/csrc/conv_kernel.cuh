@@ -39,7 +39,7 @@ namespace wfb {
 
 constexpr int kMaxTable = 384;  // schedule entries per launch (constant bank)
 #ifndef WFB_ISSUE_GROUP
-#define WFB_ISSUE_GROUP 8
+#define WFB_ISSUE_GROUP 7
 #endif
 constexpr int kIssueGroup = WFB_ISSUE_GROUP;  // MMAs whose table words are loaded together
 constexpr int kGatherWarps = 4;  // row-staged producer: transposer warps 10..13
