@@ -168,7 +168,7 @@ wf_status wf_conv_fold_fwd_ws(const void* x, void* workspace, const void* w_pack
                               const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype,
                               uint32_t epilogue, void* stream) {
   if (!x || !w_packed || !y || !desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
-  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0x7FFF00))  // 0x7FFF00: profiling / cross-check switches
+  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0xFFFF00))  // 0xFFFF00: profiling / cross-check switches
     return fail(WF_INVALID_ARGUMENT, "unknown epilogue flags");
   if (plan->workspace_bytes > 0 && !workspace && !(epilogue & 0x4000))
     return fail(WF_INVALID_ARGUMENT, "this plan needs a workspace of plan->workspace_bytes (wf_conv_fold_fwd_ws)");

@@ -661,7 +661,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       }
       const uint32_t tx = static_cast<uint32_t>((a.box_bytes + a.shift_box_bytes) * __popc(a.res_mask));
       int it = 0;
-      for (int u = local; u < a.num_units; u += a.unit_stride, ++it) {
+      // profiling (0x800000, with 0x600000): the producer sits the launch out too
+      for (int u = (a.epi_flags & 0x800000) ? a.num_units : local; u < a.num_units; u += a.unit_stride, ++it) {
         const int stage = it % a.stages;
         const uint32_t round = static_cast<uint32_t>(it / a.stages);
         mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
