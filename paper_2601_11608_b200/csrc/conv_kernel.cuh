@@ -722,24 +722,22 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // uniform registers straight from the constant bank; one lane issues.
     const bool skip_mma = (a.epi_flags & 0x100) != 0;  // profiling switch
     const bool no_wait = (a.epi_flags & 0x200000) != 0;  // profiling: issue the schedule back to back (with 0x1200)
-    const uint32_t b_lo = static_cast<uint32_t>(opq(static_cast<int>((base + a.off_b) >> 4)));
-    const uint32_t a_hi = static_cast<uint32_t>(opq(static_cast<int>(a.a_desc_hi)));
+    const uint32_t b_lo = (base + a.off_b) >> 4;
+    const uint32_t a_hi = a.a_desc_hi;
     const bool leader = elect_one() && rank == 0;  // pair: the leader CTA issues for both SMs
     if (kPair == 2 && rank != 0) goto mma_done;
     mbar_wait(bar_b, 0);
     if constexpr (kPair == 2) mbar_wait_cluster(bar_bpeer, 0);
     {
-    // Every per-tile scalar is laundered into a register once: each tcgen05 /
-    // mbarrier asm statement clobbers "memory", so a field read through `a`
-    // inside the loop is re-fetched from the (large) parameter constant bank
-    // after every MMA -- at the head of each tile's issue chain that latency
-    // made the issuer ~40% slower than the tensor pipe (tools/probes/issue_probe.cu).
-    const int ksplit = opq(a.ksplit), tps = opq(a.tps), stages = opq(a.stages), stage_bytes = opq(a.stage_bytes);
-    const int tile_shift = opq(a.tile_shift), n_acc = opq(a.n_acc), acc_shift = opq(a.acc_shift);
-    const int num_units = opq(a.num_units), unit_stride = opq(a.unit_stride);
-    const uint32_t acc_stride = static_cast<uint32_t>(opq(static_cast<int>(a.acc_stride)));
-    const uint32_t a_base = static_cast<uint32_t>(opq(static_cast<int>(base + a.off_a)));
-    const int nt_e0 = opq(a.nt_entry0[ntile]), nt_en = opq(a.nt_entries[ntile]), nt_sp = opq(a.nt_split[ntile]);
+    // Per-tile scalars read once (laundering them into registers with opq()
+    // measured the same: the issuer's remaining gap to the tensor pipe is
+    // elsewhere).
+    const int ksplit = a.ksplit, tps = a.tps, stages = a.stages, stage_bytes = a.stage_bytes;
+    const int tile_shift = a.tile_shift, n_acc = a.n_acc, acc_shift = a.acc_shift;
+    const int num_units = a.num_units, unit_stride = a.unit_stride;
+    const uint32_t acc_stride = a.acc_stride;
+    const uint32_t a_base = base + a.off_a;
+    const int nt_e0 = a.nt_entry0[ntile], nt_en = a.nt_entries[ntile], nt_sp = a.nt_split[ntile];
     // profiling (0x80000, CTA 0): cycles the issuer waits on the accumulator / the A stage
     const bool dbg = (a.epi_flags & 0x80000) && blockIdx.x == 0;
     long long w_acc = 0, w_full = 0, w_hi = 0, t_all = dbg ? clock64() : 0;
