@@ -52,3 +52,54 @@ def gather_scalars(values: list[float], device: torch.device | str = "cpu") -> l
     out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(out, t)
     return [o.cpu().tolist() for o in out]
+
+
+def gather_to(tensor: torch.Tensor, sizes: list[int], dst: int = 0) -> torch.Tensor | None:
+    """Concatenate every rank's leading-dimension shard on rank ``dst`` (the
+    shards may differ in length by one; ``sizes`` are all ranks' lengths).
+    Verification / collection only -- never on the hot path. NCCL on CUDA
+    tensors, gloo on CPU ones; identity when not distributed."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return tensor
+    rank, world = dist.get_rank(), dist.get_world_size()
+    biggest = max(sizes)
+    pad = torch.zeros((biggest,) + tuple(tensor.shape[1:]), dtype=tensor.dtype, device=tensor.device)
+    pad[: tensor.shape[0]] = tensor
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)  # all_gather: NCCL has no gather of unequal shards
+    if rank != dst:
+        return None
+    return torch.cat([p[:n] for p, n in zip(parts, sizes)], dim=0)
+
+
+class ShardedConv:
+    """The batch-sharded launcher: rank r of a torchrun job convolves images
+    ``shard_range(N, r, world)`` of a global batch on its own GPU with the
+    folded kernel; there is no collective between the ranks' launches.
+    ``gather(y)`` collects the full output on one rank for verification.
+
+        conv = ShardedConv(w, b, (8192, 224, 224, 3), stride=2, padding=3)
+        y_local = conv(x[conv.lo:conv.hi].cuda())     # hot path, rank-local
+        y_all = conv.gather(y_local)                  # rank 0: (8192, 112, 112, 64)
+    """
+
+    def __init__(self, w, b, global_shape, stride=1, padding=0, dtype=None, **kw):
+        from .api import FoldedConv2d
+        self.rank, local, self.world = dist_env()
+        if dist.is_available() and dist.is_initialized():
+            self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.device = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
+        n = int(global_shape[0])
+        self.lo, self.hi = shard_range(n, self.rank, self.world)
+        self.sizes = [b_ - a_ for a_, b_ in (shard_range(n, r, self.world) for r in range(self.world))]
+        shape = (self.hi - self.lo,) + tuple(int(v) for v in global_shape[1:])
+        w = w.to(self.device) if isinstance(w, torch.Tensor) else torch.as_tensor(w, device=self.device)
+        if b is not None:
+            b = b.to(self.device) if isinstance(b, torch.Tensor) else torch.as_tensor(b, device=self.device)
+        self.conv = FoldedConv2d(w, b, shape, stride=stride, padding=padding, dtype=dtype, **kw)
+
+    def __call__(self, x_local: torch.Tensor, **kw) -> torch.Tensor:
+        return self.conv(x_local, **kw)
+
+    def gather(self, y_local: torch.Tensor, dst: int = 0) -> torch.Tensor | None:
+        return gather_to(y_local, self.sizes, dst)

@@ -361,6 +361,20 @@ def test_cuda_graph_replay_matches_eager():
         torch.testing.assert_close(out, conv(x), rtol=0, atol=0)
 
 
+def test_sharded_launcher_single_rank():
+    """shard.ShardedConv (the batch-sharded launcher) at world size 1 is the plain folded conv."""
+    from paper_2601_11608_b200 import shard
+    torch.manual_seed(3)
+    w = (torch.randn(7, 7, 3, 64) * 0.1).bfloat16()
+    b = torch.randn(64)
+    x = torch.randn(5, 64, 64, 3).bfloat16()
+    sc = shard.ShardedConv(w, b, x.shape, stride=2, padding=3)
+    assert (sc.lo, sc.hi) == (0, 5)
+    y = sc(x.cuda())
+    ref = wf.FoldedConv2d(w.cuda(), b.cuda(), x.shape, stride=2, padding=3)(x.cuda())
+    torch.testing.assert_close(sc.gather(y), ref, rtol=0, atol=0)
+
+
 def test_no_cpu_fallback_on_cpu_tensors():
     conv = wf.FoldedConv2d(torch.randn(3, 3, 3, 16, device="cuda").bfloat16(), None, (1, 32, 32, 3), padding=1)
     with pytest.raises(ValueError):

@@ -5,6 +5,7 @@ import os
 import socket
 
 import pytest
+import torch
 import torch.multiprocessing as mp
 
 from paper_2601_11608_b200 import shard
@@ -48,7 +49,11 @@ def _worker(rank, world, port, q):
         ms = 10.0 + r  # per-rank "device time"
         mx = shard.max_over_ranks(ms)
         got = shard.gather_scalars([float(lo), float(hi), ms])
-        q.put((r, local, w, lo, hi, mx, got))
+        # unequal shards (7 images over 2 ranks) collected on rank 0
+        a, b = shard.shard_range(7, r, w)
+        mine = torch.arange(a, b, dtype=torch.float32).reshape(-1, 1).repeat(1, 3)
+        full = shard.gather_to(mine, [y - x for x, y in (shard.shard_range(7, k, w) for k in range(w))], dst=0)
+        q.put((r, local, w, lo, hi, mx, got, None if full is None else full.tolist()))
     finally:
         dist.barrier()
         dist.destroy_process_group()
@@ -65,9 +70,13 @@ def test_two_rank_gloo_shard_and_reduce():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    spans = [(lo, hi) for (_, _, _, lo, hi, _, _) in res]
+    spans = [(lo, hi) for (_, _, _, lo, hi, _, _, _) in res]
     assert spans == [(0, 4096), (4096, 8192)]
-    for (r, local, w, _, _, mx, got) in res:
+    for (r, local, w, _, _, mx, got, full) in res:
         assert w == 2 and local == r
-        assert mx == 11.0  # max over ranks, as bench.py times multi-GPU runs
+        assert mx == 11.0
+        if r == 0:
+            assert full == [[float(i)] * 3 for i in range(7)]
+        else:
+            assert full is None  # max over ranks, as bench.py times multi-GPU runs
         assert got == [[0.0, 4096.0, 10.0], [4096.0, 8192.0, 11.0]]
