@@ -76,6 +76,44 @@ def time_conv(conv, x, y, relu, iters, flush):
     return tot / iters
 
 
+def bench_gemm_shapes(iters, hbm):
+    """fold_tall_skinny vs cuBLAS over a few (K, N, F) tall-skinny shapes (M = 2^24, bf16)."""
+    dev = torch.device("cuda", 0)
+    out = {}
+    for (K, N, F) in ((3, 64, 8), (4, 64, 4), (8, 64, 2), (8, 128, 2), (16, 64, 1), (3, 32, 8)):
+        M = 1 << 24
+        g = torch.Generator(device=dev).manual_seed(K * 100 + N)
+        a = (torch.rand((M, K), generator=g, device=dev) * 2 - 1).bfloat16()
+        b = (torch.rand((K, N), generator=g, device=dev) * 2 - 1).bfloat16()
+        c = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+        fold = wf.FoldedConv2d(b.reshape(1, 1, K, N), None, (1, M // F, F, K), fold=F)
+
+        def timed(fn):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(iters):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / iters
+
+        tf = timed(lambda: fold(a.reshape(1, M // F, F, K), bias=False, out=c.reshape(1, M // F, F, N)))
+        ref = (a[:4096].double() @ b.double()).float().cpu().numpy()
+        err = float(np.max(np.abs(c[:4096].float().cpu().numpy() - ref)) / np.max(np.abs(ref)))
+        tc = timed(lambda: torch.matmul(a, b, out=c))
+        byts = (M * K + M * N) * 2
+        out[f"K{K}_N{N}_F{F}"] = {"fold_ms": tf, "cublas_ms": tc, "fold_speedup_vs_cublas": tc / tf,
+                                  "fold_hbm_frac": byts / (tf / 1e3) / 1e9 / hbm, "normwise_rel_err": err}
+        print(f"gemm K={K} N={N} F={F}: fold {tf:.3f} ms ({byts / (tf / 1e3) / 1e9 / hbm:.2f} of HBM), "
+              f"cuBLAS {tc:.3f} ms, x{tc / tf:.2f}, err {err:.1e}", flush=True)
+        del a, b, c, fold
+        torch.cuda.empty_cache()
+    return out
+
+
 def bench_gemm(iters, hbm):
     """tall-skinny C = A B (M = 2^24 rows, K = 3, N = 64, bf16)
     three ways -- fold_tall_skinny on the folded tcgen05 kernel (F = 8, one
@@ -201,6 +239,7 @@ def main():
         torch.cuda.empty_cache()
     if not args.only or "gemm" in args.only:
         results["tall_skinny_gemm"] = bench_gemm(args.iters, hbm)
+        results["tall_skinny_gemm_shapes"] = bench_gemm_shapes(args.iters, hbm)
     results["_peaks"] = {"hbm_gbs": hbm, "bf16_tflops": tc, "source": "MEASURED_PEAKS.json"}
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(results, open(args.out, "w"), indent=1)
