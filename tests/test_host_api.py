@@ -134,3 +134,22 @@ def test_folded_filter_shape():
     assert _core.folded_filter_shape([5, 1, 1, 1], 8) == [5, 1, 8, 8]
     with pytest.raises(wf.IllegalFoldError):
         _core.folded_filter_shape([7, 7, 3, 64], 3, 2, 3)
+
+
+def test_auto_schedule_choices_for_the_bench_workloads(monkeypatch):
+    """Guard the planner's automatic choices (DESIGN 4): cross-kh core-column
+    pairs, two M tiles per A stage, no CTA pairs for the headline R50 b8192;
+    R50 issued/useful MACs at 1/0.63."""
+    for k in ("WF_KPAIR", "WF_TPS", "WF_CTA_PAIR"):
+        monkeypatch.delenv(k, raising=False)
+    from paper_2601_11608_b200 import _abi as A
+    p = A.plan_fold(A.make_desc(8192, 224, 224, 3, 7, 7, 64, 2, 2, 3, 3), 0, 0, A.WF_BF16).as_dict()
+    assert (p["kstep_mode"], p["stage_tiles"], p["cta_pair"], p["n_tiles"]) == (1, 2, 1, 1)
+    assert p["mma_entries"] == 21
+    assert abs(p["useful_macs"] / p["issued_macs"] - 0.631) < 0.005
+    # AlexNet zero-padded to Cin 8: B does not fit one SM -> CTA pairs
+    p = A.plan_fold(A.make_desc(512, 227, 227, 8, 11, 11, 96, 4, 4, 0, 0), 0, 0, A.WF_BF16).as_dict()
+    assert p["status"] == "apply" and p["cta_pair"] == 2
+    # batch 1: one output group per N-tile (more CTAs for a latency-bound launch)
+    p = A.plan_fold(A.make_desc(1, 224, 224, 3, 7, 7, 64, 2, 2, 3, 3), 0, 0, A.WF_TF32).as_dict()
+    assert p["n_tiles"] == 2 and p["stage_tiles"] == 1
