@@ -1,7 +1,7 @@
 #!/bin/bash
-# config x planner-knob timing matrix (short runs)
+# config x planner/launch-knob timing matrix (short runs)
 mkdir -p gpurun_out
-( for env in "" "WF_TPS=1" "WF_KPAIR=0" "WF_KPAIR=1" "WF_NACC=2" "WF_CTA_PAIR=1"; do
+( for env in "" "WF_TPS=1" "WF_TPS=4" "WF_KPAIR=0" "WF_KPAIR=1" "WF_NACC=2" "WF_EPI_PP=0" "WF_EPI_PP=1"; do
   echo "== $env"
   for c in "r50 4096" "alex 1024" "mnv2 1024" "vgg 512"; do
     set -- $c
