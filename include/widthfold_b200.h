@@ -186,6 +186,11 @@ wf_status wf_conv_direct_fwd(const float* x, const float* w, float* y, const wf_
 /* out = ReLU?(y + b[i % c]) -- widthfold::bias_add (src/refconv.cpp:82-95). */
 wf_status wf_bias_add(const float* y, const float* b, float* out, int64_t n, int64_t c, int32_t relu, void* stream);
 
+/* y = (bf16 | f16) x, round to nearest even: the device dtype of a graph node
+ * the pass folds at bf16/f16 precision (the reference graph is f32). No
+ * reference counterpart. */
+wf_status wf_cast_f32(const float* x, void* y, int64_t n, wf_dtype to, void* stream);
+
 /* out[j*cout + co] = b[co], j < r -- widthfold::replicate_bias (src/fold.cpp:213-226). */
 wf_status wf_replicate_bias(const float* b, int64_t cout, int64_t r, float* out, void* stream);
 

@@ -579,11 +579,14 @@ class Graph:
         return next((n for n in self.nodes if n["id"] == id), None)
 
 
-def width_fold_pass(graph: Graph, factor: int | None = None, align: int = 8):
+def width_fold_pass(graph: Graph, factor: int | None = None, align: int = 8, precision: str = "tf32"):
     """Rewrite every conv2d the generalized device fold applies to into one
-    ``folded_conv2d`` (tcgen05 TF32, sole-consumer constant bias fused).
+    ``folded_conv2d`` (tcgen05; sole-consumer constant bias fused).
+    ``precision``: "tf32" (default, within 1e-3 of the f32 graph) or
+    "bf16"/"f16" (the node casts its input and filter on the device; 1e-2).
     Returns ``(graph, report)`` like PassResult (include/widthfold/pass.hpp:45-52)."""
-    nodes, weights, report = _core.width_fold_pass(graph.nodes, graph.weights, int(factor or 0), int(align))
+    nodes, weights, report = _core.width_fold_pass(graph.nodes, graph.weights, int(factor or 0), int(align),
+                                                   {"fp16": "f16"}.get(precision, precision))
     return Graph(nodes, weights), report
 
 

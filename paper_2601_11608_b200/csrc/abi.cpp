@@ -198,6 +198,15 @@ wf_status wf_conv_direct_fwd(const float* x, const float* w, float* y, const wf_
   return WF_OK;
 }
 
+wf_status wf_cast_f32(const float* x, void* y, int64_t n, wf_dtype to, void* stream) {
+  if ((!x || !y) && n > 0) return fail(WF_INVALID_ARGUMENT, "null argument");
+  if (n <= 0) return WF_OK;
+  std::string err;
+  wf_status st = wfb::launch_cast_f32(x, y, n, to, static_cast<cudaStream_t>(stream), &err);
+  if (st != WF_OK) return fail(st, err);
+  return WF_OK;
+}
+
 wf_status wf_bias_add(const float* y, const float* b, float* out, int64_t n, int64_t c, int32_t relu, void* stream) {
   if (!y || !b || !out) return fail(WF_INVALID_ARGUMENT, "null argument");
   if (c < 1 || n < 0 || n % c != 0) return fail(WF_SHAPE_MISMATCH, "bias length does not divide the output");

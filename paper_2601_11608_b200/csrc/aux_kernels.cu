@@ -16,7 +16,11 @@
 //   blockdiag_check      BlockDiagFilter::from_expanded's strict-zero check
 //                        (src/blockdiag.cpp:24-84): any off-diagonal entry that
 //                        is not +-0.0f is an error.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include <algorithm>
 #include <cstdint>
@@ -184,6 +188,32 @@ wf_status launch_bias_add(const float* y, const float* b, float* out, long long 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("bias_add_kernel: ") + cudaGetErrorString(e);
+    return WF_CUDA_ERROR;
+  }
+  return WF_OK;
+}
+
+// fp32 -> bf16 / fp16, round to nearest even (the device dtypes of a folded graph node)
+template <typename T>
+__global__ void cast_f32_kernel(const float* __restrict__ x, T* __restrict__ y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(T) == 2 && std::is_same<T, __nv_bfloat16>::value) y[i] = __float2bfloat16_rn(x[i]);
+    else y[i] = __float2half_rn(x[i]);
+  }
+}
+
+wf_status launch_cast_f32(const float* x, void* y, long long n, wf_dtype to, cudaStream_t st, std::string* err) {
+  if (to == WF_BF16)
+    cast_f32_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(x, static_cast<__nv_bfloat16*>(y), n);
+  else if (to == WF_F16)
+    cast_f32_kernel<__half><<<grid_for(n), 256, 0, st>>>(x, static_cast<__half*>(y), n);
+  else {
+    *err = "cast: target dtype must be bf16 or f16";
+    return WF_INVALID_ARGUMENT;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("cast_f32_kernel: ") + cudaGetErrorString(e);
     return WF_CUDA_ERROR;
   }
   return WF_OK;

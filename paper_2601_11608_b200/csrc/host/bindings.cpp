@@ -101,6 +101,7 @@ wf::Graph graph_of(const py::list& nodes, const py::dict& weights) {
     n.pad_w = get_or<std::int64_t>(d, "pad_w", 0);
     n.factor = get_or<std::int64_t>(d, "factor", 0);
     n.bias = get_or<bool>(d, "bias", false);
+    n.dtype = dtype_of(get_or<std::string>(d, "dtype", "tf32"));
     g.nodes.push_back(std::move(n));
   }
   return g;
@@ -125,6 +126,7 @@ py::list nodes_of(const wf::Graph& g) {
     if (n.op == wf::OpKind::FoldedConv2d) {
       d["factor"] = n.factor;
       d["bias"] = n.bias;
+      d["dtype"] = n.dtype == wf::Dtype::BF16 ? "bf16" : (n.dtype == wf::Dtype::F16 ? "f16" : "tf32");
     }
     d["out_shape"] = n.out_shape;
     out.append(d);
@@ -318,9 +320,10 @@ PYBIND11_MODULE(_core, m) {
       py::arg("nodes"), py::arg("weights"), "Validate a graph and annotate out_shape (graph.hpp).");
   m.def(
       "width_fold_pass",
-      [](const py::list& nodes, const py::dict& weights, std::int64_t factor, std::int64_t align) {
+      [](const py::list& nodes, const py::dict& weights, std::int64_t factor, std::int64_t align,
+         const std::string& precision) {
         const wf::FoldFactor ff = factor > 0 ? wf::FoldFactor::fixed(factor) : wf::FoldFactor::automatic();
-        wf::PassResult r = wf::width_fold_pass(graph_of(nodes, weights), ff, align);
+        wf::PassResult r = wf::width_fold_pass(graph_of(nodes, weights), ff, align, dtype_of(precision));
         py::list decisions;
         for (const auto& d : r.report.decisions) {
           py::dict e;
@@ -340,7 +343,7 @@ PYBIND11_MODULE(_core, m) {
         for (const auto& kv : r.graph.weights) w[py::str(kv.first)] = to_array(kv.second);
         return py::make_tuple(nodes_of(r.graph), w, report);
       },
-      py::arg("nodes"), py::arg("weights"), py::arg("factor") = 0, py::arg("align") = 8,
+      py::arg("nodes"), py::arg("weights"), py::arg("factor") = 0, py::arg("align") = 8, py::arg("precision") = "tf32",
       "Rewrite-rule pass (src/pass.cpp:71): every conv2d the device fold applies to becomes folded_conv2d.");
   m.def(
       "interpret",

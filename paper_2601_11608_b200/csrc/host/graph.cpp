@@ -173,7 +173,7 @@ CostEstimate cost(const Graph& g0, std::int64_t align) {
     } else if (n.op == OpKind::FoldedConv2d) {
       const ConvSpec s = conv_spec_of(g, n);
       c.macs += count_macs(s);
-      c.issued_macs += plan_device_fold(s, n.factor, 0, Dtype::TF32).raw.issued_macs;
+      c.issued_macs += plan_device_fold(s, n.factor, 0, n.dtype).raw.issued_macs;
     } else if (n.op == OpKind::Matmul) {
       const Shape& a = g.find(n.inputs[0])->out_shape;
       const std::uint64_t m = static_cast<std::uint64_t>(a[0]) * a[1] * n.out_shape[1];
@@ -186,8 +186,10 @@ CostEstimate cost(const Graph& g0, std::int64_t align) {
 }
 
 // ---- the pass (src/pass.cpp:89-218, conv branch) ------------------------------------
-PassResult width_fold_pass(Graph g, FoldFactor factor, std::int64_t align) {
+PassResult width_fold_pass(Graph g, FoldFactor factor, std::int64_t align, Dtype precision) {
   if (align < 1) throw std::invalid_argument("alignment must be >= 1");
+  if (precision != Dtype::TF32 && precision != Dtype::BF16 && precision != Dtype::F16)
+    throw std::invalid_argument("pass precision must be tf32, bf16 or f16");
   if (!factor.is_auto() && *factor.value < 1) throw std::invalid_argument("fold factor must be >= 1");
   g = infer_shapes(std::move(g));
   RewriteReport report;
@@ -259,7 +261,7 @@ PassResult width_fold_pass(Graph g, FoldFactor factor, std::int64_t align) {
       out.push_back(node);
       continue;
     }
-    const DevicePlan dp = plan_device_fold(spec, factor.is_auto() ? 0 : *factor.value, 0, Dtype::TF32);
+    const DevicePlan dp = plan_device_fold(spec, factor.is_auto() ? 0 : *factor.value, 0, precision);
     if (!dp.plan.ok()) {
       report.decisions.push_back(skipped(node, dp.plan.reason, dp.plan.factor));
       out.push_back(node);
@@ -283,6 +285,7 @@ PassResult width_fold_pass(Graph g, FoldFactor factor, std::int64_t align) {
     Node folded = node;
     folded.op = OpKind::FoldedConv2d;
     folded.factor = dp.raw.f;
+    folded.dtype = precision;
     if (bias_node) {
       folded.bias = true;
       folded.inputs.push_back(bias_node->inputs[1]);
@@ -362,16 +365,29 @@ TensorMap interpret(const Graph& g0, const TensorMap& inputs, ExecMode mode) {
       }
       case OpKind::FoldedConv2d: {
         const ConvSpec s = conv_spec_of(g, n);
-        FoldedConv fc(s, Dtype::TF32, n.factor, 0);
+        FoldedConv fc(s, n.dtype, n.factor, 0);
         auto packed = dev_alloc(fc.packed_bytes());
         std::shared_ptr<void> brep;
         if (n.bias) brep = dev_alloc(static_cast<std::size_t>(fc.cout_f()) * sizeof(float));
-        fc.pack(val.at(n.inputs[1]).p, n.bias ? val.at(n.inputs[2]).p : nullptr, packed.get(),
+        // graph values are f32: a bf16/f16 node casts its input and filter on the device
+        const void* xin = val.at(n.inputs[0]).p;
+        const void* win = val.at(n.inputs[1]).p;
+        std::shared_ptr<void> x16, w16;
+        if (n.dtype != Dtype::TF32) {
+          const std::int64_t nx = numel(s.input_shape), nw = numel(s.filter_shape);
+          x16 = dev_alloc(static_cast<std::size_t>(nx) * 2);
+          w16 = dev_alloc(static_cast<std::size_t>(nw) * 2);
+          cast_f32(val.at(n.inputs[0]).p, x16.get(), nx, n.dtype, st);
+          cast_f32(val.at(n.inputs[1]).p, w16.get(), nw, n.dtype, st);
+          xin = x16.get();
+          win = w16.get();
+        }
+        fc.pack(win, n.bias ? val.at(n.inputs[2]).p : nullptr, packed.get(),
                 n.bias ? static_cast<float*>(brep.get()) : nullptr, st);
         std::shared_ptr<void> ws;
         if (fc.workspace_bytes()) ws = dev_alloc(fc.workspace_bytes());
         DevBuf y = make(n.out_shape);
-        fc.forward(val.at(n.inputs[0]).p, packed.get(), n.bias ? static_cast<float*>(brep.get()) : nullptr, y.p,
+        fc.forward(xin, packed.get(), n.bias ? static_cast<float*>(brep.get()) : nullptr, y.p,
                    Dtype::F32, n.bias, false, st, 0, ws.get());
         cuda_check(cudaStreamSynchronize(st), "folded conv");  // packed/brep/ws are freed below
         val[n.id] = y;

@@ -51,6 +51,7 @@ struct Node {
   std::int64_t pad_w = 0;
   std::int64_t factor = 0;     // FoldedConv2d: the device fold factor
   bool bias = false;           // FoldedConv2d: inputs[2] is a bias constant fused in the epilogue
+  Dtype dtype = Dtype::TF32;   // FoldedConv2d: tensor-core input dtype (TF32; BF16/F16 cast on the device)
   Shape out_shape;             // filled in by infer_shapes
 };
 
@@ -107,7 +108,9 @@ struct PassResult {
 // Rewrites every conv2d the device fold applies to into a FoldedConv2d
 // (TF32 tensor cores; a sole-consumer constant bias_add is fused). Never
 // fails on legality: skipped nodes carry their FoldReason. Idempotent.
-PassResult width_fold_pass(Graph g, FoldFactor factor, std::int64_t align);
+// precision: the folded nodes' tensor-core dtype -- TF32 (default; within
+// 1e-3 of the f32 graph) or BF16 / F16 (values cast on the device, 1e-2).
+PassResult width_fold_pass(Graph g, FoldFactor factor, std::int64_t align, Dtype precision = Dtype::TF32);
 
 enum class ExecMode { Dense, Grouped, Device };
 using TensorMap = std::map<std::string, HostTensor>;

@@ -234,6 +234,7 @@ json node_to_json(const Node& n) {
       j["pad"] = {n.pad_h, n.pad_w};
       j["factor"] = n.factor;
       j["bias"] = n.bias;
+      j["dtype"] = n.dtype == Dtype::BF16 ? "bf16" : (n.dtype == Dtype::F16 ? "f16" : "tf32");
       break;
     default:
       break;
@@ -271,6 +272,11 @@ Node node_from_json(const json& j) {
       if (n.op == OpKind::FoldedConv2d) {
         n.factor = j.at("factor").get<std::int64_t>();
         n.bias = j.value("bias", false);
+        const std::string dt = j.value("dtype", std::string("tf32"));
+        if (dt == "bf16") n.dtype = Dtype::BF16;
+        else if (dt == "f16") n.dtype = Dtype::F16;
+        else if (dt == "tf32") n.dtype = Dtype::TF32;
+        else throw ManifestParse("folded_conv2d '" + n.id + "': unknown dtype '" + dt + "'");
       }
       break;
     default:

@@ -171,6 +171,10 @@ void bias_add(const float* y, const float* b, float* out, std::int64_t n, std::i
   throw_on(wf_bias_add(y, b, out, n, c, relu ? 1 : 0, stream));
 }
 
+void cast_f32(const float* x, void* y, std::int64_t n, Dtype to, void* stream) {
+  throw_on(wf_cast_f32(x, y, n, static_cast<wf_dtype>(to), stream));
+}
+
 void replicate_bias(const float* b, std::int64_t cout, std::int64_t factor, float* out, void* stream) {
   throw_on(wf_replicate_bias(b, cout, factor, out, stream));
 }

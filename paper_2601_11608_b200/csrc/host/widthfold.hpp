@@ -117,6 +117,8 @@ MacReport mac_report(const ConvSpec& spec, const FoldPlan& plan, std::int64_t al
 // Exact-order fp32 conv2d + optional bias/ReLU (reference conv2d/bias_add bits).
 void conv2d_exact(const float* x, const float* w, float* y, const ConvSpec& spec, void* stream);
 void bias_add(const float* y, const float* b, float* out, std::int64_t n, std::int64_t c, bool relu, void* stream);
+// y = (bf16 | f16) x on the device (round to nearest even)
+void cast_f32(const float* x, void* y, std::int64_t n, Dtype to, void* stream);
 void replicate_bias(const float* b, std::int64_t cout, std::int64_t factor, float* out, void* stream);
 // Reference expand_filter_general (KW must be 1 -> IllegalFold), fp32 device.
 void expand_filter_general(const float* w, const Shape& filter_shape, std::int64_t factor, float* out, void* stream);

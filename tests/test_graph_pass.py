@@ -128,3 +128,31 @@ def test_pass_soundness_on_random_graphs():
                 err = np.max(np.abs(y1[k] - y0[k])) / max(np.max(np.abs(y0[k])), 1e-30)
                 assert err <= 1e-3, (seed, k, err)
     assert applied >= 50  # most random first layers fold
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["bf16", "f16"])
+def test_pass_at_16_bit_precision(precision, tmp_path):
+    """width_fold_pass(precision=bf16/f16): folded nodes cast their f32 input and
+    filter on the device; integer graphs stay exact (small integers are exact in
+    16 bits), real-valued ones within 1e-2; the node dtype survives write/read."""
+    applied = 0
+    for seed in range(20):
+        integer = seed % 2 == 0
+        g, inputs = random_graph(seed, integer)
+        g2, rep = wf.width_fold_pass(g, precision=precision)
+        applied += rep["applied_count"]
+        assert all(n.get("dtype") == precision for n in g2.nodes if n["op"] == "folded_conv2d")
+        y0 = wf.interpret(g, inputs, mode="dense")
+        y1 = wf.interpret(g2, inputs, mode="device")
+        for k in y0:
+            if integer:
+                np.testing.assert_array_equal(y1[k], y0[k], err_msg=f"seed {seed} output {k}")
+            else:
+                err = np.max(np.abs(y1[k] - y0[k])) / max(np.max(np.abs(y0[k])), 1e-30)
+                assert err <= 1e-2, (seed, k, err)
+        if seed == 0:
+            wf.write_graph(g2, tmp_path / "g.json")
+            back = wf.read_graph(tmp_path / "g.json")
+            assert [n.get("dtype") for n in back.nodes] == [n.get("dtype") for n in g2.nodes]
+    assert applied >= 10
