@@ -176,7 +176,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   if (const char* env = std::getenv("WF_EPI_PP")) a.epi_pp = (env[0] == '1' && S.pair == 1) ? 1 : 0;
   a.epi_flags = static_cast<int>(epilogue);
   // shared-memory carve-up (offsets from the 1024-aligned base)
-  a.off_a = 1024;
+  a.off_a = kCtrlBytes;
   a.off_b = a.off_a + a.stages * a.stage_bytes + kTileM * 16;
   a.off_b = (a.off_b + 127) / 128 * 128;
   a.off_bias = a.off_b + S.b_smem_bytes;

@@ -503,8 +503,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   const uint32_t bar_tempty_hi = base + 448;  // [n_acc] x 8 B: upper half drained
   const uint32_t bar_bpeer = base + 184;      // pair: the peer's B half landed (leader's barrier)
   const uint32_t bar_b = base + 160;
-  const uint32_t bar_raw_full = base + 256;   // [raw_slots <= 16] x 8 B
-  const uint32_t bar_raw_empty = base + 512;  // [raw_slots <= 16] x 8 B
+  const uint32_t bar_raw_full = base + 1024;   // [raw_slots <= 32] x 8 B
+  const uint32_t bar_raw_empty = base + 1280;  // [raw_slots <= 32] x 8 B (control area: kCtrlBytes)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + 192);
 
   // warp index via shuffle so the compiler knows it is warp-uniform (keeps the

@@ -603,7 +603,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   };
 
   // ---- N-tiles and shared-memory budget ------------------------------------
-  const int ctrl_bytes = 1024;
+  const int ctrl_bytes = kCtrlBytes;
   const int staging = kStagingBytes;   // 4 epilogue warps x 2 x 2 KB
   const int a_pad = kTileM * 16;
   const int bias_bytes = kMaxAccCols * 4;
@@ -922,7 +922,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
       for (const auto& t : S.ntiles) max_b = std::max(max_b, t.b_bytes / 2);
       S.pair = 2;
       S.b_smem_bytes = static_cast<int>((max_b + 127) / 128 * 128);
-      const int64_t fixed = 1024 + kTileM * 16 + 128 + S.b_smem_bytes + kMaxAccCols * 4 + 1024;
+      const int64_t fixed = kCtrlBytes + kTileM * 16 + 128 + S.b_smem_bytes + kMaxAccCols * 4 + 1024;
       for (int st2 = 6; st2 >= 2; --st2)
         if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { S.stages = st2; break; }
     }
@@ -976,7 +976,7 @@ wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Sched
   const int64_t b_total = d.kh * U * d.cout * 32;
   S.raw_slots = kRawSlots;
   S.raw_slot_bytes = raw_slot_bytes_for(d.w * d.c * S.esize);
-  const int64_t fixed0 = 1024 + kTileM * 16 + 128 + (b_total + 127) / 128 * 128 + kMaxAccCols * 4 +
+  const int64_t fixed0 = kCtrlBytes + kTileM * 16 + 128 + (b_total + 127) / 128 * 128 + kMaxAccCols * 4 +
                          static_cast<int64_t>(S.raw_slots) * S.raw_slot_bytes + 1024;
   int64_t ksplit = 1;
   while (ksplit < 8 && fixed0 + 2 * ceil_div(d.kh, ksplit) * U * region > kSmemLimit) ++ksplit;

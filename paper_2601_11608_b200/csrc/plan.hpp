@@ -48,7 +48,8 @@ constexpr int kMaxResidues = 8;
 constexpr int kMaxNTiles = 16;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kStagingBytes = 0;  // epilogue writes straight from registers (no staging)
-constexpr int kRawSlots = 16;     // staged-row ring slots (row producer)
+constexpr int kRawSlots = 32;     // staged-row ring slots (row producer; >= the raw rows of a stage)
+constexpr int kCtrlBytes = 2048;  // barriers, TMEM slot, row table at the base of shared memory
 inline int raw_slot_bytes_for(int64_t row_bytes) { return static_cast<int>((row_bytes + 32 + 127) / 128 * 128); }
 
 // Output-column permutation inside an epilogue chunk of CH accumulator
