@@ -57,19 +57,30 @@ def gather_scalars(values: list[float], device: torch.device | str = "cpu") -> l
 def gather_to(tensor: torch.Tensor, sizes: list[int], dst: int = 0) -> torch.Tensor | None:
     """Concatenate every rank's leading-dimension shard on rank ``dst`` (the
     shards may differ in length by one; ``sizes`` are all ranks' lengths).
-    Verification / collection only -- never on the hot path. NCCL on CUDA
-    tensors, gloo on CPU ones; identity when not distributed."""
+    Verification / collection only -- never on the hot path. Each rank sends
+    its shard straight into its slice of ``dst``'s output (grouped
+    point-to-point ops: NCCL send/recv on CUDA tensors, gloo on CPU ones), so
+    ``dst`` holds the output once and no other rank receives anything; an
+    all-gather would land all 8 x 13.15 GB of the R50 b8192 output on every
+    rank. Identity when not distributed."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return tensor
     rank, world = dist.get_rank(), dist.get_world_size()
-    biggest = max(sizes)
-    pad = torch.zeros((biggest,) + tuple(tensor.shape[1:]), dtype=tensor.dtype, device=tensor.device)
-    pad[: tensor.shape[0]] = tensor
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad)  # all_gather: NCCL has no gather of unequal shards
-    if rank != dst:
+    if len(sizes) != world or tensor.shape[0] != sizes[rank]:
+        raise ValueError(f"shard sizes {sizes} do not match rank {rank}'s {tuple(tensor.shape)}")
+    if rank != dst:  # every rank joins a grouped call (NCCL needs all ranks in a first one)
+        ops = [dist.P2POp(dist.isend, tensor.contiguous(), dst)] if sizes[rank] > 0 else []
+        for req in (dist.batch_isend_irecv(ops) if ops else []):
+            req.wait()
         return None
-    return torch.cat([p[:n] for p, n in zip(parts, sizes)], dim=0)
+    out = torch.empty((sum(sizes),) + tuple(tensor.shape[1:]), dtype=tensor.dtype, device=tensor.device)
+    offs = [sum(sizes[:r]) for r in range(world)]
+    out[offs[dst]:offs[dst] + sizes[dst]] = tensor
+    ops = [dist.P2POp(dist.irecv, out[offs[r]:offs[r] + sizes[r]], r)
+           for r in range(world) if r != dst and sizes[r] > 0]
+    for req in (dist.batch_isend_irecv(ops) if ops else []):
+        req.wait()
+    return out
 
 
 class ShardedConv:

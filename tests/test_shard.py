@@ -80,3 +80,44 @@ def test_two_rank_gloo_shard_and_reduce():
         else:
             assert full is None  # max over ranks, as bench.py times multi-GPU runs
         assert got == [[0.0, 4096.0, 10.0], [4096.0, 8192.0, 11.0]]
+
+
+def _gather_worker(rank, world, port, dst, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import torch.distributed as dist
+    shard.init("gloo")
+    try:
+        sizes = [b - a for a, b in (shard.shard_range(n, k, world) for k in range(world))]
+        a, b = shard.shard_range(n, rank, world)
+        mine = torch.arange(a * 6, b * 6, dtype=torch.float32).reshape(-1, 2, 3)
+        full = shard.gather_to(mine, sizes, dst=dst)
+        bad = None
+        try:
+            shard.gather_to(mine[:0] if sizes[rank] else torch.zeros(1, 2, 3), sizes, dst=dst)
+        except ValueError as e:
+            bad = str(e)
+        q.put((rank, None if full is None else full.tolist(), bad is not None))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dst,n", [(3, 1, 7), (4, 3, 2)])
+def test_gather_to_lands_only_on_dst(world, dst, n):
+    """gather_to: point-to-point sends into dst's slices (unequal and empty shards, dst != 0);
+    the other ranks receive nothing; a shard that does not match its size is rejected."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, dst, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = torch.arange(n * 6, dtype=torch.float32).reshape(n, 2, 3).tolist()
+    for r, full, rejected in res:
+        assert full == (want if r == dst else None)
+        assert rejected
