@@ -252,7 +252,7 @@ def run_gpu(args) -> None:
                               STRIDE, PAD)
         got = y[i:i + 1].float().cpu().numpy()
         err = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
-        csum = float(y.double().sum().item())
+        csum = float(y.sum(dtype=torch.float64).item())  # no 52 GB float64 copy of the output
         verify = shard.gather_scalars([float(lo + i), err, csum], dev)
 
     # ---- variants of the same kernel: zero-padded Cin 3 -> 8 (f=2) and unfolded Cin=3 ----
