@@ -741,6 +741,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // profiling (0x80000, CTA 0): cycles the issuer waits on the accumulator / the A stage
     const bool dbg = (a.epi_flags & 0x80000) && blockIdx.x == 0;
     long long w_acc = 0, w_full = 0, w_hi = 0, t_all = dbg ? clock64() : 0;
+    unsigned long long ns_all = 0;  // wall time of the same span: cycles / ns = the SM clock it ran at
+    if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_all));
     int tile = 0;
     int stage_c = 0;           // A stage of the next sub-stage (kept incrementally: no division per tile)
     uint32_t round_c = 0;      // its fill round
@@ -810,8 +812,13 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
        if (++stage_c == stages) { stage_c = 0; ++round_c; }
     }
     if (dbg && leader)
-      printf("mma issuer cta0: %d tiles, %lld cycles: wait accumulator %lld (upper half %lld), wait A stage %lld\n",
-             tile, clock64() - t_all, w_acc, w_hi, w_full);
+    {
+      unsigned long long ns_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_end));
+      const long long cyc = clock64() - t_all;
+      printf("mma issuer cta0: %d tiles, %lld cycles in %llu ns (%.0f MHz): wait accumulator %lld (upper half %lld), "
+             "wait A stage %lld\n", tile, cyc, ns_end - ns_all, 1e3 * cyc / (double)(ns_end - ns_all), w_acc, w_hi, w_full);
+    }
     }
   mma_done:;
   } else if (warp >= 2 && warp < 10) {

@@ -173,6 +173,110 @@ double run(const Args& a, unsigned long long* d, int iters) {
   return (double)mx / iters;
 }
 
+// Kernel-shaped launches (item 1): 320 threads like conv_fold_kernel.
+//   K=0 warps 2..9 parked on an mbarrier for the whole launch
+//   K=1 + the kernel's per-tile accumulator handshake: the issuer commits to
+//       tfull[acc] and waits tempty[acc] (2 buffers); warps 2..9 wait tfull,
+//       fence, arrive tempty (the MMA-only kernel's epilogue)
+//   K=2 K=1 + the epilogue reads its 32 lanes x 256 columns with tcgen05.ld
+template <int K>
+__global__ void __launch_bounds__(320, 1) probe_k(const __grid_constant__ Args a, int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar_end, tfull[2], tempty[2];
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const uint32_t base = (smem_u32(smem) + 1023) & ~1023u;
+  for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) ((uint32_t*)smem)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar_end), 1);
+    for (int k = 0; k < 2; ++k) { mbar_init(smem_u32(&tfull[k]), 1); mbar_init(smem_u32(&tempty[k]), 256); }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(smem_u32(&tslot), 512);
+  asm volatile("fence.proxy.async.shared::cta;");
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp == 1) {
+    const uint32_t a_hi = (1u << 14) | (128u >> 4);
+    const uint32_t b_lo = (base + 96 * 1024) >> 4;
+    const bool leader = elect_one();
+    const int entries = a.n;
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int acc = it & 1;
+      if (K >= 1) { mbar_wait(smem_u32(&tempty[acc]), ((it >> 1) & 1) ^ 1); tc_fence_after(); }
+      const uint32_t d_base = tmem + acc * 256;
+      const uint32_t a_lo = (base + (it & 1) * 32768) >> 4;
+      int i = 0;
+      for (; i + 8 <= entries; i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 e = a.table[i + j];
+          const uint64_t adesc = (static_cast<uint64_t>(a_hi) << 32) | (e.x + a_lo);
+          const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
+          if (leader) mma<0>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
+        }
+      }
+      for (; i < entries; ++i) {
+        const uint4 e = a.table[i];
+        const uint64_t adesc = (static_cast<uint64_t>(a_hi) << 32) | (e.x + a_lo);
+        const uint64_t bdesc = (static_cast<uint64_t>(0x4008u) << 32) | (e.y + b_lo);
+        if (leader) mma<0>(d_base + e.w, adesc, bdesc, e.z & 0x7FFFFFFFu, e.z >> 31);
+      }
+      if (K >= 1 && leader) mma_commit(smem_u32(&tfull[acc]));
+      __syncwarp();
+    }
+    if (leader) mma_commit(smem_u32(&bar_end));
+    __syncwarp();
+    mbar_wait(smem_u32(&bar_end), 0);
+    if (threadIdx.x == 32) out[blockIdx.x] = clock64() - t0;
+  } else if (warp >= 2) {
+    if (K == 0) {
+      mbar_wait(smem_u32(&bar_end), 0);
+    } else {
+      const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+      float sink = 0.f;
+      for (int it = 0; it < iters; ++it) {
+        const int acc = it & 1;
+        mbar_wait(smem_u32(&tfull[acc]), (it >> 1) & 1);
+        tc_fence_after();
+        if (K == 2) {
+          uint32_t r[32];
+          const uint32_t col = acc * 256 + (warp >= 6 ? 128 : 0);
+          for (int c = 0; c < 128; c += 32) {
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                         : "r"(tmem + lane_base + col + c));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            for (int q = 0; q < 32; ++q) sink += __uint_as_float(r[q]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty[acc]));
+      }
+      if (sink == 1234.5f) out[0] = 0;
+    }
+  }
+  tc_fence_before(); __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+template <int K>
+double run_k(const Args& a, unsigned long long* d, int iters) {
+  cudaFuncSetAttribute(probe_k<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+  probe_k<K><<<148, 320, 210 * 1024>>>(a, iters, d);
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  std::vector<unsigned long long> h(148);
+  cudaMemcpy(h.data(), d, 8 * 148, cudaMemcpyDeviceToHost);
+  unsigned long long mx = 0;
+  for (auto v : h) mx = v > mx ? v : mx;
+  return (double)mx / iters;
+}
+
 int main(int argc, char** argv) {
   FILE* f = fopen(argc > 1 ? argv[1] : "gpurun_out/sched_kpair.txt", "r");
   if (!f) { printf("no table\n"); return 1; }
@@ -208,5 +312,8 @@ int main(int argc, char** argv) {
   for (int i = a.n; i < 384; ++i) big.table[i] = make_uint4(i, i, i, i);
   printf("big param block       %8.1f cycles/tile\n", run_big(big, d, iters, 0));
   printf("big + noise warps     %8.1f cycles/tile\n", run_big(big, d, iters, 1));
+  printf("k0 320 thr, parked    %8.1f cycles/tile\n", run_k<0>(a, d, iters));
+  printf("k1 + acc handshake    %8.1f cycles/tile\n", run_k<1>(a, d, iters));
+  printf("k2 + tcgen05.ld drain %8.1f cycles/tile\n", run_k<2>(a, d, iters));
   return 0;
 }
