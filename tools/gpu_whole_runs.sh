@@ -1,4 +1,5 @@
 #!/bin/bash
+# Historical: the 0x2000 switch existed only for this experiment; it is a no-op on main.
 # Issue path A/B: whole unrolled runs of the 21/28-entry schedules (default)
 # vs rolled groups of 7 (profiling switch 0x2000); full kernel and MMA-only
 # (0x1200), short runs, then the GPU parity suite and the sustained bench.
