@@ -333,7 +333,14 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     return WF_UNSUPPORTED;
   }
   const int kind = tf32 ? 1 : 0;
-  if ((prod == 0 || prod == 3) && S.pair == 2)
+  // two N-tiles as a 2-CTA cluster sharing each A stage by multicast
+  // (AlexNet 1.08-1.15x, VGG neutral; WF_MCAST=0 turns it off)
+  const char* mc_env = std::getenv("WF_MCAST");
+  const bool mc = !(mc_env && mc_env[0] == '0') && (prod == 0 || prod == 3) && S.pair == 1 && !tf32 &&
+                  a.n_tiles == 2 && a.ksplit == 1 && grid % 2 == 0;
+  if (mc)
+    e = launch_conv_mc(a, maps, grid, smem, st, out_dtype, S.CH);
+  else if ((prod == 0 || prod == 3) && S.pair == 2)
     e = launch_conv_pair(a, maps, grid, smem, st, out_dtype, S.CH);
   else if (prod == 0 || prod == 3)
     e = launch_conv_prod<0>(a, maps, grid, smem, st, kind, out_dtype, S.CH);

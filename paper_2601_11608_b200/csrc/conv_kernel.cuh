@@ -488,7 +488,12 @@ __device__ __forceinline__ void arrive_at(uint32_t bar) {
 // kPair = 2: a cluster of two CTAs (one per SM of a TPC) runs cta_group::2
 // MMAs -- M = 256 (each CTA's 128-row tile), each CTA holding half of every B
 // block, so the per-SM shared-memory operand traffic drops by the B half.
-template <int kKind, typename OutT, int CH, int kProd, int kPair = 1>
+// kMc = 1: the two N-tiles of a plan run as a 2-CTA cluster walking the same
+// M tiles; each CTA issues the TMA boxes of every other residue with
+// .multicast::cluster so both receive the whole A stage and each SM's TMA
+// unit issues half of the pieces; a stage is refilled only after both CTAs'
+// MMAs released it (multicast commits, empty barriers of count 2).
+template <int kKind, typename OutT, int CH, int kProd, int kPair = 1, int kMc = 0>
 __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     conv_fold_kernel(const __grid_constant__ ConvArgs a, const __grid_constant__ TmaMaps maps) {
   using namespace ptx;
@@ -512,6 +517,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const uint32_t rank = (kPair == 2) ? cluster_ctarank() : 0u;  // 0: pair leader (issues the MMAs)
+  const uint32_t mrank = kMc ? cluster_ctarank() : 0u;           // multicast cluster: this CTA's residue half
   const int cl = static_cast<int>(blockIdx.x) / kPair;           // cluster (or CTA) index
   const int ntile = cl % a.n_tiles;
   const int local = cl / a.n_tiles;                               // first M-tile unit of this CTA
@@ -531,7 +537,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
       mbar_init(bar_full + 8 * i, kProd == 0 ? 1 : kGatherWarps);  // TMA: one expect_tx; rows: one arrive per transposer
-      mbar_init(bar_empty + 8 * i, 1);
+      mbar_init(bar_empty + 8 * i, (kMc && !(a.epi_flags & 0x2000)) ? 2 : 1);  // multicast: both CTAs' MMAs release the stage
     }
     for (int i = 0; i < a.n_acc; ++i) {
       mbar_init(bar_tfull + 8 * i, 1);
@@ -559,7 +565,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     else tmem_alloc(smem_u32(tmem_slot), a.tmem_cols);
   }
   tc_fence_before();
-  if constexpr (kPair == 2) cluster_sync();  // the peer's barriers are initialised before remote use
+  if constexpr (kPair == 2 || kMc) cluster_sync();  // the peer's barriers are initialised before remote use
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -686,11 +692,14 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         }
         if (rank == 0) mbar_arrive_expect_tx(bar_full + 8 * stage, txs * kPair);
         if (a.sw32) {  // one SWIZZLE_32B box of 32-byte K-step pieces per (residue, in-pixel offset)
-          for (int b = 0; b < a.s; ++b) {
+          for (int b = 0, j = 0; b < a.s; ++b) {
             if (!((a.res_mask >> b) & 1u)) continue;
+            if (kMc && ((j++ & 1) != static_cast<int>(mrank))) continue;  // the peer multicasts this residue
             for (int qi = 0; qi < a.nq; ++qi) {
               const uint32_t dq = dst + b * a.region_bytes + qi * a.qregion_bytes;
-              if constexpr (kPair == 2)
+              if constexpr (kMc)
+                tma_load_4d_mc(dq, &maps.in[b], a.qcoord[qi], a.c0, oh0 + a.amin[b], n, fbar, 0x3);
+              else if constexpr (kPair == 2)
                 tma_load_4d_pair(dq, &maps.in[b], a.qcoord[qi], a.c0, oh0 + a.amin[b], n, fbar);
               else
                 tma_load_4d(dq, &maps.in[b], a.qcoord[qi], a.c0, oh0 + a.amin[b], n, fbar);
@@ -698,10 +707,19 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
           }
           continue;
         }
-        for (int b = 0; b < a.s; ++b) {
+        for (int b = 0, j = 0; b < a.s; ++b) {
           if (!((a.res_mask >> b) & 1u)) continue;
           if (dbg_oneres && b != __ffs(a.res_mask) - 1) continue;
-          if constexpr (kPair == 2) {
+          // profiling 0x2000: every CTA loads every residue into itself only (cluster sync logic alone)
+          const bool mc_self = (a.epi_flags & 0x2000) != 0;
+          if (kMc && !mc_self && ((j++ & 1) != static_cast<int>(mrank))) continue;  // the peer multicasts this residue
+          if constexpr (kMc) {
+            const uint16_t mask = mc_self ? static_cast<uint16_t>(1u << mrank) : static_cast<uint16_t>(0x3);
+            tma_load_5d_mc(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, fbar, mask);
+            if (a.shift_box_bytes && !dbg_noshift)
+              tma_load_5d_mc(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1,
+                             oh0 + a.amin[b], 0, n, fbar, mask);
+          } else if constexpr (kPair == 2) {
             tma_load_5d_pair(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, fbar);
             if (a.shift_box_bytes && !dbg_noshift)
               tma_load_5d_pair(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1,
@@ -722,7 +740,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     // uniform registers straight from the constant bank; one lane issues.
     const bool skip_mma = (a.epi_flags & 0x100) != 0;  // profiling switch
     const bool no_wait = (a.epi_flags & 0x200000) != 0;  // profiling: issue the schedule back to back (with 0x1200)
-    const uint32_t b_lo = (base + a.off_b) >> 4;
+    // descriptor start fields are 14-bit CTA-local offsets (>> 4): in a
+    // cluster launch a rank-1 CTA's shared::cta addresses carry 0x1000000,
+    // which must not spill into the LBO field
+    const uint32_t b_lo = ((base + a.off_b) & 0x3FFFFu) >> 4;
     const uint32_t a_hi = a.a_desc_hi;
     const bool leader = elect_one() && rank == 0;  // pair: the leader CTA issues for both SMs
     if (kPair == 2 && rank != 0) goto mma_done;
@@ -769,7 +790,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         if (k == 0 && !no_wait) mbar_wait(bar_full + 8 * stage, round & 1u);
         if (dbg) { const long long t1 = clock64(); w_full += t1 - t0; t0 = t1; }
         tc_fence_after();
-        const uint32_t a_lo = (a_base + stage * stage_bytes + k * tile_shift) >> 4;
+        const uint32_t a_lo = ((a_base + stage * stage_bytes + k * tile_shift) & 0x3FFFFu) >> 4;
         if (!skip_mma) {
           int i = 0;
           if (split > 0) {  // lower half first, then wait for the epilogue to drain the upper half
@@ -803,7 +824,13 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         else if (split > 0) {
           mbar_wait(bar_tempty_hi + 8 * acc, (acc_round & 1u) ^ 1u);
         }
-        if (leader && k == tps - 1) commit_to<kPair>(bar_empty + 8 * stage);  // last tile frees the stage
+        if (leader && k == tps - 1) {  // last tile frees the stage (multicast: in both CTAs)
+          if constexpr (kMc) {
+            if (a.epi_flags & 0x2000) mma_commit(bar_empty + 8 * stage);
+            else mma_commit_mc(bar_empty + 8 * stage, 0x3);
+          }
+          else commit_to<kPair>(bar_empty + 8 * stage);
+        }
       }
       if (leader) commit_to<kPair>(bar_tfull + 8 * acc);
       __syncwarp();
@@ -988,7 +1015,9 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   }
 
   tc_fence_before();
-  if constexpr (kPair == 2) cluster_sync();  // the leader's MMAs wrote this CTA's TMEM
+  // pair: the leader's MMAs wrote this CTA's TMEM; multicast: no CTA leaves
+  // while the peer may still commit to its barriers
+  if constexpr (kPair == 2 || kMc) cluster_sync();
   else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -1060,6 +1089,34 @@ cudaError_t launch_pair_typed(const ConvArgs& args, const TmaMaps& maps, int gri
 
 cudaError_t launch_conv_pair(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st,
                              wf_dtype out, int ch);
+
+// 2-CTA N-tile cluster with multicast A loads (kMc = 1), TMA producer, kind::f16.
+template <typename OutT, int CH>
+cudaError_t launch_mc_typed(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st) {
+  auto kern = conv_fold_kernel<0, OutT, CH, 0, 1, 1>;
+  static int configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args, maps);
+}
+
+cudaError_t launch_conv_mc(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st,
+                           wf_dtype out, int ch);
 
 extern template cudaError_t launch_conv_prod<0>(const ConvArgs&, const TmaMaps&, int, int, cudaStream_t, int, wf_dtype,
                                                 int);
