@@ -488,3 +488,23 @@ def test_reference_acceptance_sweep_on_device():
                         np.testing.assert_array_equal(got, want, err_msg=f"F={F} K={K} H={H} W={W} Co={Co}")
                         cases += 1
     assert cases == 336
+
+
+@pytest.mark.parametrize("n,h,k,co,s,p", [(64, 227, 11, 96, 4, 0), (7, 227, 11, 96, 4, 0), (16, 224, 3, 64, 1, 1)])
+def test_multicast_cluster_matches_single_cta(monkeypatch, n, h, k, co, s, p):
+    """Two-N-tile plans run as a 2-CTA cluster sharing A stages by TMA multicast
+    (the default); WF_MCAST=0 forces the single-CTA launch. Bit-identical."""
+    torch.manual_seed(5)
+    x = torch.randn(n, h, h, 3, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(k, k, 3, co, device="cuda") * 0.1).to(torch.bfloat16)
+    b = torch.randn(co, device="cuda")
+    conv = wf.FoldedConv2d(w, b, x.shape, stride=s, padding=p, dtype=torch.bfloat16)
+    assert conv.device_plan["n_tiles"] == 2
+    y_mc = conv(x)
+    monkeypatch.setenv("WF_MCAST", "0")
+    y_one = conv(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y_mc, y_one)
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(3, 2, 0, 1), b, stride=s,
+                                     padding=p).permute(0, 2, 3, 1)
+    assert ((y_mc.float() - ref).norm() / ref.norm()).item() < 1e-2
