@@ -72,7 +72,12 @@ typedef enum {
 
 typedef enum { WF_FOLD_APPLY = 0, WF_FOLD_FALLBACK = 1 } wf_fold_status;
 
-typedef enum { WF_EPI_NONE = 0, WF_EPI_BIAS = 1, WF_EPI_RELU = 2 } wf_epilogue;
+/* Epilogue flags of wf_conv_fold_fwd[_ws]. WF_EPI_ROW_PRODUCER is a
+ * cross-check, not a fast path: it builds the TMA-layout A tile with the
+ * row-gather producer instead (same shared-memory image, bit-identical
+ * output). Any other bit is rejected with WF_INVALID_ARGUMENT (profiling
+ * switches exist only in a WFB_PROFILE=1 build of the library). */
+typedef enum { WF_EPI_NONE = 0, WF_EPI_BIAS = 1, WF_EPI_RELU = 2, WF_EPI_ROW_PRODUCER = 0x4000 } wf_epilogue;
 
 /* Kernel variant: the width-folded conv, or the same tcgen05 kernel on the
  * unfolded Cin=C input (explicit im2col A tiles) for the comparison. The
@@ -123,7 +128,11 @@ typedef struct {
                               output-row bands share their input-row halo */
   int32_t kstep_mode;      /* MMA K-steps: 0 32-byte covers of each kh row's
                               window, 1 cross-kh pairs of 16-byte core columns */
-  int32_t reserved0;
+  int32_t launch_opts;     /* launch tuning decided at plan time (never read
+                              from the environment at launch): bit 0 two TMEM
+                              accumulator buffers only, bits 1-2 epilogue
+                              ping-pong (0 auto, 1 off, 2 on), bit 3 no
+                              multicast N-tile cluster */
   int64_t pitched_w;       /* producer 3: workspace row width (>= W, % f == 0) */
   int64_t workspace_bytes; /* device scratch wf_conv_fold_fwd_ws needs (0: none) */
   uint64_t useful_macs;    /* count_macs of the original conv */

@@ -22,6 +22,7 @@ WF_F32, WF_TF32, WF_BF16, WF_F16 = 0, 1, 2, 3
 WF_FOLD_APPLY, WF_FOLD_FALLBACK = 0, 1
 # wf_epilogue
 WF_EPI_NONE, WF_EPI_BIAS, WF_EPI_RELU = 0, 1, 2
+WF_EPI_ROW_PRODUCER = 0x4000  # cross-check: the row-gather producer builds the TMA A layout
 
 # FoldReason strings, same order as include/widthfold/fold.hpp:14-23 and
 # src/fold.cpp:8-20, plus the two the generalized device fold adds.
@@ -52,7 +53,7 @@ class FoldPlan(ctypes.Structure):
         ("units_per_px", c_int64), ("group_size", c_int64), ("n_groups", c_int64),
         ("n_tiles", c_int64), ("tile_rows", c_int64), ("wbox", c_int64), ("nrows", c_int64),
         ("mma_entries", c_int64), ("table_bytes", c_int64), ("packed_bytes", c_int64), ("epi_chunk", c_int64), ("variant", c_int32), ("producer", c_int32), ("cta_pair", c_int32),
-        ("stage_tiles", c_int32), ("kstep_mode", c_int32), ("reserved0", c_int32),
+        ("stage_tiles", c_int32), ("kstep_mode", c_int32), ("launch_opts", c_int32),
         ("pitched_w", c_int64), ("workspace_bytes", c_int64),
         ("useful_macs", c_uint64), ("issued_macs", c_uint64),
     ]

@@ -129,7 +129,15 @@ class FoldedConv2d:
         return self.core.device
 
     def __call__(self, x: torch.Tensor, *, relu: bool = False, bias: bool = True, out: torch.Tensor | None = None,
-                 out_dtype: torch.dtype | None = None, _profile_flags: int = 0) -> torch.Tensor:
+                 out_dtype: torch.dtype | None = None) -> torch.Tensor:
+        """y = ReLU?(conv(x, w) + b) into ``out`` (allocated when None), stream-ordered."""
+        return self._forward(x, relu=relu, bias=bias, out=out, out_dtype=out_dtype, flags=0)
+
+    def _forward(self, x: torch.Tensor, *, relu: bool = False, bias: bool = True, out: torch.Tensor | None = None,
+                 out_dtype: torch.dtype | None = None, flags: int = 0) -> torch.Tensor:
+        """__call__ with extra wf_conv_fold_fwd epilogue bits: tests and tools
+        only (``_abi.WF_EPI_ROW_PRODUCER`` cross-check; the 0xFFFF00 profiling
+        switches need a ``make PROFILE=1`` build and are rejected otherwise)."""
         if not (isinstance(x, torch.Tensor) and x.is_cuda):
             raise ValueError("FoldedConv2d takes a CUDA tensor (use conv2d() for numpy inputs)")
         if x.dtype != self.dtype:
@@ -144,7 +152,7 @@ class FoldedConv2d:
             raise ShapeMismatchError("output buffer has the wrong shape/dtype/layout")
         use_bias = bias and self.b_rep is not None
         self.core.forward(x.data_ptr(), self.packed.data_ptr(), _ptr(self.b_rep) if use_bias else 0,
-                          out.data_ptr(), _OUT_NAME[out_dtype], use_bias, relu, _stream(x.device), _profile_flags,
+                          out.data_ptr(), _OUT_NAME[out_dtype], use_bias, relu, _stream(x.device), int(flags),
                           _ptr(self.workspace))
         return out
 
@@ -167,19 +175,32 @@ class FoldedConv2d:
         torch.cuda.current_stream(x.device).wait_stream(side)
         return graph.replay, out
 
+    # plan fields that scale with the batch but leave the packed operand (the
+    # schedule table + B layout) unchanged; every other field must match to share it
+    _BATCH_COUNTERS = ("useful_macs", "issued_macs", "workspace_bytes")
+
     def with_batch(self, n: int) -> "FoldedConv2d":
-        """Same filter for batch ``n`` -- shares the packed operand (the pack is batch-independent)."""
+        """Same filter for batch ``n``, with its own workspace. The packed operand
+        is shared when the batch-``n`` plan has the same schedule (N-tiling,
+        stage tiles, CTA pairs, K-step mode...); otherwise the filter is packed
+        again for the new plan (a batch-dependent planner choice never runs
+        against a mismatched operand)."""
         other = object.__new__(FoldedConv2d)
         other.__dict__.update(self.__dict__)
         shape = (int(n),) + self.input_shape[1:]
         sh, sw, ph, pw = self._geom
-        w = self._keep[0]
+        w, bf = self._keep
         other.core = _core.FoldedConv(list(shape), list(w.shape), sh, sw, ph, pw, _DT_NAME[self.dtype],
                                       self.core.device["f"] if self.variant == "fold" else 0,
                                       self.core.device["group_size"] if self.variant == "fold" else 0, self.variant)
-        if other.core.packed_bytes != self.core.packed_bytes:
-            raise UnsupportedError("batch-specific plan changed the packed operand")
-        other.workspace = (torch.empty(other.core.workspace_bytes, dtype=torch.uint8, device=self.packed.device)
+        mine = {k: v for k, v in self.core.device.items() if k not in self._BATCH_COUNTERS}
+        theirs = {k: v for k, v in other.core.device.items() if k not in self._BATCH_COUNTERS}
+        dev = self.packed.device
+        if mine != theirs:
+            other.packed = torch.empty(other.core.packed_bytes, dtype=torch.uint8, device=dev)
+            other.b_rep = None if self.b_rep is None else torch.empty_like(self.b_rep)
+            other.core.pack(w.data_ptr(), _ptr(bf), other.packed.data_ptr(), _ptr(other.b_rep), _stream(dev))
+        other.workspace = (torch.empty(other.core.workspace_bytes, dtype=torch.uint8, device=dev)
                            if other.core.workspace_bytes else None)
         other.input_shape = shape
         other.output_shape = tuple(other.core.output_shape)
@@ -191,6 +212,9 @@ class FoldedConv2d:
 
         Chunks of ``chunk`` images alternate over two streams, so the H2D copy of
         one chunk, the folded conv of another and the D2H copy of a third overlap.
+        Each stream has its own input/output buffers and its own conv (and so
+        its own workspace for plans that re-pitch the input), so concurrent
+        chunks never share scratch memory.
         """
         if x_host.is_cuda or y_host.is_cuda:
             raise ValueError("run_host takes host tensors (pinned for overlap)")
@@ -208,9 +232,9 @@ class FoldedConv2d:
             m = min(chunk, n - start)
             k = i & 1
             with torch.cuda.stream(streams[k]):
-                conv = convs.get(m)
+                conv = convs.get((m, k))
                 if conv is None:
-                    conv = convs[m] = self.with_batch(m) if m != self.input_shape[0] else self
+                    conv = convs[(m, k)] = self.with_batch(m)
                 xd, yd = xbufs[k][:m], ybufs[k][:m]
                 xd.copy_(x_host[start:start + m], non_blocking=True)
                 conv(xd, relu=relu, bias=bias, out=yd, out_dtype=y_host.dtype)

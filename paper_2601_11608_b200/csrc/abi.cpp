@@ -30,32 +30,53 @@ struct SchedKey {
     return std::memcmp(&d, &o.d, sizeof(d)) == 0 && std::memcmp(&p, &o.p, sizeof(p)) == 0;
   }
 };
+// A cached schedule and the launches prepared from it.
+struct SchedEntry {
+  SchedKey key;
+  wfb::Schedule S;
+  wfb::LaunchCache launches;
+};
 std::mutex g_sched_mu;
-std::vector<std::pair<SchedKey, std::shared_ptr<const wfb::Schedule>>> g_sched;
+std::vector<std::shared_ptr<SchedEntry>> g_sched;  // most recently used first
+thread_local std::shared_ptr<SchedEntry> t_last;    // this thread's last hit (no lock, no scan)
 
-wf_status cached_schedule(const wf_conv_desc& d, const wf_fold_plan& p, std::shared_ptr<const wfb::Schedule>* out,
+wf_status cached_schedule(const wf_conv_desc& d, const wf_fold_plan& p, std::shared_ptr<SchedEntry>* out,
                           std::string* err) {
   SchedKey key;
   std::memset(&key, 0, sizeof(key));
   key.d = d;
   key.p = p;
+  if (t_last && t_last->key == key) {
+    *out = t_last;
+    return WF_OK;
+  }
   {
     std::lock_guard<std::mutex> lk(g_sched_mu);
-    for (auto& e : g_sched)
-      if (e.first == key) {
-        *out = e.second;
+    for (size_t i = 0; i < g_sched.size(); ++i)
+      if (g_sched[i]->key == key) {
+        *out = t_last = g_sched[i];
+        if (i) std::swap(g_sched[i], g_sched[0]);
         return WF_OK;
       }
   }
-  auto S = std::make_shared<wfb::Schedule>();
-  wf_status st = wfb::schedule_from_plan(d, p, S.get(), err);
+  auto E = std::make_shared<SchedEntry>();
+  E->key = key;
+  wf_status st = wfb::schedule_from_plan(d, p, &E->S, err);
   if (st != WF_OK) return st;
   std::lock_guard<std::mutex> lk(g_sched_mu);
-  if (g_sched.size() >= 64) g_sched.erase(g_sched.begin());
-  g_sched.emplace_back(key, S);
-  *out = S;
+  g_sched.insert(g_sched.begin(), E);
+  if (g_sched.size() > 64) g_sched.pop_back();
+  *out = t_last = E;
   return WF_OK;
 }
+
+// Epilogue bits wf_conv_fold_fwd accepts: the documented ones, plus the
+// 0xFFFF00 profiling switches in a WFB_PROFILE=1 build only.
+#ifndef WFB_PROFILE
+#define WFB_PROFILE 0
+#endif
+constexpr uint32_t kEpilogueAccepted =
+    WF_EPI_BIAS | WF_EPI_RELU | WF_EPI_ROW_PRODUCER | (WFB_PROFILE ? 0xFFFF00u : 0u);
 
 wf_status fail(wf_status st, const std::string& msg) {
   g_last_error = msg;
@@ -168,16 +189,15 @@ wf_status wf_conv_fold_fwd_ws(const void* x, void* workspace, const void* w_pack
                               const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype,
                               uint32_t epilogue, void* stream) {
   if (!x || !w_packed || !y || !desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
-  if (epilogue & ~static_cast<uint32_t>(WF_EPI_BIAS | WF_EPI_RELU | 0xFFFF00))  // 0xFFFF00: profiling / cross-check switches
-    return fail(WF_INVALID_ARGUMENT, "unknown epilogue flags");
-  if (plan->workspace_bytes > 0 && !workspace && !(epilogue & 0x4000))
+  if (epilogue & ~kEpilogueAccepted) return fail(WF_INVALID_ARGUMENT, "unknown epilogue flags");
+  if (plan->workspace_bytes > 0 && !workspace && !(epilogue & WF_EPI_ROW_PRODUCER))
     return fail(WF_INVALID_ARGUMENT, "this plan needs a workspace of plan->workspace_bytes (wf_conv_fold_fwd_ws)");
-  std::shared_ptr<const wfb::Schedule> S;
+  std::shared_ptr<SchedEntry> E;
   std::string err;
-  wf_status st = cached_schedule(*desc, *plan, &S, &err);
+  wf_status st = cached_schedule(*desc, *plan, &E, &err);
   if (st != WF_OK) return fail(st, err);
-  st = wfb::launch_conv(*S, *desc, x, workspace, w_packed, b_rep, y, out_dtype, epilogue,
-                        static_cast<cudaStream_t>(stream), g_num_sms.load(), &err);
+  st = wfb::launch_conv(E->S, *desc, x, workspace, w_packed, b_rep, y, out_dtype, epilogue,
+                        static_cast<cudaStream_t>(stream), g_num_sms.load(), &E->launches, &err);
   if (st != WF_OK) return fail(st, err);
   return WF_OK;
 }

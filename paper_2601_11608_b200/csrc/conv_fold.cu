@@ -7,7 +7,10 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "conv_kernel.cuh"
 
@@ -51,9 +54,65 @@ uint32_t pow2ceil(uint32_t v) {
 
 }  // namespace
 
-wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, const void* workspace, const void* packed,
-                      const float* b_rep, void* y, wf_dtype out_dtype, uint32_t epilogue, cudaStream_t st,
-                      int num_sms, std::string* err) {
+// Everything one launch needs, built once per (schedule, buffers, epilogue,
+// device): kernel arguments with the MMA table, encoded tensor maps, the
+// kernel, grid and shared memory. Immutable once built.
+struct PreparedLaunch {
+  // key
+  const void *x, *workspace, *packed;
+  const float* b_rep;
+  void* y;
+  wf_dtype out_dtype;
+  uint32_t epilogue;
+  int num_sms, device;
+  // launch
+  ConvArgs a;
+  TmaMaps maps;
+  const void* fn = nullptr;
+  int grid = 0, block = 0, smem = 0, cluster = 1;
+  // producer 3: re-pitch x into the workspace first
+  bool repitch = false;
+  long long rp_rows = 0;
+  int rp_in = 0, rp_out = 0;
+
+  bool same(const void* x_, const void* ws_, const void* pk_, const float* b_, void* y_, wf_dtype o_, uint32_t e_,
+            int sms_, int dev_) const {
+    return x == x_ && workspace == ws_ && packed == pk_ && b_rep == b_ && y == y_ && out_dtype == o_ &&
+           epilogue == e_ && num_sms == sms_ && device == dev_;
+  }
+};
+
+namespace {
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per (device context,
+// function): remembered per device, under a lock.
+cudaError_t ensure_smem(const void* fn, int device, int smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void*>, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done)
+    if (e.first.first == device && e.first.second == fn) {
+      if (e.second >= smem) return cudaSuccess;
+      cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (r == cudaSuccess) e.second = smem;
+      return r;
+    }
+  cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (r == cudaSuccess) done.push_back({{device, fn}, smem});
+  return r;
+}
+
+wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch& L, std::string* err) {
+  const void* x = L.x;
+  const void* workspace = L.workspace;
+  const void* packed = L.packed;
+  const float* b_rep = L.b_rep;
+  void* y = L.y;
+  const wf_dtype out_dtype = L.out_dtype;
+  const uint32_t epilogue = L.epilogue;
+  const int num_sms = L.num_sms;
+  ConvArgs& a = L.a;
+  TmaMaps& maps = L.maps;
   const wf_fold_plan& p = S.plan;
   const wf_dtype in_t = static_cast<wf_dtype>(p.in_dtype);
   if (out_dtype != WF_F32 && out_dtype != WF_BF16 && out_dtype != WF_F16) {
@@ -82,9 +141,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     *err = "schedule too long for the constant bank";
     return WF_UNSUPPORTED;
   }
-  ConvArgs a;
   std::memset(&a, 0, sizeof(a));
-  TmaMaps maps;
   std::memset(&maps, 0, sizeof(maps));
   a.bias = b_rep;
   a.out = static_cast<uint8_t*>(y);
@@ -144,11 +201,6 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
       a.chunk_col[i][c] = S.order[t.g0 + slot] * S.Ng + (c * S.CH) % S.Ng;
     }
   }
-  if (num_sms <= 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   a.ctas_per_ntile = std::max(1, std::min<int>(num_sms / a.n_tiles, a.num_mtiles));
   if (S.pair == 2) a.ctas_per_ntile = std::max(2, a.ctas_per_ntile & ~1);  // whole CTA pairs
   a.tps = S.tps;
@@ -164,16 +216,13 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   a.acc_stride = pow2ceil(max_cols);
   // as many accumulator buffers as fit in the 512 TMEM columns (<= 4): the
   // MMAs run further ahead of the epilogue when an N-tile is narrow (MNv2 128)
-  a.n_acc = (a.acc_stride <= 128) ? 4 : 2;
+  a.n_acc = (a.acc_stride <= 128 && !(p.launch_opts & 1)) ? 4 : 2;
   a.acc_shift = (a.n_acc == 4) ? 2 : 1;
-  if (const char* env = std::getenv("WF_NACC")) {
-    if (env[0] == '2') { a.n_acc = 2; a.acc_shift = 1; }
-  }
   a.tmem_cols = a.n_acc * a.acc_stride;
   // epilogue ping-pong for a single narrow N-tile (MNv2: 128 columns, +3%);
-  // wider tiles lose with it (R50 -13%, VGG -25%). WF_EPI_PP=0/1 overrides.
+  // wider tiles lose with it (R50 -13%, VGG -25%). launch_opts overrides.
   a.epi_pp = (max_cols <= 128 && a.n_tiles == 1 && S.pair == 1) ? 1 : 0;
-  if (const char* env = std::getenv("WF_EPI_PP")) a.epi_pp = (env[0] == '1' && S.pair == 1) ? 1 : 0;
+  if (const int pp = (p.launch_opts >> 1) & 3) a.epi_pp = (pp == 2 && S.pair == 1) ? 1 : 0;
   a.epi_flags = static_cast<int>(epilogue);
   // shared-memory carve-up (offsets from the 1024-aligned base)
   a.off_a = kCtrlBytes;
@@ -183,7 +232,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   // 0x4000 (profiling / cross-check): build the TMA-layout A tile with the row
   // producer instead -- same shared-memory image, so results are bit-identical
   const bool tf32 = (in_t == WF_TF32);
-  const int prod = ((S.prod == 0 || S.prod == 3) && (epilogue & 0x4000u) && !tf32) ? 1 : S.prod;
+  const int prod = ((S.prod == 0 || S.prod == 3) && (epilogue & WF_EPI_ROW_PRODUCER) && !tf32) ? 1 : S.prod;
   a.prod = prod;
   a.off_raw = a.off_bias + kMaxAccCols * 4;
   a.raw_slots = (prod == 1 || prod == 2) ? S.raw_slots : 0;
@@ -259,9 +308,10 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
       *err = "this plan needs a 16-byte aligned workspace of plan->workspace_bytes";
       return WF_INVALID_ARGUMENT;
     }
-    wf_status rs = launch_repitch(x, const_cast<void*>(workspace), d.n * d.h, static_cast<int>(d.w * d.c * es),
-                                  static_cast<int>(S.Wp * d.c * es), st, err);
-    if (rs != WF_OK) return rs;
+    L.repitch = true;
+    L.rp_rows = d.n * d.h;
+    L.rp_in = static_cast<int>(d.w * d.c * es);
+    L.rp_out = static_cast<int>(S.Wp * d.c * es);
     xt = workspace;
   }
   // ---- A descriptor high word and the SWIZZLE_32B layout parameters -------------
@@ -323,7 +373,6 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   }
 
   const int grid = a.n_tiles * a.ctas_per_ntile;
-  cudaError_t e;
   if (S.pair == 2 && (prod == 1 || prod == 2)) {
     *err = "the row producers run single-CTA plans";
     return WF_UNSUPPORTED;
@@ -334,25 +383,113 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
   }
   const int kind = tf32 ? 1 : 0;
   // two N-tiles as a 2-CTA cluster sharing each A stage by multicast
-  // (AlexNet 1.08-1.15x, VGG neutral; WF_MCAST=0 turns it off)
-  const char* mc_env = std::getenv("WF_MCAST");
-  const bool mc = !(mc_env && mc_env[0] == '0') && (prod == 0 || prod == 3) && S.pair == 1 && !tf32 &&
-                  a.n_tiles == 2 && a.ksplit == 1 && grid % 2 == 0;
-  if (mc)
-    e = launch_conv_mc(a, maps, grid, smem, st, out_dtype, S.CH);
-  else if ((prod == 0 || prod == 3) && S.pair == 2)
-    e = launch_conv_pair(a, maps, grid, smem, st, out_dtype, S.CH);
-  else if (prod == 0 || prod == 3)
-    e = launch_conv_prod<0>(a, maps, grid, smem, st, kind, out_dtype, S.CH);
-  else if (prod == 1)
-    e = launch_conv_prod<1>(a, maps, grid, smem, st, kind, out_dtype, S.CH);
-  else
-    e = launch_conv_prod<2>(a, maps, grid, smem, st, kind, out_dtype, S.CH);
+  // (AlexNet 1.08-1.15x, VGG neutral; launch_opts bit 3 turns it off)
+  const bool mc = !(p.launch_opts & 8) && (prod == 0 || prod == 3) && S.pair == 1 && !tf32 && a.n_tiles == 2 &&
+                  a.ksplit == 1 && grid % 2 == 0;
+  L.cluster = 1;
+  if (mc) {
+    L.fn = conv_kernel_fn_mc(out_dtype, S.CH);
+    L.cluster = 2;
+  } else if ((prod == 0 || prod == 3) && S.pair == 2) {
+    L.fn = conv_kernel_fn_pair(out_dtype, S.CH);
+    L.cluster = 2;
+  } else if (prod == 0 || prod == 3) {
+    L.fn = conv_kernel_fn<0>(kind, out_dtype, S.CH);
+  } else if (prod == 1) {
+    L.fn = conv_kernel_fn<1>(kind, out_dtype, S.CH);
+  } else {
+    L.fn = conv_kernel_fn<2>(kind, out_dtype, S.CH);
+  }
+  if (!L.fn) {
+    *err = "no conv kernel built for this producer / MMA kind / output type";
+    return WF_UNSUPPORTED;
+  }
+  L.grid = grid;
+  L.block = (prod == 1 || prod == 2) ? 320 + 32 * kGatherWarps : 320;
+  L.smem = smem;
+  cudaError_t e = ensure_smem(L.fn, L.device, smem);
+  if (e != cudaSuccess) {
+    *err = std::string("cudaFuncSetAttribute(max dynamic shared memory) failed: ") + cudaGetErrorString(e);
+    return WF_CUDA_ERROR;
+  }
+  return WF_OK;
+}
+
+cudaError_t launch_prepared(const PreparedLaunch& L, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(L.grid);
+  cfg.blockDim = dim3(L.block);
+  cfg.dynamicSmemBytes = static_cast<size_t>(L.smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (L.cluster > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = L.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  void* args[2] = {const_cast<ConvArgs*>(&L.a), const_cast<TmaMaps*>(&L.maps)};
+  return cudaLaunchKernelExC(&cfg, L.fn, args);
+}
+
+}  // namespace
+
+wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, const void* workspace, const void* packed,
+                      const float* b_rep, void* y, wf_dtype out_dtype, uint32_t epilogue, cudaStream_t st,
+                      int num_sms, LaunchCache* cache, std::string* err) {
+  int device = 0;
+  if (cudaGetDevice(&device) != cudaSuccess) {
+    *err = "cudaGetDevice failed";
+    return WF_CUDA_ERROR;
+  }
+  if (num_sms <= 0) num_sms = sm_count(device);
+  std::shared_ptr<const PreparedLaunch> L;
+  if (cache) {
+    std::lock_guard<std::mutex> lk(cache->mu);
+    for (size_t i = 0; i < cache->entries.size(); ++i)
+      if (cache->entries[i]->same(x, workspace, packed, b_rep, y, out_dtype, epilogue, num_sms, device)) {
+        L = cache->entries[i];
+        if (i) std::swap(cache->entries[i], cache->entries[0]);  // most recent first
+        break;
+      }
+  }
+  if (!L) {
+    auto n = std::make_shared<PreparedLaunch>();
+    n->x = x; n->workspace = workspace; n->packed = packed; n->b_rep = b_rep; n->y = y;
+    n->out_dtype = out_dtype; n->epilogue = epilogue; n->num_sms = num_sms; n->device = device;
+    wf_status ps = prepare_conv(S, d, *n, err);
+    if (ps != WF_OK) return ps;
+    L = n;
+    if (cache) {
+      std::lock_guard<std::mutex> lk(cache->mu);
+      cache->entries.insert(cache->entries.begin(), n);
+      if (cache->entries.size() > LaunchCache::kMax) cache->entries.pop_back();
+    }
+  }
+  if (L->repitch) {
+    wf_status rs = launch_repitch(x, const_cast<void*>(workspace), L->rp_rows, L->rp_in, L->rp_out, st, err);
+    if (rs != WF_OK) return rs;
+  }
+  const cudaError_t e = launch_prepared(*L, st);
   if (e != cudaSuccess) {
     *err = std::string("conv_fold_kernel launch failed: ") + cudaGetErrorString(e);
     return WF_CUDA_ERROR;
   }
   return WF_OK;
+}
+
+int sm_count(int device) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, int>> known;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& k : known)
+    if (k.first == device) return k.second;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  known.push_back({device, n});
+  return n;
 }
 
 }  // namespace wfb

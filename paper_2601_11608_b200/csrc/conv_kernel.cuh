@@ -105,6 +105,22 @@ struct TmaMaps {
   CUtensorMap in_shift[kMaxResidues];  // core column 0 one folded column further (region Q)
 };
 
+// Profiling / diagnosis switches (the 0xFFFF00 bits of epi_flags; DESIGN.md
+// 5.1b): compiled in only by a WFB_PROFILE=1 build (`make PROFILE=1`). A
+// release build folds every check to false and the C-ABI rejects the bits.
+#ifndef WFB_PROFILE
+#define WFB_PROFILE 0
+#endif
+__device__ __forceinline__ bool prof(const ConvArgs& a, int bit) {
+#if WFB_PROFILE
+  return (a.epi_flags & bit) != 0;
+#else
+  (void)a;
+  (void)bit;
+  return false;
+#endif
+}
+
 template <typename OutT>
 __device__ __forceinline__ uint32_t pack2(float lo, float hi);
 template <>
@@ -537,7 +553,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
       mbar_init(bar_full + 8 * i, kProd == 0 ? 1 : kGatherWarps);  // TMA: one expect_tx; rows: one arrive per transposer
-      mbar_init(bar_empty + 8 * i, (kMc && !(a.epi_flags & 0x2000)) ? 2 : 1);  // multicast: both CTAs' MMAs release the stage
+      mbar_init(bar_empty + 8 * i, (kMc && !prof(a, 0x2000)) ? 2 : 1);  // multicast: both CTAs' MMAs release the stage
     }
     for (int i = 0; i < a.n_acc; ++i) {
       mbar_init(bar_tfull + 8 * i, 1);
@@ -585,7 +601,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         for (int off = 0; off < bb; off += 32768)
           bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
         int slot_it = 0;
-        const bool no_loads = (a.epi_flags & 0x1000) != 0;
+        const bool no_loads = prof(a, 0x1000);
         for (int mt = local; mt < a.num_units; mt += a.unit_stride)  // stage units (= M tiles unless tps 2)
           for (int ks = 0; ks < rp.ksplit; ++ks) {
             const StageRows sr = stage_rows<kProd>(a, rp, mt, ks);
@@ -612,10 +628,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       __syncwarp();
     } else {
       const int tw = warp - 10;  // transposer 0..kGatherWarps-1
-      const bool dbg = (a.epi_flags & 0x8000) && blockIdx.x == 0 && tw == 0 && lane == 0;
+      const bool dbg = prof(a, 0x8000) && blockIdx.x == 0 && tw == 0 && lane == 0;
       long long t_empty = 0, t_full = 0, t_work = 0, t_fence = 0, t0 = 0;
       int it = 0, slot_it = 0;
-      const bool no_loads = (a.epi_flags & 0x1000) != 0;
+      const bool no_loads = prof(a, 0x1000);
       const int nstages = a.stages, stage_bytes = a.stage_bytes;
       const uint32_t a_base = base + a.off_a;
       for (int mt = local; mt < a.num_units; mt += a.unit_stride) {  // stage units
@@ -643,15 +659,17 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
           }
           slot_it += sr.count;
           if (dbg) t0 = clock64();
-          if (!(a.epi_flags & 0x10000)) fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05
+          if (!prof(a, 0x10000)) fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05
           __syncwarp();
           if (dbg) t_fence += clock64() - t0;
           if (lane == 0) mbar_arrive(bar_full + 8 * stage);
         }
       }
+#if WFB_PROFILE
       if (dbg) printf("transposer0 cta0: fence %lld cycles\n", t_fence);
       if (dbg) printf("transposer0 cta0: stages %d  wait-empty %lld  wait-row %lld  transpose %lld cycles\n", it,
                       t_empty, t_full, t_work);
+#endif
     }
   } else if (warp == 0) {
     // ===================== TMA producer (one elected lane) =====================
@@ -668,7 +686,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       const uint32_t tx = static_cast<uint32_t>((a.box_bytes + a.shift_box_bytes) * __popc(a.res_mask));
       int it = 0;
       // profiling (0x800000, with 0x600000): the producer sits the launch out too
-      for (int u = (a.epi_flags & 0x800000) ? a.num_units : local; u < a.num_units; u += a.unit_stride, ++it) {
+      for (int u = prof(a, 0x800000) ? a.num_units : local; u < a.num_units; u += a.unit_stride, ++it) {
         const int stage = it % a.stages;
         const uint32_t round = static_cast<uint32_t>(it / a.stages);
         mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
@@ -677,12 +695,12 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         int n, oh0;
         tile_origin<kPair>(a, u, 0, rank, n, oh0);  // the stage covers tiles 0..tps-1 from here
         const uint32_t dst = base + a.off_a + stage * a.stage_bytes;
-        if (a.epi_flags & 0x1000) {  // profiling: no A loads (stage contents stale)
+        if (prof(a, 0x1000)) {  // profiling: no A loads (stage contents stale)
           if (rank == 0) mbar_arrive(bar_full + 8 * stage);
           continue;
         }
         // profiling only: 0x20000 drops the shift boxes, 0x40000 loads residue 0 only
-        const bool dbg_noshift = (a.epi_flags & 0x20000) != 0, dbg_oneres = (a.epi_flags & 0x40000) != 0;
+        const bool dbg_noshift = prof(a, 0x20000), dbg_oneres = prof(a, 0x40000);
         uint32_t txs = tx;
         if (dbg_noshift || dbg_oneres) {
           txs = 0;
@@ -691,14 +709,16 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
               txs += a.box_bytes + (dbg_noshift ? 0 : a.shift_box_bytes);
         }
         if (rank == 0) mbar_arrive_expect_tx(bar_full + 8 * stage, txs * kPair);
+        const bool mc_self = prof(a, 0x2000);  // profiling: every CTA loads every residue into itself only
         if (a.sw32) {  // one SWIZZLE_32B box of 32-byte K-step pieces per (residue, in-pixel offset)
           for (int b = 0, j = 0; b < a.s; ++b) {
             if (!((a.res_mask >> b) & 1u)) continue;
-            if (kMc && ((j++ & 1) != static_cast<int>(mrank))) continue;  // the peer multicasts this residue
+            if (kMc && !mc_self && ((j++ & 1) != static_cast<int>(mrank))) continue;  // the peer multicasts it
             for (int qi = 0; qi < a.nq; ++qi) {
               const uint32_t dq = dst + b * a.region_bytes + qi * a.qregion_bytes;
               if constexpr (kMc)
-                tma_load_4d_mc(dq, &maps.in[b], a.qcoord[qi], a.c0, oh0 + a.amin[b], n, fbar, 0x3);
+                tma_load_4d_mc(dq, &maps.in[b], a.qcoord[qi], a.c0, oh0 + a.amin[b], n, fbar,
+                               mc_self ? static_cast<uint16_t>(1u << mrank) : static_cast<uint16_t>(0x3));
               else if constexpr (kPair == 2)
                 tma_load_4d_pair(dq, &maps.in[b], a.qcoord[qi], a.c0, oh0 + a.amin[b], n, fbar);
               else
@@ -710,8 +730,6 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         for (int b = 0, j = 0; b < a.s; ++b) {
           if (!((a.res_mask >> b) & 1u)) continue;
           if (dbg_oneres && b != __ffs(a.res_mask) - 1) continue;
-          // profiling 0x2000: every CTA loads every residue into itself only (cluster sync logic alone)
-          const bool mc_self = (a.epi_flags & 0x2000) != 0;
           if (kMc && !mc_self && ((j++ & 1) != static_cast<int>(mrank))) continue;  // the peer multicasts this residue
           if constexpr (kMc) {
             const uint16_t mask = mc_self ? static_cast<uint16_t>(1u << mrank) : static_cast<uint16_t>(0x3);
@@ -732,14 +750,21 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
           }
         }
       }
+      if constexpr (kMc) {
+        // producer tail: wait for the final release of every stage in use --
+        // the peer's last multicast commit lands on this CTA's empty
+        // barriers -- so no remote arrive is in flight at teardown
+        for (int i = max(0, it - a.stages); i < it; ++i)
+          mbar_wait(bar_empty + 8 * (i % a.stages), static_cast<uint32_t>(i / a.stages) & 1u);
+      }
     }
     __syncwarp();
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     // The whole warp walks the (warp-uniform) schedule so descriptors live in
     // uniform registers straight from the constant bank; one lane issues.
-    const bool skip_mma = (a.epi_flags & 0x100) != 0;  // profiling switch
-    const bool no_wait = (a.epi_flags & 0x200000) != 0;  // profiling: issue the schedule back to back (with 0x1200)
+    const bool skip_mma = prof(a, 0x100);  // profiling switch
+    const bool no_wait = prof(a, 0x200000);  // profiling: issue the schedule back to back (with 0x1200)
     // descriptor start fields are 14-bit CTA-local offsets (>> 4): in a
     // cluster launch a rank-1 CTA's shared::cta addresses carry 0x1000000,
     // which must not spill into the LBO field
@@ -760,10 +785,12 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     const uint32_t a_base = base + a.off_a;
     const int nt_e0 = a.nt_entry0[ntile], nt_en = a.nt_entries[ntile], nt_sp = a.nt_split[ntile];
     // profiling (0x80000, CTA 0): cycles the issuer waits on the accumulator / the A stage
-    const bool dbg = (a.epi_flags & 0x80000) && blockIdx.x == 0;
+    const bool dbg = prof(a, 0x80000) && blockIdx.x == 0;
     long long w_acc = 0, w_full = 0, w_hi = 0, t_all = dbg ? clock64() : 0;
     unsigned long long ns_all = 0;  // wall time of the same span: cycles / ns = the SM clock it ran at
+#if WFB_PROFILE
     if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_all));
+#endif
     int tile = 0;
     int stage_c = 0;           // A stage of the next sub-stage (kept incrementally: no division per tile)
     uint32_t round_c = 0;      // its fill round
@@ -826,7 +853,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
         }
         if (leader && k == tps - 1) {  // last tile frees the stage (multicast: in both CTAs)
           if constexpr (kMc) {
-            if (a.epi_flags & 0x2000) mma_commit(bar_empty + 8 * stage);
+            if (prof(a, 0x2000)) mma_commit(bar_empty + 8 * stage);
             else mma_commit_mc(bar_empty + 8 * stage, 0x3);
           }
           else commit_to<kPair>(bar_empty + 8 * stage);
@@ -838,6 +865,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
      for (int ks = 0; ks < ksplit; ++ks)  // advance past the unit's sub-stages
        if (++stage_c == stages) { stage_c = 0; ++round_c; }
     }
+#if WFB_PROFILE
     if (dbg && leader)
     {
       unsigned long long ns_end;
@@ -846,6 +874,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
       printf("mma issuer cta0: %d tiles, %lld cycles in %llu ns (%.0f MHz): wait accumulator %lld (upper half %lld), "
              "wait A stage %lld\n", tile, cyc, ns_end - ns_all, 1e3 * cyc / (double)(ns_end - ns_all), w_acc, w_hi, w_full);
     }
+#endif
     }
   mma_done:;
   } else if (warp >= 2 && warp < 10) {
@@ -876,10 +905,10 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     const int lo_it = split_acc ? (pp ? 2 * (nchunks / 2) : 2 * ((nchunks / 2 - half + 1) / 2)) : n_it;
     const int k4 = lane & 3;
     const bool relu = (a.epi_flags & WF_EPI_RELU) != 0;
-    const bool dbg_skip_epi = (a.epi_flags & 0x200) != 0;
-    const bool dbg_skip_store = (a.epi_flags & 0x400) != 0;
-    const bool skip_ld = (a.epi_flags & 0x800) != 0;
-    const bool stream_st = (a.epi_flags & 0x100000) != 0;  // experiment: streaming store hints
+    const bool dbg_skip_epi = prof(a, 0x200);
+    const bool dbg_skip_store = prof(a, 0x400);
+    const bool skip_ld = prof(a, 0x800);
+    const bool stream_st = prof(a, 0x100000);  // experiment: streaming store hints
     const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
     // chunk cc of this warp is accumulator chunk c_first + c_step * cc; its output
     // column comes from the slot order (chunk_col), read per iteration
@@ -922,7 +951,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     const uint32_t te_lo = (kPair == 2) ? mapa(bar_tempty, 0) : bar_tempty;
     const uint32_t te_hi = (kPair == 2) ? mapa(bar_tempty_hi, 0) : bar_tempty_hi;
     // profiling (0x400000, with 0x200000): the epilogue warps sit the launch out
-    for (int u = (a.epi_flags & 0x400000) ? a.num_units : local; u < a.num_units; u += a.unit_stride) {
+    for (int u = prof(a, 0x400000) ? a.num_units : local; u < a.num_units; u += a.unit_stride) {
      const int vn_u = vn, vrem_u = vrem;
      vn += vq;
      vrem += vr;
@@ -1026,103 +1055,43 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   }
 }
 
-// Typed launch for one producer kind (instantiated in conv_prod<kProd>.cu).
-template <int kKind, typename OutT, int CH, int kProd>
-cudaError_t launch_typed(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st) {
-  auto kern = conv_fold_kernel<kKind, OutT, CH, kProd>;
-  static int configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  kern<<<grid, kProd == 0 ? 320 : 320 + 32 * kGatherWarps, smem, st>>>(args, maps);
-  return cudaGetLastError();
+// Kernel selectors: the device function for one (producer, MMA kind, output
+// type, epilogue chunk[, pair | multicast]) combination, or nullptr when the
+// combination is not built. Instantiated in conv_prod<kProd>.cu / conv_pair.cu;
+// conv_fold.cu launches them with cudaLaunchKernelExC.
+template <int kKind, typename OutT, int CH, int kProd, int kPair = 1, int kMc = 0>
+const void* kernel_ptr() {
+  return reinterpret_cast<const void*>(&conv_fold_kernel<kKind, OutT, CH, kProd, kPair, kMc>);
 }
 
 // kind: 0 kind::f16, 1 kind::tf32; out: output dtype; ch: epilogue chunk.
 template <int kProd>
-cudaError_t launch_conv_prod(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st, int kind,
-                             wf_dtype out, int ch) {
+const void* conv_kernel_fn(int kind, wf_dtype out, int ch) {
   if constexpr (kProd != 0) {
-    if (kind == 1) return cudaErrorInvalidValue;  // tf32 runs with the TMA producer only
+    if (kind == 1) return nullptr;  // tf32 runs with the TMA producer only
   } else if (kind == 1) {
-    if (ch != 32) return cudaErrorInvalidValue;
-    if (out == WF_BF16) return launch_typed<1, __nv_bfloat16, 32, kProd>(args, maps, grid, smem, st);
-    if (out == WF_F16) return launch_typed<1, __half, 32, kProd>(args, maps, grid, smem, st);
-    return launch_typed<1, float, 32, kProd>(args, maps, grid, smem, st);
+    if (ch != 32) return nullptr;
+    if (out == WF_BF16) return kernel_ptr<1, __nv_bfloat16, 32, kProd>();
+    if (out == WF_F16) return kernel_ptr<1, __half, 32, kProd>();
+    return kernel_ptr<1, float, 32, kProd>();
   }
   if (ch == 64) {
-    if (out == WF_BF16) return launch_typed<0, __nv_bfloat16, 64, kProd>(args, maps, grid, smem, st);
-    if (out == WF_F16) return launch_typed<0, __half, 64, kProd>(args, maps, grid, smem, st);
-    return launch_typed<0, float, 64, kProd>(args, maps, grid, smem, st);
+    if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 64, kProd>();
+    if (out == WF_F16) return kernel_ptr<0, __half, 64, kProd>();
+    return kernel_ptr<0, float, 64, kProd>();
   }
-  if (out == WF_BF16) return launch_typed<0, __nv_bfloat16, 32, kProd>(args, maps, grid, smem, st);
-  if (out == WF_F16) return launch_typed<0, __half, 32, kProd>(args, maps, grid, smem, st);
-  return launch_typed<0, float, 32, kProd>(args, maps, grid, smem, st);
+  if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 32, kProd>();
+  if (out == WF_F16) return kernel_ptr<0, __half, 32, kProd>();
+  return kernel_ptr<0, float, 32, kProd>();
 }
 
-// CTA-pair launch (cluster of 2, cta_group::2 MMAs), TMA producer, kind::f16.
-template <typename OutT, int CH>
-cudaError_t launch_pair_typed(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st) {
-  auto kern = conv_fold_kernel<0, OutT, CH, 0, 2>;
-  static int configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(320);
-  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args, maps);
-}
+// CTA-pair kernel (cluster of 2, cta_group::2 MMAs), TMA producer, kind::f16.
+const void* conv_kernel_fn_pair(wf_dtype out, int ch);
+// 2-CTA N-tile cluster with multicast A loads, TMA producer, kind::f16.
+const void* conv_kernel_fn_mc(wf_dtype out, int ch);
 
-cudaError_t launch_conv_pair(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st,
-                             wf_dtype out, int ch);
-
-// 2-CTA N-tile cluster with multicast A loads (kMc = 1), TMA producer, kind::f16.
-template <typename OutT, int CH>
-cudaError_t launch_mc_typed(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st) {
-  auto kern = conv_fold_kernel<0, OutT, CH, 0, 1, 1>;
-  static int configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(320);
-  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args, maps);
-}
-
-cudaError_t launch_conv_mc(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st,
-                           wf_dtype out, int ch);
-
-extern template cudaError_t launch_conv_prod<0>(const ConvArgs&, const TmaMaps&, int, int, cudaStream_t, int, wf_dtype,
-                                                int);
-extern template cudaError_t launch_conv_prod<1>(const ConvArgs&, const TmaMaps&, int, int, cudaStream_t, int, wf_dtype,
-                                                int);
-extern template cudaError_t launch_conv_prod<2>(const ConvArgs&, const TmaMaps&, int, int, cudaStream_t, int, wf_dtype,
-                                                int);
+extern template const void* conv_kernel_fn<0>(int, wf_dtype, int);
+extern template const void* conv_kernel_fn<1>(int, wf_dtype, int);
+extern template const void* conv_kernel_fn<2>(int, wf_dtype, int);
 
 }  // namespace wfb

@@ -1,30 +1,29 @@
-// conv_pair.cu -- instantiates the CTA-pair (cta_group::2) conv kernel; see conv_kernel.cuh.
+// conv_pair.cu -- instantiates the cluster kernels: CTA pairs (cta_group::2)
+// and the multicast N-tile cluster; see conv_kernel.cuh.
 #include "conv_kernel.cuh"
 
 namespace wfb {
 
-cudaError_t launch_conv_pair(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st,
-                             wf_dtype out, int ch) {
+const void* conv_kernel_fn_pair(wf_dtype out, int ch) {
   if (ch == 64) {
-    if (out == WF_BF16) return launch_pair_typed<__nv_bfloat16, 64>(args, maps, grid, smem, st);
-    if (out == WF_F16) return launch_pair_typed<__half, 64>(args, maps, grid, smem, st);
-    return launch_pair_typed<float, 64>(args, maps, grid, smem, st);
+    if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 64, 0, 2>();
+    if (out == WF_F16) return kernel_ptr<0, __half, 64, 0, 2>();
+    return kernel_ptr<0, float, 64, 0, 2>();
   }
-  if (out == WF_BF16) return launch_pair_typed<__nv_bfloat16, 32>(args, maps, grid, smem, st);
-  if (out == WF_F16) return launch_pair_typed<__half, 32>(args, maps, grid, smem, st);
-  return launch_pair_typed<float, 32>(args, maps, grid, smem, st);
+  if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 32, 0, 2>();
+  if (out == WF_F16) return kernel_ptr<0, __half, 32, 0, 2>();
+  return kernel_ptr<0, float, 32, 0, 2>();
 }
 
-cudaError_t launch_conv_mc(const ConvArgs& args, const TmaMaps& maps, int grid, int smem, cudaStream_t st,
-                           wf_dtype out, int ch) {
+const void* conv_kernel_fn_mc(wf_dtype out, int ch) {
   if (ch == 64) {
-    if (out == WF_BF16) return launch_mc_typed<__nv_bfloat16, 64>(args, maps, grid, smem, st);
-    if (out == WF_F16) return launch_mc_typed<__half, 64>(args, maps, grid, smem, st);
-    return launch_mc_typed<float, 64>(args, maps, grid, smem, st);
+    if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 64, 0, 1, 1>();
+    if (out == WF_F16) return kernel_ptr<0, __half, 64, 0, 1, 1>();
+    return kernel_ptr<0, float, 64, 0, 1, 1>();
   }
-  if (out == WF_BF16) return launch_mc_typed<__nv_bfloat16, 32>(args, maps, grid, smem, st);
-  if (out == WF_F16) return launch_mc_typed<__half, 32>(args, maps, grid, smem, st);
-  return launch_mc_typed<float, 32>(args, maps, grid, smem, st);
+  if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 32, 0, 1, 1>();
+  if (out == WF_F16) return kernel_ptr<0, __half, 32, 0, 1, 1>();
+  return kernel_ptr<0, float, 32, 0, 1, 1>();
 }
 
 }  // namespace wfb

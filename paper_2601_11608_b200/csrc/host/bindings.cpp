@@ -403,6 +403,6 @@ PYBIND11_MODULE(_core, m) {
                       workspace ? P(workspace) : nullptr);
           },
           py::arg("x"), py::arg("packed"), py::arg("b_rep"), py::arg("y"), py::arg("out_dtype"), py::arg("bias"),
-          py::arg("relu"), py::arg("stream"), py::arg("profile_flags") = 0, py::arg("workspace") = 0)
+          py::arg("relu"), py::arg("stream"), py::arg("extra_flags") = 0, py::arg("workspace") = 0)
       .def_property_readonly("workspace_bytes", &wf::FoldedConv::workspace_bytes);
 }

@@ -227,7 +227,13 @@ json node_to_json(const Node& n) {
     case OpKind::Conv2d:
       j["stride"] = {n.stride_h, n.stride_w};
       j["groups"] = n.groups;
-      if (n.pad_h || n.pad_w) j["pad"] = {n.pad_h, n.pad_w};  // extension (reference convs are VALID)
+      if (n.pad_h || n.pad_w) {
+        // extension (reference convs are VALID): a padded conv is written as
+        // its own op kind, which the reference reader rejects as unknown
+        // (src/graph.cpp:28-32) instead of silently loading it unpadded
+        j["op"] = "conv2d_padded";
+        j["pad"] = {n.pad_h, n.pad_w};
+      }
       break;
     case OpKind::FoldedConv2d:
       j["stride"] = {n.stride_h, n.stride_w};
@@ -252,7 +258,8 @@ Node node_from_json(const json& j) {
   Node n;
   n.id = j.at("id").get<std::string>();
   try {
-    n.op = op_kind_from_string(j.at("op").get<std::string>());
+    const std::string op = j.at("op").get<std::string>();
+    n.op = (op == "conv2d_padded") ? OpKind::Conv2d : op_kind_from_string(op);
   } catch (const std::invalid_argument& e) {
     throw ManifestParse(e.what());  // unknown ops are rejected, not guessed (docs/model_format.md)
   }

@@ -151,7 +151,7 @@ class FoldedConv {
   void pack(const void* w, const float* b, void* packed, float* b_rep, void* stream) const;
   // y = ReLU?(conv(x) + b?) ; x in in_dtype, y in out_dtype, NHWC.
   void forward(const void* x, const void* packed, const float* b_rep, void* y, Dtype out_dtype, bool bias, bool relu,
-               void* stream, std::uint32_t profile_flags = 0, void* workspace = nullptr) const;
+               void* stream, std::uint32_t extra_flags = 0, void* workspace = nullptr) const;
 
  private:
   ConvSpec spec_;

@@ -3,7 +3,10 @@
 
 #include <cuda_runtime.h>
 
+#include <memory>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "plan.hpp"
 
@@ -18,10 +21,22 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
 wf_status launch_expand_dense(const wf_conv_desc& d, int64_t f, const float* w, float* out,
                               cudaStream_t st, std::string* err);
 
+// Prepared launches of one schedule (kernel arguments + encoded tensor maps
+// per buffer set), most recent first. Repeated calls on the same buffers skip
+// argument building and tensor-map encoding entirely.
+struct PreparedLaunch;  // conv_fold.cu
+struct LaunchCache {
+  static constexpr size_t kMax = 8;
+  std::mutex mu;
+  std::vector<std::shared_ptr<const PreparedLaunch>> entries;
+};
+
 // K2: the folded implicit-GEMM convolution (TMA -> tcgen05.mma -> TMEM -> epilogue).
+// num_sms <= 0: the device's SM count. cache may be null (no reuse).
 wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, const void* workspace,
                       const void* packed, const float* b_rep, void* y, wf_dtype out_dtype, uint32_t epilogue,
-                      cudaStream_t st, int num_sms, std::string* err);
+                      cudaStream_t st, int num_sms, LaunchCache* cache, std::string* err);
+int sm_count(int device);
 
 // Exact-order fp32 direct conv (reference conv2d semantics, with padding).
 wf_status launch_conv_direct(const wf_conv_desc& d, const float* x, const float* w, float* y, cudaStream_t st,

@@ -211,8 +211,8 @@ bool zero_init_order(const std::vector<std::pair<int, int>>& runs, int nslots, s
 //    fits as well as one tile per stage does and the batch is large; WF_TPS=1
 //    forces one.
 // kpair_req / pair_req / tps_req >= 0 pin a choice (schedule_from_plan).
-wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, Schedule* out,
-                        std::string* err, int kpair_req, int pair_req, int tps_req) {
+static wf_status make_schedule_variant(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype,
+                                       Schedule* out, std::string* err, int kpair_req, int pair_req, int tps_req) {
   if (pair_req < 0) {
     const char* env = std::getenv("WF_CTA_PAIR");
     if (env && (env[0] == '0' || env[0] == '1')) pair_req = env[0] - '0';
@@ -1070,6 +1070,25 @@ wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Sched
   return WF_OK;
 }
 
+// Launch tuning knobs, decided once per plan (wf_fold_plan::launch_opts): the
+// launch path never reads the environment. WF_NACC=2 two accumulator
+// buffers, WF_EPI_PP=0/1 epilogue ping-pong off/on, WF_MCAST=0 no multicast
+// N-tile cluster.
+static int32_t launch_opts_from_env() {
+  int32_t o = 0;
+  if (const char* e = std::getenv("WF_NACC")) o |= (e[0] == '2') ? 1 : 0;
+  if (const char* e = std::getenv("WF_EPI_PP")) o |= (e[0] == '1') ? (2 << 1) : (e[0] == '0' ? (1 << 1) : 0);
+  if (const char* e = std::getenv("WF_MCAST")) o |= (e[0] == '0') ? 8 : 0;
+  return o;
+}
+
+wf_status make_schedule(const wf_conv_desc& d, int64_t f_req, int64_t gs_req, wf_dtype in_dtype, Schedule* out,
+                        std::string* err, int kpair_req, int pair_req, int tps_req) {
+  wf_status st = make_schedule_variant(d, f_req, gs_req, in_dtype, out, err, kpair_req, pair_req, tps_req);
+  if (st == WF_OK && out->plan.status == WF_FOLD_APPLY) out->plan.launch_opts = launch_opts_from_env();
+  return st;
+}
+
 wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
                              Schedule* out, std::string* err) {
   if (p.status != WF_FOLD_APPLY) {
@@ -1086,6 +1105,7 @@ wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
     *err = "plan does not match this conv descriptor";
     return WF_SHAPE_MISMATCH;
   }
+  out->plan.launch_opts = p.launch_opts;
   return WF_OK;
 }
 

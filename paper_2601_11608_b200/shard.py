@@ -66,9 +66,17 @@ def gather_to(tensor: torch.Tensor, sizes: list[int], dst: int = 0) -> torch.Ten
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return tensor
     rank, world = dist.get_rank(), dist.get_world_size()
-    if len(sizes) != world or tensor.shape[0] != sizes[rank]:
-        raise ValueError(f"shard sizes {sizes} do not match rank {rank}'s {tuple(tensor.shape)}")
-    if rank != dst:  # every rank joins a grouped call (NCCL needs all ranks in a first one)
+    # validate collectively BEFORE any rank posts a receive: a mismatch on one
+    # rank raises on every rank instead of leaving dst blocked in irecv. The
+    # all-reduce also brings the communicator up on every rank, so a rank
+    # with an empty shard may then skip the point-to-point phase (NCCL needs
+    # every rank in the FIRST collective call only).
+    bad = float(len(sizes) != world or tensor.shape[0] != (sizes[rank] if rank < len(sizes) else -1))
+    flag = torch.tensor([bad], dtype=torch.float64, device=tensor.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+    if flag.item() > 0:
+        raise ValueError(f"shard sizes {sizes} do not match the ranks' shards (rank {rank}: {tuple(tensor.shape)})")
+    if rank != dst:
         ops = [dist.P2POp(dist.isend, tensor.contiguous(), dst)] if sizes[rank] > 0 else []
         for req in (dist.batch_isend_irecv(ops) if ops else []):
             req.wait()

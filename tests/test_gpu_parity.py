@@ -102,7 +102,7 @@ def _config_run(golden_configs, name, suffix, out_dtype=None, variant="fold", fl
     x, w, b = (golden_configs[f"{name}_{k}{suffix}"] for k in ("x", "w", "b"))
     tdt = TDT[dt]
     conv = wf.FoldedConv2d(cuda(w, tdt), cuda(b), x.shape, stride=s, padding=p, dtype=tdt, variant=variant)
-    y = conv(cuda(x, tdt), relu=bool(relu), out_dtype=out_dtype, _profile_flags=flags)
+    y = conv._forward(cuda(x, tdt), relu=bool(relu), out_dtype=out_dtype, flags=flags)
     torch.cuda.synchronize()
     return y.float().cpu().numpy(), golden_configs[f"{name}_y{suffix}"], dt, conv
 
@@ -411,7 +411,7 @@ def test_alexnet_full_geometry_sampled(oracle):
     conv = wf.FoldedConv2d(w, b, x.shape, stride=4, padding=0, dtype=torch.bfloat16)
     assert conv.device_plan["producer"] == "repitch+tma"
     y = conv(x).float().cpu().numpy()
-    y_gather = conv(x, _profile_flags=0x4000).float().cpu().numpy()  # row producer straight from x
+    y_gather = conv._forward(x, flags=A.WF_EPI_ROW_PRODUCER).float().cpu().numpy()  # row producer straight from x
     np.testing.assert_array_equal(y, y_gather)
     assert y.shape == (5, 55, 55, 96)
     for i in (0, 4):

@@ -97,7 +97,13 @@ def _gather_worker(rank, world, port, dst, n, q):
             shard.gather_to(mine[:0] if sizes[rank] else torch.zeros(1, 2, 3), sizes, dst=dst)
         except ValueError as e:
             bad = str(e)
-        q.put((rank, None if full is None else full.tolist(), bad is not None))
+        # a mismatch on ONE rank only: every rank raises (nobody is left blocked in irecv)
+        one_bad = False
+        try:
+            shard.gather_to(torch.zeros(sizes[0] + 1, 2, 3) if rank == 0 else mine, sizes, dst=dst)
+        except ValueError:
+            one_bad = True
+        q.put((rank, None if full is None else full.tolist(), bad is not None and one_bad))
     finally:
         dist.barrier()
         dist.destroy_process_group()

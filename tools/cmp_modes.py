@@ -14,6 +14,6 @@ for (n, h, w, kh, co, s, p, dt, relu) in [(5, 224, 224, 7, 64, 2, 3, torch.bfloa
     y0 = conv(x, relu=relu)
     for fl in (0x1000, 0x2000):
         y1 = torch.full_like(y0, float("nan"))
-        conv(x, relu=relu, out=y1, _profile_flags=fl)
+        conv._forward(x, relu=relu, out=y1, flags=fl)
         torch.cuda.synchronize()
         print(tuple(x.shape), dt, hex(fl), "identical" if torch.equal(y0, y1) else f"DIFF max {(y0.float()-y1.float()).abs().max().item()}")

@@ -26,7 +26,7 @@ y = conv(x)
 FLAGS = [int(v, 0) for v in sys.argv[3].split(',')] if len(sys.argv) > 3 else [0, 0x100, 0x200, 0x1000, 0x300]
 for flags in FLAGS:
     for _ in range(3):
-        conv(x, out=y, _profile_flags=max(flags, 0))
+        conv._forward(x, out=y, flags=max(flags, 0))
     torch.cuda.synchronize()
     smi = subprocess.Popen(["nvidia-smi", "--query-gpu=power.draw,clocks.sm", "--format=csv,noheader,nounits",
                             "-lms", "100"], stdout=subprocess.PIPE, text=True)
@@ -39,7 +39,7 @@ for flags in FLAGS:
             if flags == -1:  # write-only stream of the same output bytes (torch fill kernel)
                 y.fill_(1.0)
             else:
-                conv(x, out=y, _profile_flags=flags)
+                conv._forward(x, out=y, flags=flags)
         it += 10
         torch.cuda.synchronize()
     e1.record()

@@ -28,7 +28,7 @@ flags = int(sys.argv[6], 0) if len(sys.argv) > 6 else 0
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize(); e0.record()
 for _ in range(iters):
-    ff(x, relu=relu, out=y, _profile_flags=flags)
+    ff._forward(x, relu=relu, out=y, flags=flags)
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / iters
 print(f"{name} flags={flags:#x} n={n} f={ff.device_plan["f"]} gs={ff.device_plan["group_size"]} nt={ff.device_plan["n_tiles"]}: {ms:.3f} ms {n/ms*1e3:.0f} img/s "

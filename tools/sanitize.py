@@ -24,7 +24,7 @@ for kp, (n, h, w_, kh, co, s, p, dt, relu, var) in [(k, c) for k in ("0", "1") f
     conv = wf.FoldedConv2d(w, b, x.shape, stride=s, padding=p, dtype=dt, variant=var)
     for flags in ((0, 0x4000) if var == "fold" and dt != torch.float32 else (0,)):
         try:
-            y = conv(x, relu=relu, _profile_flags=flags).float()
+            y = conv._forward(x, relu=relu, flags=flags).float()
         except wf.UnsupportedError as e:  # the row-producer cross-check has a 64-row stage table
             print(f"{var:9s} {str(dt):14s} {kh}x{kh}/s{s}/p{p} flags={flags:#x} skipped: {e}")
             continue
