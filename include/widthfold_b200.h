@@ -192,6 +192,15 @@ wf_status wf_conv_fold_fwd_ws(const void* x, void* workspace, const void* w_pack
  * tcgen05 kernel does not cover, and the engine of grouped_conv. */
 wf_status wf_conv_direct_fwd(const float* x, const float* w, float* y, const wf_conv_desc* desc, void* stream);
 
+/* Grouped exact-order fp32 conv (widthfold::grouped_conv, src/blockdiag.cpp:138-187):
+ * w_dense is the (kh,kw,c,cout) block-diagonal filter; output channel oc of
+ * block g = oc / (cout/groups) sums only input channels of block g, in the
+ * reference order -- bit-identical to wf_conv_direct_fwd on finite data, and
+ * off-block terms are never formed (a NaN/Inf input poisons only its block).
+ * Run wf_check_block_diagonal first to enforce the strict-zero structure. */
+wf_status wf_conv_grouped_fwd(const float* x, const float* w_dense, float* y, const wf_conv_desc* desc,
+                              int64_t groups, void* stream);
+
 /* out = ReLU?(y + b[i % c]) -- widthfold::bias_add (src/refconv.cpp:82-95). */
 wf_status wf_bias_add(const float* y, const float* b, float* out, int64_t n, int64_t c, int32_t relu, void* stream);
 

@@ -34,7 +34,7 @@ REASONS = [
 EXPORTED = [
     "wf_plan_fold", "wf_plan_unfolded", "wf_packed_filter_bytes", "wf_expand_filter_pack", "wf_expand_filter_dense",
     "wf_conv_fold_fwd", "wf_conv_fold_fwd_ws", "wf_set_num_sms", "wf_last_error", "wf_abi_version",
-    "wf_schedule_describe", "wf_cast_f32",
+    "wf_schedule_describe", "wf_cast_f32", "wf_conv_grouped_fwd",
 ]
 
 

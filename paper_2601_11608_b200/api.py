@@ -499,8 +499,10 @@ def apply_width_fold_general(x, w, b, factor: int, *, stride_w: int | None = Non
 def grouped_conv(x, w_dense, groups: int, stride_h: int = 1, stride_w: int = 1):
     """Verified block-diagonal filter run as groups (src/blockdiag.cpp:138-187).
 
-    Strict-zero check on the device (NotBlockDiagonalError), then the exact
-    conv -- bitwise equal to the dense conv2d like the reference guarantees.
+    Strict-zero check on the device (NotBlockDiagonalError), then the
+    exact-order conv in grouped mode (only the diagonal blocks are read, off-block
+    terms are never formed) -- bitwise equal to the dense conv2d on finite data,
+    as the reference guarantees.
     """
     xt, host = _as_tensor(x, torch.float32)
     wt, _ = _as_tensor(w_dense, torch.float32)
@@ -508,7 +510,15 @@ def grouped_conv(x, w_dense, groups: int, stride_h: int = 1, stride_w: int = 1):
         raise ShapeMismatchError(f"expanded filter must be rank-4, got {tuple(wt.shape)}")
     scratch = torch.empty(1, dtype=torch.int64, device=wt.device)
     _core.check_block_diagonal(wt.data_ptr(), list(wt.shape), groups, scratch.data_ptr(), _stream(wt.device))
-    return _ret(conv2d(xt, wt, stride_h, stride_w, precision="exact"), host)
+    if xt.dim() != 4:
+        raise ShapeMismatchError(f"grouped_conv input must be rank-4 NHWC, got {tuple(xt.shape)}")
+    B, H, W, _ = xt.shape
+    KH, KW, _, Co = wt.shape
+    y = torch.empty((B, max((H - KH) // stride_h + 1, 0), max((W - KW) // stride_w + 1, 0), Co),
+                    dtype=torch.float32, device=xt.device)
+    _core.conv2d_grouped(xt.data_ptr(), wt.data_ptr(), y.data_ptr(), list(xt.shape), list(wt.shape), stride_h,
+                         stride_w, groups, _stream(xt.device))
+    return _ret(y, host)
 
 
 def gemm_ref(a, b):

@@ -213,7 +213,21 @@ wf_status wf_conv_direct_fwd(const float* x, const float* w, float* y, const wf_
   std::string err;
   wf_status st = wfb::validate_desc(*desc, &err);
   if (st != WF_OK) return fail(st, err);
-  st = wfb::launch_conv_direct(*desc, x, w, y, static_cast<cudaStream_t>(stream), &err);
+  st = wfb::launch_conv_direct(*desc, x, w, y, 1, static_cast<cudaStream_t>(stream), &err);
+  if (st != WF_OK) return fail(st, err);
+  return WF_OK;
+}
+
+wf_status wf_conv_grouped_fwd(const float* x, const float* w_dense, float* y, const wf_conv_desc* desc,
+                              int64_t groups, void* stream) {
+  if (!x || !w_dense || !y || !desc) return fail(WF_INVALID_ARGUMENT, "null argument");
+  std::string err;
+  wf_status st = wfb::validate_desc(*desc, &err);
+  if (st != WF_OK) return fail(st, err);
+  if (groups < 1 || desc->c % groups != 0 || desc->cout % groups != 0)
+    return fail(WF_SHAPE_MISMATCH, "channel extents not divisible into the requested groups");
+  st = wfb::launch_conv_direct(*desc, x, w_dense, y, static_cast<int>(groups), static_cast<cudaStream_t>(stream),
+                               &err);
   if (st != WF_OK) return fail(st, err);
   return WF_OK;
 }

@@ -114,7 +114,12 @@ wf_status launch_repitch(const void* x, void* ws, long long rows, int rb_in, int
 
 __global__ void conv_direct_kernel(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y,
                                    int B, int H, int W, int C, int KH, int KW, int Co, int sh, int sw, int ph,
-                                   int pw, int OH, int OW) {
+                                   int pw, int OH, int OW, int groups) {
+  // groups > 1: the grouped conv of a block-diagonal dense filter -- output
+  // channel oc reads only the input channels of its own block, in the same
+  // kh -> kw -> ci order (src/blockdiag.cpp:138-187), so skipped terms are
+  // never formed (no 0 * NaN) and the surviving sum is the dense one's.
+  const int Cib = C / groups, Cob = Co / groups;
   const long long total = (long long)B * OH * OW * Co;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -131,7 +136,8 @@ __global__ void conv_direct_kernel(const float* __restrict__ x, const float* __r
         const bool in = (ih >= 0 && ih < H && iw >= 0 && iw < W);
         const float* xr = x + (((long long)b * H + (in ? ih : 0)) * W + (in ? iw : 0)) * C;
         const float* wr = w + ((long long)(kh * KW + kw) * C) * Co + oc;
-        for (int ci = 0; ci < C; ++ci) {
+        const int c_lo = (oc / Cob) * Cib;
+        for (int ci = c_lo; ci < c_lo + Cib; ++ci) {
           const float xv = in ? xr[ci] : 0.0f;
           acc = __fadd_rn(acc, __fmul_rn(xv, wr[(long long)ci * Co]));
         }
@@ -166,14 +172,14 @@ static int grid_for(long long total) {
   return static_cast<int>(g < 1 ? 1 : (g > 65535 ? 65535 : g));
 }
 
-wf_status launch_conv_direct(const wf_conv_desc& d, const float* x, const float* w, float* y, cudaStream_t st,
-                             std::string* err) {
+wf_status launch_conv_direct(const wf_conv_desc& d, const float* x, const float* w, float* y, int groups,
+                             cudaStream_t st, std::string* err) {
   const int64_t OH = (d.h + 2 * d.pad_h - d.kh) / d.stride_h + 1;
   const int64_t OW = (d.w + 2 * d.pad_w - d.kw) / d.stride_w + 1;
   const long long total = (long long)d.n * OH * OW * d.cout;
   conv_direct_kernel<<<grid_for(total), 256, 0, st>>>(x, w, y, (int)d.n, (int)d.h, (int)d.w, (int)d.c, (int)d.kh,
                                                       (int)d.kw, (int)d.cout, (int)d.stride_h, (int)d.stride_w,
-                                                      (int)d.pad_h, (int)d.pad_w, (int)OH, (int)OW);
+                                                      (int)d.pad_h, (int)d.pad_w, (int)OH, (int)OW, groups);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("conv_direct_kernel: ") + cudaGetErrorString(e);

@@ -52,7 +52,8 @@ py::dict raw_dict(const wf_fold_plan& p) {
   d["packed_bytes"] = p.packed_bytes; d["epi_chunk"] = p.epi_chunk;
   d["variant"] = p.variant == WF_VARIANT_UNFOLDED ? "unfolded" : "fold";
   d["producer"] = p.producer == 0 ? "tma" : (p.producer == 1 ? "gather" : (p.producer == 2 ? "im2col" : "repitch+tma"));
-  d["pitched_w"] = p.pitched_w; d["workspace_bytes"] = p.workspace_bytes; d["cta_pair"] = p.cta_pair; d["stage_tiles"] = p.stage_tiles; d["kstep_mode"] = p.kstep_mode; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
+  d["pitched_w"] = p.pitched_w; d["workspace_bytes"] = p.workspace_bytes; d["cta_pair"] = p.cta_pair; d["stage_tiles"] = p.stage_tiles; d["kstep_mode"] = p.kstep_mode;
+  d["in_dtype"] = p.in_dtype; d["launch_opts"] = p.launch_opts; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
   return d;
 }
 
@@ -175,7 +176,7 @@ PYBIND11_MODULE(_core, m) {
   m.def(
       "count_macs",
       [](const wf::Shape& in, const wf::Shape& filt, std::int64_t sh, std::int64_t sw, std::int64_t ph,
-         std::int64_t pw) { return wf::count_macs(spec_of(in, filt, sh, sw, ph, pw)); },
+         std::int64_t pw) { return wf::count_macs(spec_of(in, filt, sh, sw, ph, pw)).macs; },
       py::arg("input_shape"), py::arg("filter_shape"), py::arg("stride_h") = 1, py::arg("stride_w") = 1,
       py::arg("pad_h") = 0, py::arg("pad_w") = 0);
 
@@ -221,6 +222,17 @@ PYBIND11_MODULE(_core, m) {
       },
       py::arg("x"), py::arg("w"), py::arg("y"), py::arg("input_shape"), py::arg("filter_shape"),
       py::arg("stride_h"), py::arg("stride_w"), py::arg("pad_h"), py::arg("pad_w"), py::arg("stream"));
+
+  m.def(
+      "conv2d_grouped",
+      [](std::uintptr_t x, std::uintptr_t w, std::uintptr_t y, const wf::Shape& in, const wf::Shape& filt,
+         std::int64_t sh, std::int64_t sw, std::int64_t groups, std::uintptr_t stream) {
+        const wf::ConvSpec spec = spec_of(in, filt, sh, sw, 0, 0);
+        py::gil_scoped_release nogil;
+        wf::conv2d_grouped(F(x), F(w), static_cast<float*>(P(y)), spec, groups, P(stream));
+      },
+      py::arg("x"), py::arg("w"), py::arg("y"), py::arg("input_shape"), py::arg("filter_shape"),
+      py::arg("stride_h"), py::arg("stride_w"), py::arg("groups"), py::arg("stream"));
 
   m.def(
       "bias_add",

@@ -16,10 +16,6 @@ namespace widthfold {
 
 namespace {
 
-std::int64_t numel(const Shape& s) {
-  return std::accumulate(s.begin(), s.end(), std::int64_t{1}, std::multiplies<std::int64_t>());
-}
-
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -94,7 +90,7 @@ Graph infer_shapes(Graph g) {
   std::set<std::string> seen;
   for (auto& n : g.nodes) {
     auto fail = [&](const std::string& why) {
-      throw ShapeInferenceFailure("node '" + n.id + "' (" + to_string(n.op) + "): " + why);
+      throw ShapeInferenceFailure(n.id, std::string("(") + to_string(n.op) + "): " + why);
     };
     if (n.id.empty() || seen.count(n.id)) fail("missing or duplicate id");
     for (const auto& in : n.inputs)
@@ -168,12 +164,12 @@ CostEstimate cost(const Graph& g0, std::int64_t align) {
   for (const auto& n : g.nodes) {
     if (n.op == OpKind::Conv2d) {
       const ConvSpec s = conv_spec_of(g, n);
-      c.macs += count_macs(s);
-      c.issued_macs += count_macs(s);
+      c.macs += count_macs(s).macs;
+      c.issued_macs += count_macs(s).macs;
       if (s.in_c() % align) c.aligned = false;
     } else if (n.op == OpKind::FoldedConv2d) {
       const ConvSpec s = conv_spec_of(g, n);
-      c.macs += count_macs(s);
+      c.macs += count_macs(s).macs;
       c.issued_macs += plan_device_fold(s, n.factor, 0, n.dtype).raw.issued_macs;
     } else if (n.op == OpKind::Matmul) {
       const Shape& a = g.find(n.inputs[0])->out_shape;

@@ -64,8 +64,7 @@ struct Graph {
   std::vector<std::string> output_ids() const;
 };
 
-struct ShapeInferenceFailure : std::runtime_error { using std::runtime_error::runtime_error; };
-struct MissingInput : std::runtime_error { using std::runtime_error::runtime_error; };
+// ShapeInferenceFailure, MissingInput: widthfold/errors.hpp
 
 // Structural validation plus per-node output shapes (include/widthfold/graph.hpp:48).
 Graph infer_shapes(Graph g);

@@ -32,9 +32,7 @@
 
 namespace widthfold {
 
-struct ManifestParse : std::runtime_error { using std::runtime_error::runtime_error; };
-struct BlobSizeMismatch : std::runtime_error { using std::runtime_error::runtime_error; };
-struct IoFailure : std::runtime_error { using std::runtime_error::runtime_error; };
+// ManifestParse, BlobSizeMismatch, IoFailure: widthfold/errors.hpp
 
 // One bundle tensor: shape, dtype tag and the little-endian payload bytes.
 struct BundleTensor {

@@ -1,6 +1,11 @@
 // widthfold.cpp -- see widthfold.hpp.
 #include "widthfold.hpp"
 
+// fold.hpp spells FoldReason with literal values; they are the C-ABI's.
+static_assert(static_cast<int>(widthfold::FoldReason::UnalignedPixel) == WF_REASON_UNALIGNED_PIXEL);
+static_assert(static_cast<int>(widthfold::FoldReason::NotProfitable) == WF_REASON_NOT_PROFITABLE);
+static_assert(static_cast<int>(widthfold::FoldReason::OutputTail) == WF_REASON_OUTPUT_TAIL);
+
 #include <numeric>
 #include <sstream>
 
@@ -18,15 +23,6 @@ void throw_on(wf_status st) {
     case WF_UNSUPPORTED: throw Unsupported(msg);
     default: throw CudaError(msg.empty() ? "CUDA error" : msg);
   }
-}
-
-std::string shape_str(const Shape& s) {
-  std::ostringstream os;
-  os << "(";
-  for (std::size_t i = 0; i < s.size(); ++i) os << (i ? ", " : "") << s[i];
-  if (s.size() == 1) os << ",";
-  os << ")";
-  return os.str();
 }
 
 void ConvSpec::validate() const {
@@ -133,11 +129,11 @@ DevicePlan plan_device_fold(const ConvSpec& spec, std::int64_t factor, std::int6
   return out;
 }
 
-std::uint64_t count_macs(const ConvSpec& spec) {
+MacCount count_macs(const ConvSpec& spec) {
   spec.validate();
   const auto u = [](std::int64_t v) { return static_cast<std::uint64_t>(v); };
-  return u(spec.batch()) * u(spec.out_h()) * u(spec.out_w()) * u(spec.out_c()) * u(spec.k_h()) * u(spec.k_w()) *
-         u(spec.in_c());
+  return MacCount{u(spec.batch()) * u(spec.out_h()) * u(spec.out_w()) * u(spec.out_c()) * u(spec.k_h()) *
+                  u(spec.k_w()) * u(spec.in_c())};
 }
 
 MacReport mac_report(const ConvSpec& spec, const FoldPlan& plan, std::int64_t align) {
@@ -146,18 +142,18 @@ MacReport mac_report(const ConvSpec& spec, const FoldPlan& plan, std::int64_t al
   spec.validate();
   MacReport r;
   r.factor = plan.factor;
-  r.original = count_macs(spec);
+  r.original = count_macs(spec).macs;
   ConvSpec folded = spec;
   folded.input_shape = plan.folded_input_shape;
   folded.filter_shape = plan.expanded_filter_shape;
   folded.stride_w = 1;
-  r.dense_folded = count_macs(folded);
+  r.dense_folded = count_macs(folded).macs;
   r.grouped_folded = r.dense_folded / static_cast<std::uint64_t>(plan.factor);
   ConvSpec padded = spec;
   const std::int64_t cin_pad = (spec.in_c() + align - 1) / align * align;
   padded.input_shape[3] = cin_pad;
   padded.filter_shape[2] = cin_pad;
-  r.zero_padded = count_macs(padded);
+  r.zero_padded = count_macs(padded).macs;
   return r;
 }
 
@@ -165,6 +161,13 @@ void conv2d_exact(const float* x, const float* w, float* y, const ConvSpec& spec
   spec.validate();
   const wf_conv_desc d = spec.desc();
   throw_on(wf_conv_direct_fwd(x, w, y, &d, stream));
+}
+
+void conv2d_grouped(const float* x, const float* w_dense, float* y, const ConvSpec& spec, std::int64_t groups,
+                    void* stream) {
+  spec.validate();
+  const wf_conv_desc d = spec.desc();
+  throw_on(wf_conv_grouped_fwd(x, w_dense, y, &d, groups, stream));
 }
 
 void bias_add(const float* y, const float* b, float* out, std::int64_t n, std::int64_t c, bool relu, void* stream) {

@@ -39,8 +39,9 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
 int sm_count(int device);
 
 // Exact-order fp32 direct conv (reference conv2d semantics, with padding).
-wf_status launch_conv_direct(const wf_conv_desc& d, const float* x, const float* w, float* y, cudaStream_t st,
-                             std::string* err);
+// groups > 1: grouped conv of a block-diagonal dense filter (diagonal blocks only).
+wf_status launch_conv_direct(const wf_conv_desc& d, const float* x, const float* w, float* y, int groups,
+                             cudaStream_t st, std::string* err);
 wf_status launch_cast_f32(const float* x, void* y, long long n, wf_dtype to, cudaStream_t st, std::string* err);
 wf_status launch_bias_add(const float* y, const float* b, float* out, long long n, int C, int relu, cudaStream_t st,
                           std::string* err);
