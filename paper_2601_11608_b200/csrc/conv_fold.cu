@@ -232,11 +232,14 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   // 0x4000 (profiling / cross-check): build the TMA-layout A tile with the row
   // producer instead -- same shared-memory image, so results are bit-identical
   const bool tf32 = (in_t == WF_TF32);
-  const int prod = ((S.prod == 0 || S.prod == 3) && (epilogue & WF_EPI_ROW_PRODUCER) && !tf32) ? 1 : S.prod;
+  const int prod =
+      ((S.prod == 0 || S.prod == 3 || S.prod == 4) && (epilogue & WF_EPI_ROW_PRODUCER) && !tf32) ? 1 : S.prod;
   a.prod = prod;
   a.off_raw = a.off_bias + kMaxAccCols * 4;
-  a.raw_slots = (prod == 1 || prod == 2) ? S.raw_slots : 0;
-  a.raw_slot_bytes = S.raw_slot_bytes;
+  // raw staging: the planner's slots for its own producer; the row-ring
+  // cross-check (prod 1 forced on a TMA / gather plan) sizes its ring here
+  a.raw_slots = (prod == S.prod) ? ((prod == 1 || prod == 2 || prod == 4) ? S.raw_slots : 0) : kRawSlots;
+  a.raw_slot_bytes = (prod == S.prod) ? S.raw_slot_bytes : raw_slot_bytes_for(d.w * d.c * S.esize);
   if (prod == 1 && S.prod != 1) {  // forced: make room for the ring by dropping A stages
     while (a.stages > 2 && a.off_raw + a.raw_slots * a.raw_slot_bytes + 1024 > kSmemLimit) {
       --a.stages;
@@ -249,7 +252,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   a.rows_per_stage = 0;
   a.log_wbox = 0;
   while ((1 << a.log_wbox) < a.Wbox) ++a.log_wbox;
-  for (int b = 0; b < S.s && prod == 1; ++b) {  // folded raw rows of one stage (row producer)
+  for (int b = 0; b < S.s && (prod == 1 || prod == 4); ++b) {  // folded raw rows of one stage (row producers)
     if (!S.has_res[b]) continue;
     const int rows = S.amax[b] - S.amin[b] + static_cast<int>(p.tile_rows) * S.tps;
     for (int i = 0; i < rows; ++i) {
@@ -373,11 +376,11 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   }
 
   const int grid = a.n_tiles * a.ctas_per_ntile;
-  if (S.pair == 2 && (prod == 1 || prod == 2)) {
+  if (S.pair == 2 && (prod == 1 || prod == 2 || prod == 4)) {
     *err = "the row producers run single-CTA plans";
     return WF_UNSUPPORTED;
   }
-  if (tf32 && (S.CH != 32 || prod == 1 || prod == 2)) {
+  if (tf32 && (S.CH != 32 || prod == 1 || prod == 2 || prod == 4)) {
     *err = "tf32 plans use 32-column epilogue chunks and the TMA producer";
     return WF_UNSUPPORTED;
   }
@@ -397,6 +400,8 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     L.fn = conv_kernel_fn<0>(kind, out_dtype, S.CH);
   } else if (prod == 1) {
     L.fn = conv_kernel_fn<1>(kind, out_dtype, S.CH);
+  } else if (prod == 4) {
+    L.fn = conv_kernel_fn<4>(kind, out_dtype, S.CH);
   } else {
     L.fn = conv_kernel_fn<2>(kind, out_dtype, S.CH);
   }
@@ -405,7 +410,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     return WF_UNSUPPORTED;
   }
   L.grid = grid;
-  L.block = (prod == 1 || prod == 2) ? 320 + 32 * kGatherWarps : 320;
+  L.block = (prod == 4) ? 320 + 32 * kGatherWarps4 : ((prod == 1 || prod == 2) ? 320 + 32 * kGatherWarps : 320);
   L.smem = smem;
   cudaError_t e = ensure_smem(L.fn, L.device, smem);
   if (e != cudaSuccess) {

@@ -43,6 +43,9 @@ constexpr int kMaxTable = 384;  // schedule entries per launch (constant bank)
 #endif
 constexpr int kIssueGroup = WFB_ISSUE_GROUP;  // MMAs whose table words are loaded together
 constexpr int kGatherWarps = 4;  // row-staged producer: transposer warps 10..13
+// direct gather producer (kProd 4): warps 10..17 (row loads are latency-bound:
+// more warps beat the 128-register cap of 16 warps)
+constexpr int kGatherWarps4 = 8;
 constexpr int kMaxKsplit = 8;    // A stages per M tile (im2col kh ranges)
 constexpr int kMaxStageRows = 64;  // folded raw rows per A stage (row producer)
 
@@ -81,7 +84,7 @@ struct ConvArgs {
   int H, Q, Qr, NR;               // core cols per pixel, regions per residue (+shift), rows per region
   int lbo_a;                      // bytes between core-column regions
   int prod;                       // A producer (plan.hpp Schedule::prod)
-  int off_raw, raw_slots, raw_slot_bytes;  // staged-row ring (kProd 1/2)
+  int off_raw, raw_slots, raw_slot_bytes;  // staged-row ring (kProd 1/2) / the two raw unit slots (kProd 4)
   int rows_per_stage;             // folded: raw rows per A stage
   int log_wbox;                   // log2(Wbox)
   signed char row_b[kMaxStageRows], row_i[kMaxStageRows], row_a[kMaxStageRows];  // folded stage rows
@@ -474,6 +477,129 @@ __device__ __forceinline__ void transpose_row(const RowProd& p, const FoldChunks
   }
 }
 
+// ---- staged gather producer (kProd 4) ------------------------------------------
+// For rows whose pitch TMA cannot address (AlexNet: 227 px x 3 ch x 2 B = 1362
+// bytes, 2-byte aligned) the A stages are built from the rows themselves, with
+// no workspace and no second pass over the input. The input rows of a stage
+// unit are contiguous in x: warp 0 lands the whole span (its 16-byte aligned
+// superset) in a raw slot with bulk copies (two slots, the next unit's copy in
+// flight while this one is realigned; the L2 is prefetched a further unit
+// ahead). The gather warps then realign it: each lane reads aligned 16-byte
+// blocks of a row's folded window from the slot, takes its right neighbour's
+// block by a warp shuffle, funnel-shifts the pair by the row's misalignment
+// and stores the 16-byte core column at its place in the A layout -- the same
+// shared-memory image the TMA boxes land (plan.hpp), so the MMA schedule is
+// unchanged. (Reading the rows with per-lane global loads instead was bound by
+// their latency: ~1.5x slower on AlexNet.) Chunk k of a row window is core
+// column k % Q of folded pixel c0 + k / Q; with the shift region (Qr = Q + 1)
+// core column 0 of pixel w'' + 1 is stored again as region Q of column w''.
+
+// Input bytes [s0, s1) (relative to x, 16-byte aligned superset) holding the
+// rows [oh0*s - ph, (oh0 + tps*OHt - 1)*s - ph + KH) of stage unit u, clipped
+// to the image; empty when the unit lies past the batch.
+__device__ __forceinline__ void unit_span(const ConvArgs& a, const RowProd& p, int u, int& n, int& oh0,
+                                          long long& s0, long long& s1) {
+  tile_origin<1>(a, u, 0, 0u, n, oh0);
+  s0 = s1 = 0;
+  if (n >= p.n_img) return;
+  const int lo = max(0, oh0 * p.s - p.ph), hi = min(p.H, (oh0 + a.tps * p.OHt - 1) * p.s - p.ph + p.kh_count);
+  if (hi <= lo) return;
+  const long long img = static_cast<long long>(n) * p.in_img_bytes;
+  s0 = (img + static_cast<long long>(lo) * p.rb) & ~15LL;
+  s1 = (img + static_cast<long long>(hi) * p.rb + 15) & ~15LL;
+}
+struct GatherRow {
+  uint4 v[4];     // this lane's aligned blocks lane + 32i of the window
+  int s2;         // window misalignment in bytes (even; warp-uniform)
+  uint32_t roff;  // A-stage offset of the row: residue region + region row
+};
+
+// Loads of raw row r of the stage unit at (image n, first output row oh0) from
+// the raw slot holding input bytes [s0, ...). Everything but the block index
+// is warp-uniform; per-block bounds are 32-bit offsets from the row start.
+__device__ __forceinline__ void gather_load(const RowProd& p, int n, int oh0, int r, int lane, int nit,
+                                            uint32_t slot, long long s0, GatherRow& g) {
+  const uint32_t e = ptx::ld_shared_u32(p.row_tab + 4 * r);
+  const int ih = (oh0 + static_cast<int>(static_cast<int8_t>(e >> 16))) * p.s + static_cast<int>(e & 0xFF);
+  g.roff = (e & 0xFF) * p.region_bytes + ((e >> 8) & 0xFF) * p.Wbox * 16;
+  const bool valid = ih >= 0 && ih < p.H && n < p.n_img;
+  const long long row = static_cast<long long>(n) * p.in_img_bytes + static_cast<long long>(ih) * p.rb;
+  const int wrel = p.c0 * p.pix;                        // window start relative to the row (< 0: left padding)
+  const int mis = static_cast<int>((row + wrel) & 15);  // (row + wrel) mod 16, wrel possibly negative
+  g.s2 = mis;
+  const int rel0 = wrel - mis;                          // first block, relative to the row start
+  const uint32_t sb = slot + static_cast<uint32_t>(row + rel0 - s0);  // its slot address (16-byte aligned)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int brel = rel0 + 16 * (lane + 32 * i);
+    // only blocks holding row bytes are read (an aligned block never crosses a page)
+    const bool ok = valid && i < nit && brel > -16 && brel < p.rb;
+    g.v[i] = ok ? ptx::ld_shared_v4(sb + 16 * (lane + 32 * i)) : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+// Bytes [s2, s2 + 16) of the 32-byte pair (a, b), s2 = 4*Q4 + (0 | 2).
+template <int Q4>
+__device__ __forceinline__ uint4 realign(const uint4& a, const uint4& b, uint32_t sh) {
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  return make_uint4(__funnelshift_r(w[Q4], w[Q4 + 1], sh), __funnelshift_r(w[Q4 + 1], w[Q4 + 2], sh),
+                    __funnelshift_r(w[Q4 + 2], w[Q4 + 3], sh), __funnelshift_r(w[Q4 + 3], w[Q4 + 4], sh));
+}
+
+// Zero the chunk bytes outside the row: keep [lo, hi) of the 16.
+__device__ __forceinline__ uint4 edge_mask(uint4 c, int lo, int hi) {
+  uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int a = min(max(lo - 4 * k, 0), 4), b = min(max(hi - 4 * k, 0), 4);
+    const uint32_t keep_hi = (b >= 4) ? 0xFFFFFFFFu : ((1u << (8 * b)) - 1u);
+    const uint32_t drop_lo = (a >= 4) ? 0xFFFFFFFFu : ((1u << (8 * a)) - 1u);
+    w[k] &= keep_hi & ~drop_lo;
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int Q4, bool kShift>
+__device__ __forceinline__ void gather_store_q(const GatherRow& g, const uint4 (&t)[4], uint32_t rbase, int lane,
+                                               const int (&d1)[4], const int (&d2)[4], unsigned edge, int o0, int rb) {
+  const uint32_t sh = static_cast<uint32_t>(g.s2 & 3) * 8;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (d1[i] < 0 && (!kShift || d2[i] < 0)) continue;
+    // right neighbour block: lane + 1's block i, or (lane 31) lane 0's block i + 1
+    const uint4 nx = (lane == 31) ? (i < 3 ? t[i + 1] : make_uint4(0u, 0u, 0u, 0u)) : t[i];
+    uint4 c = realign<Q4>(g.v[i], nx, sh);
+    if ((edge >> i) & 1u) {  // chunk at a row edge (per lane, row independent)
+      const int o = o0 + 512 * i;
+      c = edge_mask(c, -o, rb - o);
+    }
+    if (d1[i] >= 0) ptx::st_shared_v4(rbase + d1[i], c.x, c.y, c.z, c.w);
+    if (kShift && d2[i] >= 0) ptx::st_shared_v4(rbase + d2[i], c.x, c.y, c.z, c.w);
+  }
+}
+
+__device__ __forceinline__ uint32_t shfl_next(uint32_t v, int lane) {
+  return __shfl_sync(0xffffffffu, v, (lane + 1) & 31);
+}
+
+// Realign the row's blocks into 16-byte chunks and store them into the A stage.
+template <bool kShift>
+__device__ __forceinline__ void gather_store(const GatherRow& g, uint32_t stage, int lane, const int (&d1)[4],
+                                             const int (&d2)[4], unsigned edge, int o0, int rb) {
+  uint4 t[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    t[i] = make_uint4(shfl_next(g.v[i].x, lane), shfl_next(g.v[i].y, lane), shfl_next(g.v[i].z, lane),
+                      shfl_next(g.v[i].w, lane));
+  const uint32_t rbase = stage + g.roff;
+  switch (g.s2 >> 2) {  // warp-uniform
+    case 0: gather_store_q<0, kShift>(g, t, rbase, lane, d1, d2, edge, o0, rb); break;
+    case 1: gather_store_q<1, kShift>(g, t, rbase, lane, d1, d2, edge, o0, rb); break;
+    case 2: gather_store_q<2, kShift>(g, t, rbase, lane, d1, d2, edge, o0, rb); break;
+    default: gather_store_q<3, kShift>(g, t, rbase, lane, d1, d2, edge, o0, rb); break;
+  }
+}
+
 template <int kKind, int kPair>
 __device__ __forceinline__ void issue_mma(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   if constexpr (kPair == 2) {
@@ -510,7 +636,7 @@ __device__ __forceinline__ void arrive_at(uint32_t bar) {
 // unit issues half of the pieces; a stage is refilled only after both CTAs'
 // MMAs released it (multicast commits, empty barriers of count 2).
 template <int kKind, typename OutT, int CH, int kProd, int kPair = 1, int kMc = 0>
-__global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
+__global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kGatherWarps4 : kGatherWarps), 1)
     conv_fold_kernel(const __grid_constant__ ConvArgs a, const __grid_constant__ TmaMaps maps) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
@@ -540,7 +666,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   const int ncols = a.nt_cols[ntile];
   const int col0 = a.nt_col0[ntile];
 
-  if (kProd == 1)  // folded stage-row table of the row producer (b | i << 8 | a << 16)
+  if (kProd == 1 || kProd == 4)  // folded stage-row table of the row producers (b | i << 8 | a << 16)
     for (int r = threadIdx.x; r < a.rows_per_stage; r += blockDim.x)
       reinterpret_cast<uint32_t*>(gbase + 768)[r] = static_cast<uint32_t>(static_cast<uint8_t>(a.row_b[r])) |
                                                     (static_cast<uint32_t>(static_cast<uint8_t>(a.row_i[r])) << 8) |
@@ -552,7 +678,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
-      mbar_init(bar_full + 8 * i, kProd == 0 ? 1 : kGatherWarps);  // TMA: one expect_tx; rows: one arrive per transposer
+      // TMA: one expect_tx; rows: one arrive per transposer / gather warp
+      mbar_init(bar_full + 8 * i, kProd == 0 ? 1 : (kProd == 4 ? kGatherWarps4 : kGatherWarps));
       mbar_init(bar_empty + 8 * i, (kMc && !prof(a, 0x2000)) ? 2 : 1);  // multicast: both CTAs' MMAs release the stage
     }
     for (int i = 0; i < a.n_acc; ++i) {
@@ -565,7 +692,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
     mbar_init(bar_bpeer, 1);
     for (int i = 0; i < a.raw_slots; ++i) {
       mbar_init(bar_raw_full + 8 * i, 1);
-      mbar_init(bar_raw_empty + 8 * i, 1);
+      mbar_init(bar_raw_empty + 8 * i, kProd == 4 ? kGatherWarps4 : 1);  // staged gather: every gather warp releases
     }
     fence_barrier_init();
   }
@@ -586,7 +713,103 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * kGatherWarps, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (kProd != 0 && (warp == 0 || warp >= 10)) {
+  if (kProd == 4 && warp >= 10) {
+    // ===================== direct gather producer (warps 10..17) =====================
+    const RowProd rp = row_prod(a, base + 768);
+    const int gw = warp - 10;
+    // this lane's chunks (row independent): region offsets of core column k % Q of
+    // folded column k / Q, and of its shift-region copy (-1: not stored)
+    int d1[4], d2[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = lane + 32 * i;
+      const int q = k % rp.Q, w2 = k / rp.Q;
+      d1[i] = (w2 < rp.Wbox) ? q * rp.lbo + w2 * 16 : -1;
+      d2[i] = (rp.Qr > rp.Q && q == 0 && w2 >= 1 && w2 <= rp.Wbox) ? rp.Q * rp.lbo + (w2 - 1) * 16 : -1;
+    }
+    const int nit = (rp.Q * rp.Wbox + 2 + 31) / 32;  // block iterations per row (<= 4, planner-checked)
+    const bool has_shift = rp.Qr > rp.Q;              // shift region (uniform)
+    // chunks at a row edge (row-relative offset o outside [0, rb - 16]): byte-masked
+    const int o0 = rp.c0 * rp.pix + 16 * lane;
+    unsigned edge = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int o = o0 + 512 * i;
+      if (o < 0 || o + 16 > rp.rb) edge |= 1u << i;
+    }
+    const int rps = rp.rows_per_stage;
+    const int nstages = a.stages, stage_bytes = a.stage_bytes, stride = a.unit_stride, units = a.num_units;
+    const uint32_t a_base = base + a.off_a, raw_base = base + a.off_raw;
+    GatherRow g0, g1;
+    constexpr int P = kGatherWarps4;
+    int it = 0;
+    for (int u = local; u < units; u += stride, ++it) {
+      const int stage = it % nstages;
+      const uint32_t round = static_cast<uint32_t>(it / nstages);
+      const int rs = it & 1;  // raw slot of this unit
+      int n, oh0;
+      long long s0, s1;
+      unit_span(a, rp, u, n, oh0, s0, s1);
+      const uint32_t slot = raw_base + rs * rp.raw_slot_bytes;
+      mbar_wait(bar_raw_full + 8 * rs, static_cast<uint32_t>(it >> 1) & 1u);
+      // two rows in flight: load one while the other is realigned and stored
+      int r = gw;
+      if (r < rps) gather_load(rp, n, oh0, r, lane, nit, slot, s0, g0);
+      if (r + P < rps) gather_load(rp, n, oh0, r + P, lane, nit, slot, s0, g1);
+      mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
+      const uint32_t dst = a_base + stage * stage_bytes;
+      auto store = [&](const GatherRow& g) {
+        if (has_shift) gather_store<true>(g, dst, lane, d1, d2, edge, o0, rp.rb);
+        else gather_store<false>(g, dst, lane, d1, d2, edge, o0, rp.rb);
+      };
+      for (; r < rps; r += 2 * P) {
+        store(g0);
+        if (r + 2 * P < rps) gather_load(rp, n, oh0, r + 2 * P, lane, nit, slot, s0, g0);
+        if (r + P < rps) {
+          store(g1);
+          if (r + 3 * P < rps) gather_load(rp, n, oh0, r + 3 * P, lane, nit, slot, s0, g1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_raw_empty + 8 * rs);  // the slot's rows are consumed
+      fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_full + 8 * stage);
+    }
+  } else if (kProd == 4 && warp == 0) {
+    // B operand, then each stage unit's raw input span into the two raw slots
+    if (elect_one()) {
+      const uint8_t* gb = reinterpret_cast<const uint8_t*>(a.nt_bsrc[ntile]);
+      const int bb = a.nt_bbytes[ntile];
+      mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
+      for (int off = 0; off < bb; off += 32768)
+        bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
+      const RowProd rp = row_prod(a, base + 768);
+      const int stride = a.unit_stride, units = a.num_units;
+      auto prefetch_unit = [&](int u) {  // L2 prefetch of a later unit's span
+        int n, oh0;
+        long long s0, s1;
+        unit_span(a, rp, u, n, oh0, s0, s1);
+        if (s1 > s0) prefetch_l2_bulk(rp.x + s0, static_cast<uint32_t>(s1 - s0));
+      };
+      for (int u = local; u < units && u < local + 2 * stride; u += stride) prefetch_unit(u);
+      int it = 0;
+      for (int u = local; u < units; u += stride, ++it) {
+        const int rs = it & 1;
+        mbar_wait(bar_raw_empty + 8 * rs, (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
+        if (u + 2 * stride < units) prefetch_unit(u + 2 * stride);
+        int n, oh0;
+        long long s0, s1;
+        unit_span(a, rp, u, n, oh0, s0, s1);
+        const uint32_t bytes = static_cast<uint32_t>(s1 - s0);
+        const uint32_t slot = base + a.off_raw + rs * rp.raw_slot_bytes;
+        mbar_arrive_expect_tx(bar_raw_full + 8 * rs, bytes);
+        for (uint32_t off = 0; off < bytes; off += 32768)
+          bulk_g2s(slot + off, rp.x + s0 + off, min(32768u, bytes - off), bar_raw_full + 8 * rs);
+      }
+    }
+    __syncwarp();
+  } else if ((kProd == 1 || kProd == 2) && (warp == 0 || warp >= 10)) {
     // ===================== row-staged producer =====================
     // warp 0 (one lane): B operand, then one bulk copy per raw input row into
     // the slot ring; warps 10..12: transpose staged rows into the A stages.
@@ -1067,22 +1290,29 @@ const void* kernel_ptr() {
 // kind: 0 kind::f16, 1 kind::tf32; out: output dtype; ch: epilogue chunk.
 template <int kProd>
 const void* conv_kernel_fn(int kind, wf_dtype out, int ch) {
-  if constexpr (kProd != 0) {
-    if (kind == 1) return nullptr;  // tf32 runs with the TMA producer only
-  } else if (kind == 1) {
-    if (ch != 32) return nullptr;
-    if (out == WF_BF16) return kernel_ptr<1, __nv_bfloat16, 32, kProd>();
-    if (out == WF_F16) return kernel_ptr<1, __half, 32, kProd>();
-    return kernel_ptr<1, float, 32, kProd>();
+  if constexpr (kProd == 4) {  // kind::f16, 32-column chunks (448 threads: CH=64 would spill)
+    if (kind == 1 || ch != 32) return nullptr;
+    if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 32, kProd>();
+    if (out == WF_F16) return kernel_ptr<0, __half, 32, kProd>();
+    return kernel_ptr<0, float, 32, kProd>();
+  } else {
+    if constexpr (kProd != 0) {
+      if (kind == 1) return nullptr;  // tf32 runs with the TMA producer only
+    } else if (kind == 1) {
+      if (ch != 32) return nullptr;
+      if (out == WF_BF16) return kernel_ptr<1, __nv_bfloat16, 32, kProd>();
+      if (out == WF_F16) return kernel_ptr<1, __half, 32, kProd>();
+      return kernel_ptr<1, float, 32, kProd>();
+    }
+    if (ch == 64) {
+      if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 64, kProd>();
+      if (out == WF_F16) return kernel_ptr<0, __half, 64, kProd>();
+      return kernel_ptr<0, float, 64, kProd>();
+    }
+    if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 32, kProd>();
+    if (out == WF_F16) return kernel_ptr<0, __half, 32, kProd>();
+    return kernel_ptr<0, float, 32, kProd>();
   }
-  if (ch == 64) {
-    if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 64, kProd>();
-    if (out == WF_F16) return kernel_ptr<0, __half, 64, kProd>();
-    return kernel_ptr<0, float, 64, kProd>();
-  }
-  if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 32, kProd>();
-  if (out == WF_F16) return kernel_ptr<0, __half, 32, kProd>();
-  return kernel_ptr<0, float, 32, kProd>();
 }
 
 // CTA-pair kernel (cluster of 2, cta_group::2 MMAs), TMA producer, kind::f16.
@@ -1093,5 +1323,6 @@ const void* conv_kernel_fn_mc(wf_dtype out, int ch);
 extern template const void* conv_kernel_fn<0>(int, wf_dtype, int);
 extern template const void* conv_kernel_fn<1>(int, wf_dtype, int);
 extern template const void* conv_kernel_fn<2>(int, wf_dtype, int);
+extern template const void* conv_kernel_fn<4>(int, wf_dtype, int);
 
 }  // namespace wfb

@@ -51,7 +51,11 @@ py::dict raw_dict(const wf_fold_plan& p) {
   d["tile_rows"] = p.tile_rows; d["wbox"] = p.wbox; d["nrows"] = p.nrows; d["mma_entries"] = p.mma_entries;
   d["packed_bytes"] = p.packed_bytes; d["epi_chunk"] = p.epi_chunk;
   d["variant"] = p.variant == WF_VARIANT_UNFOLDED ? "unfolded" : "fold";
-  d["producer"] = p.producer == 0 ? "tma" : (p.producer == 1 ? "gather" : (p.producer == 2 ? "im2col" : "repitch+tma"));
+  d["producer"] = p.producer == 0   ? "tma"
+                  : p.producer == 1 ? "row-ring"
+                  : p.producer == 2 ? "im2col"
+                  : p.producer == 3 ? "repitch+tma"
+                                    : "gather";
   d["pitched_w"] = p.pitched_w; d["workspace_bytes"] = p.workspace_bytes; d["cta_pair"] = p.cta_pair; d["stage_tiles"] = p.stage_tiles; d["kstep_mode"] = p.kstep_mode;
   d["in_dtype"] = p.in_dtype; d["launch_opts"] = p.launch_opts; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;
   return d;

@@ -9,6 +9,17 @@
 namespace wfb {
 
 namespace {
+// Producer-4 request of the planner call on this thread: -1 read WF_GATHER,
+// 0 / 1 forced (schedule_from_plan rebuilds a plan with its own producer).
+thread_local int g_gather_req = -1;
+struct GatherScope {
+  int saved;
+  explicit GatherScope(int v) : saved(g_gather_req) { g_gather_req = v; }
+  ~GatherScope() { g_gather_req = saved; }
+};
+}  // namespace
+
+namespace {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 int64_t floor_div(int64_t a, int64_t b) {
@@ -247,11 +258,12 @@ static wf_status make_schedule_variant(const wf_conv_desc& d, int64_t f_req, int
     const bool want = (tps_req > 0) ? tps_req == cand
                                     : (env_tps ? env_tps == cand
                                                : cand == 2 && s1.ohb >= cand && d.n * ceil_div(s1.ohb, cand) >= 4 * 148);
-    if (!want || !(s1.prod == 0 || s1.prod == 3) || s1.pair != 1) continue;
+    if (!want || !(s1.prod == 0 || s1.prod == 3 || s1.prod == 4) || s1.pair != 1) continue;
     Schedule s2;
     std::string e2;
     if (make_schedule_tps(d, f_req, gs_req, in_dtype, cand, &s2, &e2, kpair_req, 0) == WF_OK &&
-        s2.plan.status == WF_FOLD_APPLY && s2.stages >= 2 && s2.ntiles.size() == s1.ntiles.size()) {
+        s2.plan.status == WF_FOLD_APPLY && s2.stages >= 2 && s2.ntiles.size() == s1.ntiles.size() &&
+        s2.prod == s1.prod) {
       *out = std::move(s2);
       return WF_OK;
     }
@@ -328,9 +340,12 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   const int64_t Wfo = ceil_div(OW, r);
   // TMA boxes need the folded view to be a pure reshape with a 16-byte row
   // pitch. When W % f != 0 or the row pitch is not a 16-byte multiple (AlexNet:
-  // W=227, 1362-byte rows)
-  // pitch, the input is first re-pitched into a workspace of Wp columns
-  // (Wp % f == 0, 16-byte rows, zero tail; producer 3) and then read by TMA.
+  // W=227, 1362-byte rows) the input is first re-pitched into a workspace of
+  // Wp columns (Wp % f == 0, 16-byte rows, zero tail; producer 3) and then read
+  // by TMA. WF_GATHER=1 selects producer 4 instead where it applies: the rows
+  // are staged in shared memory and realigned by gather warps -- no workspace
+  // (AlexNet b512: 162 MB less device memory), bit-identical, but measured
+  // 1.13-1.16x slower than re-pitch + multicast TMA.
   int64_t Wp = d.w;
   while (Wp % f != 0 || (Wp * d.c * S.esize) % 16 != 0) ++Wp;
   S.Wp = Wp;
@@ -367,11 +382,13 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // for the TMA destination: pad rows so NR*Wbox*16 % 128 == 0
   while ((NR * Wbox) % 8 != 0) ++NR;
   if (NR > 256) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
-  if (S.prod == 1) {  // the row producer enumerates a stage's raw rows in a 64-entry table
+  if (S.prod == 3) {  // direct gather (producer 4): 16-bit data, <= 128 row blocks, <= 64 raw rows per stage
     int64_t rows = 0;
     for (int b = 0; b < sh; ++b)
-      if (S.has_res[b]) rows += S.amax[b] - S.amin[b] + OHt;
-    if (rows > 64) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
+      if (S.has_res[b]) rows += S.amax[b] - S.amin[b] + tps * OHt;
+    const char* env = std::getenv("WF_GATHER");
+    const bool want = g_gather_req >= 0 ? g_gather_req == 1 : (env && env[0] == '1');
+    if (in_dtype != WF_TF32 && S.esize == 2 && Q * Wbox + 2 <= 128 && rows <= 64 && want) S.prod = 4;
   }
 
   // ---- MMA groups ---------------------------------------------------------
@@ -395,6 +412,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // 2-byte outputs: 64-column chunks (16 bf16 = 32 B per thread and row);
   // tf32 (fp32 outputs): 32-column chunks (8 fp32 = 32 B).
   S.CH = (in_dtype != WF_TF32 && S.Ng % 64 == 0) ? 64 : 32;
+  if (S.prod == 4 && S.CH != 32) S.prod = 3;  // the gather kernel is built for 32-column epilogue chunks
   std::vector<int64_t> lo(G), hi(G);
   for (int64_t g = 0; g < G; ++g) {
     lo[g] = INT64_MAX;
@@ -571,6 +589,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // tools/probes/sw32_probe.cu). Otherwise the canonical no-swizzle layout of
   // 16-byte core columns ([q][row][folded col][16 B], + the shift region).
   S.sw32 = !S.kpair && !S.need_shift && Q >= 2 && in_dtype != WF_TF32;
+  if (S.sw32 && S.prod == 4) S.prod = 3;  // the gather warps write the no-swizzle layout only
   if (S.sw32) {
     S.qs.clear();
     for (int64_t g = 0; g < G; ++g)
@@ -607,7 +626,12 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   const int staging = kStagingBytes;   // 4 epilogue warps x 2 x 2 KB
   const int a_pad = kTileM * 16;
   const int bias_bytes = kMaxAccCols * 4;
-  const int64_t ring = (S.prod == 1 || S.prod == 2) ? static_cast<int64_t>(kRawSlots) * raw_slot_bytes_for(d.w * d.c * S.esize) : 0;
+    // raw input staging: the row producers' ring of row slots (prod 1/2), or
+  // two slots holding a stage unit's contiguous row span (prod 4)
+  const int64_t unit_rows = std::min<int64_t>(d.h, (tps * OHt - 1) * sh + d.kh);
+  const int64_t unit_slot = (unit_rows * d.w * d.c * S.esize + 32 + 127) / 128 * 128;
+  const int64_t ring = (S.prod == 1 || S.prod == 2) ? static_cast<int64_t>(kRawSlots) * raw_slot_bytes_for(d.w * d.c * S.esize)
+                       : (S.prod == 4 ? 2 * unit_slot : 0);
   // A stages that fit beside a resident B of max_b bytes (>= 2, else false)
   auto fit_stages = [&](int64_t max_b) {
     const int64_t fixed = ctrl_bytes + staging + a_pad + 128 + (max_b + 127) / 128 * 128 + bias_bytes + ring + 1024;
@@ -899,8 +923,8 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   p.table_bytes = (p.mma_entries * 24 + G * 4 + 127) / 128 * 128;
   p.packed_bytes = p.table_bytes + b_cursor;
   p.epi_chunk = S.CH;
-  S.raw_slots = kRawSlots;
-  S.raw_slot_bytes = raw_slot_bytes_for(d.w * d.c * S.esize);
+  S.raw_slots = (S.prod == 4) ? 2 : kRawSlots;
+  S.raw_slot_bytes = (S.prod == 4) ? static_cast<int>(unit_slot) : raw_slot_bytes_for(d.w * d.c * S.esize);
   p.variant = WF_VARIANT_FOLD;
   p.producer = S.prod;
   p.pitched_w = (S.prod == 3) ? S.Wp : 0;
@@ -1095,6 +1119,7 @@ wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
     *err = "plan is not an Apply plan";
     return WF_INVALID_ARGUMENT;
   }
+  GatherScope gather_scope(p.producer == 4 ? 1 : 0);  // the plan's own producer, whatever WF_GATHER says now
   wf_status st = (p.variant == WF_VARIANT_UNFOLDED)
                      ? make_schedule_unfolded(d, static_cast<wf_dtype>(p.in_dtype), out, err)
                      : make_schedule(d, p.f, p.group_size, static_cast<wf_dtype>(p.in_dtype), out, err,
@@ -1106,6 +1131,10 @@ wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
     return WF_SHAPE_MISMATCH;
   }
   out->plan.launch_opts = p.launch_opts;
+  if (out->prod != p.producer) {
+    *err = "plan producer does not match this conv descriptor";
+    return WF_SHAPE_MISMATCH;
+  }
   return WF_OK;
 }
 

@@ -117,6 +117,20 @@ __device__ __forceinline__ void st_global_v8(void* ptr, const uint32_t* v) {
                "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
 }
+// 16-byte read-only global load, not allocated in L1 (the gather producer's
+// row blocks: read once per CTA, the L1/shared data path is the MMA's).
+// Not volatile and no memory clobber: the compiler may hoist it.
+__device__ __forceinline__ uint4 ld_global_nc_v4(const void* ptr) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(ptr));
+  return v;
+}
+// Prefetch [ptr, ptr + bytes) into L2 (16-byte aligned, size a multiple of 16).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");

@@ -94,7 +94,7 @@ def test_device_plans_for_configs(name, oracle):
     assert d["issued_macs"] >= d["useful_macs"]
 
 
-def test_alexnet_plan_repitches_then_uses_tma():
+def test_alexnet_plan_repitches_or_gathers_unaligned_rows(monkeypatch):
     # W = 227 is prime: no pure-reshape fold exists (the reference says WidthNotDivisible,
     # src/fold.cpp:58) and the 1362-byte row pitch cannot be a TMA stride, so the
     # generalized fold re-pitches x into a 232-pixel workspace (zero tail) on the
@@ -105,6 +105,10 @@ def test_alexnet_plan_repitches_then_uses_tma():
     assert (d["f"], d["r"], d["producer"]) == (8, 2, "repitch+tma")
     assert d["pitched_w"] == 232 and d["workspace_bytes"] == 512 * 227 * 232 * 3 * 2
     assert d["wf"] == 29 and d["wfo"] == 28 and d["ow"] == 55
+    # WF_GATHER=1: rows staged in shared memory and realigned by gather warps, no workspace
+    monkeypatch.setenv("WF_GATHER", "1")
+    d = wf.plan_fold([512, 227, 227, 3], [11, 11, 3, 96], 4, 4, 0, 0, dtype="bf16")["device"]
+    assert d["producer"] == "gather" and d["workspace_bytes"] == 0 and d["pitched_w"] == 0
     ref = wf.check_legality([512, 227, 227, 3], [11, 11, 3, 96], 8, stride_h=4, stride_w=4)
     assert ref["status"] == "fallback"  # the reference rule is unchanged
 
@@ -121,6 +125,7 @@ def test_unfolded_variant_plan():
 
 
 def test_generalized_legality_reasons():
+    # 64-column epilogue chunks: the gather kernel is not built for them -> re-pitch + TMA
     assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=16)["device"]["producer"] == "repitch+tma"
     assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=4, dtype="tf32")["device"]["pitched_w"] == 32
     assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], 2, 3, factor=16)["reason"] == "StrideOnFoldAxis"
