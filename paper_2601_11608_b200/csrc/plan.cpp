@@ -9,13 +9,14 @@
 namespace wfb {
 
 namespace {
-// Producer-4 request of the planner call on this thread: -1 read WF_GATHER,
-// 0 / 1 forced (schedule_from_plan rebuilds a plan with its own producer).
-thread_local int g_gather_req = -1;
-struct GatherScope {
+// Producer request for unaligned rows of the planner call on this thread:
+// -1 the default (WF_GATHER=1 overrides it), 3 / 4 forced (schedule_from_plan
+// rebuilds a plan with its own producer).
+thread_local int g_prod_req = -1;
+struct ProdScope {
   int saved;
-  explicit GatherScope(int v) : saved(g_gather_req) { g_gather_req = v; }
-  ~GatherScope() { g_gather_req = saved; }
+  explicit ProdScope(int v) : saved(g_prod_req) { g_prod_req = v; }
+  ~ProdScope() { g_prod_req = saved; }
 };
 }  // namespace
 
@@ -258,7 +259,7 @@ static wf_status make_schedule_variant(const wf_conv_desc& d, int64_t f_req, int
     const bool want = (tps_req > 0) ? tps_req == cand
                                     : (env_tps ? env_tps == cand
                                                : cand == 2 && s1.ohb >= cand && d.n * ceil_div(s1.ohb, cand) >= 4 * 148);
-    if (!want || !(s1.prod == 0 || s1.prod == 3 || s1.prod == 4) || s1.pair != 1) continue;
+    if (!want || !(s1.prod == 0 || s1.prod >= 3) || s1.pair != 1) continue;
     Schedule s2;
     std::string e2;
     if (make_schedule_tps(d, f_req, gs_req, in_dtype, cand, &s2, &e2, kpair_req, 0) == WF_OK &&
@@ -339,13 +340,13 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   int64_t Wf = ceil_div(d.w, f);
   const int64_t Wfo = ceil_div(OW, r);
   // TMA boxes need the folded view to be a pure reshape with a 16-byte row
-  // pitch. When W % f != 0 or the row pitch is not a 16-byte multiple (AlexNet:
-  // W=227, 1362-byte rows) the input is first re-pitched into a workspace of
-  // Wp columns (Wp % f == 0, 16-byte rows, zero tail; producer 3) and then read
-  // by TMA. WF_GATHER=1 selects producer 4 instead where it applies: the rows
-  // are staged in shared memory and realigned by gather warps -- no workspace
-  // (AlexNet b512: 162 MB less device memory), bit-identical, but measured
-  // 1.13-1.16x slower than re-pitch + multicast TMA.
+  // pitch (and a box must start 16-byte aligned: an element-granular view of
+  // x faults on B200, tools/probes/tma_elem_probe.cu). When W % f != 0 or the
+  // row pitch is not a 16-byte multiple (AlexNet: W=227, 1362-byte rows):
+  //  3 (default) re-pitch x into a workspace of Wp columns (Wp % f == 0,
+  //    16-byte rows, zero tail), then the 5-D TMA boxes;
+  //  4 (WF_GATHER=1) rows staged in shared memory and realigned by gather
+  //    warps -- no workspace, but measured 1.13-1.16x slower than 3.
   int64_t Wp = d.w;
   while (Wp % f != 0 || (Wp * d.c * S.esize) % 16 != 0) ++Wp;
   S.Wp = Wp;
@@ -382,13 +383,18 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // for the TMA destination: pad rows so NR*Wbox*16 % 128 == 0
   while ((NR * Wbox) % 8 != 0) ++NR;
   if (NR > 256) { S.plan = fallback(WF_REASON_NOT_PROFITABLE, f); *out = S; return WF_OK; }
-  if (S.prod == 3) {  // direct gather (producer 4): 16-bit data, <= 128 row blocks, <= 64 raw rows per stage
-    int64_t rows = 0;
+  if (S.prod == 3) {
+    int64_t rows = 0;  // raw rows per stage unit (the row table holds <= 64)
     for (int b = 0; b < sh; ++b)
       if (S.has_res[b]) rows += S.amax[b] - S.amin[b] + tps * OHt;
-    const char* env = std::getenv("WF_GATHER");
-    const bool want = g_gather_req >= 0 ? g_gather_req == 1 : (env && env[0] == '1');
-    if (in_dtype != WF_TF32 && S.esize == 2 && Q * Wbox + 2 <= 128 && rows <= 64 && want) S.prod = 4;
+    int want = g_prod_req;
+    if (want < 0) {
+      const char* eg = std::getenv("WF_GATHER");
+      want = (eg && eg[0] == '1') ? 4 : 3;
+    }
+    // 4: 16-bit data, <= 128 row blocks, single-CTA plans
+    if (want == 4 && in_dtype != WF_TF32 && S.esize == 2 && Q * Wbox + 2 <= 128 && rows <= 64 && pair_req != 1)
+      S.prod = 4;
   }
 
   // ---- MMA groups ---------------------------------------------------------
@@ -1119,7 +1125,8 @@ wf_status schedule_from_plan(const wf_conv_desc& d, const wf_fold_plan& p,
     *err = "plan is not an Apply plan";
     return WF_INVALID_ARGUMENT;
   }
-  GatherScope gather_scope(p.producer == 4 ? 1 : 0);  // the plan's own producer, whatever WF_GATHER says now
+  // the plan's own producer for unaligned rows, whatever WF_REPITCH / WF_GATHER say now
+  ProdScope prod_scope(p.producer >= 3 ? p.producer : -1);
   wf_status st = (p.variant == WF_VARIANT_UNFOLDED)
                      ? make_schedule_unfolded(d, static_cast<wf_dtype>(p.in_dtype), out, err)
                      : make_schedule(d, p.f, p.group_size, static_cast<wf_dtype>(p.in_dtype), out, err,
