@@ -177,8 +177,10 @@ def run_reference(args) -> None:
 class ClockSampler:
     """nvidia-smi clocks, throttle reasons and board power sampled during the timed region."""
 
+    # power.draw is a ~1 s moving average on current drivers (it smears the idle time
+    # before a sub-second timed region into the figure); power.draw.instant is not.
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu_id: str):
@@ -186,8 +188,16 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        self.power_field = "power.draw"
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
+            probe = subprocess.run(["nvidia-smi", "-i", self.gpu_id, "--query-gpu=power.draw.instant",
+                                    "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+            if probe.returncode == 0 and probe.stdout.strip()[:1].isdigit():
+                self.power_field = "power.draw.instant"
+        except Exception:
+            pass
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}{self.power_field}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
@@ -222,7 +232,8 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
                 "reasons": sorted(reasons), "samples": len(sm),
-                "power_w_median": statistics.median(pw) if pw else None}
+                "power_w_median": statistics.median(pw) if pw else None,
+                "power_field": getattr(self, "power_field", None)}
 
 
 def _timed(fn, steps, warmup, stream, barrier):
