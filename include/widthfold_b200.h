@@ -172,7 +172,11 @@ wf_status wf_expand_filter_dense(const float* w, const wf_conv_desc* desc,
 /* y = ReLU?(conv(x, w) + b?) in NHWC. x: (n,h,w,c) in plan->in_dtype,
  * y: (n,oh,ow,cout) in out_dtype (WF_F32, WF_BF16 or WF_F16).
  * epilogue: WF_EPI_* flags; WF_EPI_BIAS needs b_rep from wf_expand_filter_pack.
- * No allocations; asynchronous on `stream` (a cudaStream_t). */
+ * No allocations; asynchronous on `stream` (a cudaStream_t). The kernel is
+ * launched with programmatic stream serialization: its prologue (barrier
+ * init, TMEM allocation) may overlap the previous kernel on the stream, and
+ * every global access waits on griddepcontrol.wait, so stream order holds
+ * (environment WF_PDL=0 at first use of a plan/buffer set turns it off). */
 wf_status wf_conv_fold_fwd(const void* x, const void* w_packed,
                            const float* b_rep, void* y,
                            const wf_conv_desc* desc, const wf_fold_plan* plan,

@@ -54,6 +54,11 @@ def _stream(dev: torch.device) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
+# the current stream's raw cudaStream_t without building a torch.cuda.Stream
+# object (the per-call path of FoldedConv2d; several us cheaper)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _as_tensor(a, dtype=None) -> tuple[torch.Tensor, bool]:
     """(device tensor, came_from_numpy)."""
     if isinstance(a, torch.Tensor):
@@ -119,6 +124,14 @@ class FoldedConv2d:
                           if self.core.workspace_bytes else None)
         self._geom = (sh, sw, ph, pw)
         self.output_shape = tuple(self.core.output_shape)
+        self._out_default = torch.float32 if self.dtype == torch.float32 else self.dtype
+        self._set_ptrs()
+
+    def _set_ptrs(self) -> None:
+        """Device pointers the per-call path passes (re-taken whenever a buffer is replaced)."""
+        self._packed_ptr = self.packed.data_ptr()
+        self._brep_ptr = _ptr(self.b_rep)
+        self._ws_ptr = _ptr(self.workspace)
 
     @property
     def plan(self) -> dict:
@@ -131,37 +144,45 @@ class FoldedConv2d:
     def __call__(self, x: torch.Tensor, *, relu: bool = False, bias: bool = True, out: torch.Tensor | None = None,
                  out_dtype: torch.dtype | None = None) -> torch.Tensor:
         """y = ReLU?(conv(x, w) + b) into ``out`` (allocated when None), stream-ordered."""
-        return self._forward(x, relu=relu, bias=bias, out=out, out_dtype=out_dtype, flags=0)
+        return self._forward(x, relu, bias, out, out_dtype, 0)
 
-    def _forward(self, x: torch.Tensor, *, relu: bool = False, bias: bool = True, out: torch.Tensor | None = None,
+    def _forward(self, x: torch.Tensor, relu: bool = False, bias: bool = True, out: torch.Tensor | None = None,
                  out_dtype: torch.dtype | None = None, flags: int = 0) -> torch.Tensor:
         """__call__ with extra wf_conv_fold_fwd epilogue bits: tests and tools
         only (``_abi.WF_EPI_ROW_PRODUCER`` cross-check; the 0xFFFF00 profiling
-        switches need a ``make PROFILE=1`` build and are rejected otherwise)."""
+        switches need a ``make PROFILE=1`` build and are rejected otherwise).
+
+        The per-call path is kept lean (batch-1 latency is host-bound): cheap
+        checks, the raw current stream, and pointers precomputed at plan time;
+        the C++ side reuses the launch prepared for these buffers."""
         if not (isinstance(x, torch.Tensor) and x.is_cuda):
             raise ValueError("FoldedConv2d takes a CUDA tensor (use conv2d() for numpy inputs)")
         if x.dtype != self.dtype:
             raise ValueError(f"x dtype {x.dtype} != planned {self.dtype}")
-        if tuple(x.shape) != self.input_shape:
+        if x.shape != self.input_shape:
             raise ShapeMismatchError(f"x shape {tuple(x.shape)} != planned {self.input_shape}")
-        x = x.contiguous()
-        out_dtype = out_dtype or (torch.float32 if self.dtype == torch.float32 else self.dtype)
+        if not x.is_contiguous():
+            x = x.contiguous()
+        if out_dtype is None:
+            out_dtype = self._out_default
         if out is None:
             out = torch.empty(self.output_shape, dtype=out_dtype, device=x.device)
-        elif tuple(out.shape) != self.output_shape or out.dtype != out_dtype or not out.is_contiguous():
+        elif out.shape != self.output_shape or out.dtype != out_dtype or not out.is_contiguous():
             raise ShapeMismatchError("output buffer has the wrong shape/dtype/layout")
-        use_bias = bias and self.b_rep is not None
-        self.core.forward(x.data_ptr(), self.packed.data_ptr(), _ptr(self.b_rep) if use_bias else 0,
-                          out.data_ptr(), _OUT_NAME[out_dtype], use_bias, relu, _stream(x.device), int(flags),
-                          _ptr(self.workspace))
+        use_bias = bias and self._brep_ptr != 0
+        dev = x.get_device()
+        stream = _raw_stream(dev) if _raw_stream is not None else _stream(x.device)
+        self.core.forward(x.data_ptr(), self._packed_ptr, self._brep_ptr if use_bias else 0, out.data_ptr(),
+                          _OUT_NAME[out_dtype], use_bias, relu, stream, flags, self._ws_ptr)
         return out
 
 
     def graphed(self, x: torch.Tensor, out: torch.Tensor | None = None, *, relu: bool = False, bias: bool = True):
         """Capture one forward on the static buffers ``x`` / ``out`` into a CUDA
         graph; returns ``(replay, out)``. ``replay()`` re-runs the conv on
-        whatever ``x`` holds, without host launch overhead (batch-1 latency:
-        ~15 us replayed vs ~21 us eager per launch, tools/latency_b1.py)."""
+        whatever ``x`` holds, without host launch overhead (R50 b1 TF32: ~5.3 us
+        per replayed launch vs ~5.8 us eager back to back and ~5 us of host
+        time per eager call, tools/host_path_probe.py)."""
         if out is None:
             out_dtype = torch.float32 if self.dtype == torch.float32 else self.dtype
             out = torch.empty(self.output_shape, dtype=out_dtype, device=x.device)
@@ -204,6 +225,7 @@ class FoldedConv2d:
                            if other.core.workspace_bytes else None)
         other.input_shape = shape
         other.output_shape = tuple(other.core.output_shape)
+        other._set_ptrs()
         return other
 
     def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor, *, chunk: int = 512, relu: bool = False,

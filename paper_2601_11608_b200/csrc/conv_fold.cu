@@ -70,6 +70,7 @@ struct PreparedLaunch {
   TmaMaps maps;
   const void* fn = nullptr;
   int grid = 0, block = 0, smem = 0, cluster = 1;
+  bool pdl = true;  // programmatic dependent launch (WF_PDL=0 turns it off; read at prepare time)
   // producer 3: re-pitch x into the workspace first
   bool repitch = false;
   long long rp_rows = 0;
@@ -410,6 +411,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     return WF_UNSUPPORTED;
   }
   L.grid = grid;
+  if (const char* e = std::getenv("WF_PDL")) L.pdl = e[0] != '0';
   L.block = (prod == 4) ? 320 + 32 * kGatherWarps4 : ((prod == 1 || prod == 2) ? 320 + 32 * kGatherWarps : 320);
   L.smem = smem;
   cudaError_t e = ensure_smem(L.fn, L.device, smem);
@@ -426,15 +428,22 @@ cudaError_t launch_prepared(const PreparedLaunch& L, cudaStream_t st) {
   cfg.blockDim = dim3(L.block);
   cfg.dynamicSmemBytes = static_cast<size_t>(L.smem);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
   if (L.cluster > 1) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = L.cluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = L.cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
   }
+  if (L.pdl) {  // the kernel's prologue overlaps the previous grid (griddepcontrol.wait guards every access)
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = n ? attr : nullptr;
+  cfg.numAttrs = n;
   void* args[2] = {const_cast<ConvArgs*>(&L.a), const_cast<TmaMaps*>(&L.maps)};
   return cudaLaunchKernelExC(&cfg, L.fn, args);
 }

@@ -671,11 +671,6 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
       reinterpret_cast<uint32_t*>(gbase + 768)[r] = static_cast<uint32_t>(static_cast<uint8_t>(a.row_b[r])) |
                                                     (static_cast<uint32_t>(static_cast<uint8_t>(a.row_i[r])) << 8) |
                                                     (static_cast<uint32_t>(static_cast<uint8_t>(a.row_a[r])) << 16);
-  {  // bias slice of this N-tile into shared memory
-    float* sbias = reinterpret_cast<float*>(gbase + a.off_bias);
-    const bool has_bias = (a.bias != nullptr) && (a.epi_flags & WF_EPI_BIAS);
-    for (int i = threadIdx.x; i < ncols; i += blockDim.x) sbias[i] = has_bias ? a.bias[col0 + i] : 0.0f;
-  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
       // TMA: one expect_tx; rows: one arrive per transposer / gather warp
@@ -712,6 +707,12 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above (launch, barrier init, TMEM
+  // allocation, tensor-map prefetch) overlaps the previous grid's tail; every
+  // global read (x, packed filter, bias, workspace) and every store of y comes
+  // after the wait. The next grid may start its own prologue from here on.
+  griddep_launch_dependents();
+  griddep_wait();
 
   if (kProd == 4 && warp >= 10) {
     // ===================== direct gather producer (warps 10..17) =====================
@@ -1132,7 +1133,12 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
     const bool dbg_skip_store = prof(a, 0x400);
     const bool skip_ld = prof(a, 0x800);
     const bool stream_st = prof(a, 0x100000);  // experiment: streaming store hints
-    const float* sbias = reinterpret_cast<const float*>(gbase + a.off_bias);
+    float* const sbias = reinterpret_cast<float*>(gbase + a.off_bias);
+    {  // bias slice of this N-tile into shared memory (off the producer's critical path)
+      const bool has_bias = (a.bias != nullptr) && (a.epi_flags & WF_EPI_BIAS);
+      for (int i = threadIdx.x - 64; i < ncols; i += 256) sbias[i] = has_bias ? a.bias[col0 + i] : 0.0f;
+      named_bar_sync(1, 256);  // the 8 epilogue warps
+    }
     // chunk cc of this warp is accumulator chunk c_first + c_step * cc; its output
     // column comes from the slot order (chunk_col), read per iteration
     // the four M rows this thread stores: (16-lane half h16, row group r8).
