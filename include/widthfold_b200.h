@@ -121,7 +121,11 @@ typedef struct {
   int32_t variant;         /* wf_variant */
   int32_t producer;        /* A-tile producer: 0 TMA boxes on x, 1 row gather
                               (folded layout), 2 row gather (explicit im2col),
-                              3 re-pitch x into the workspace, then TMA boxes */
+                              3 re-pitch x into the workspace, then TMA boxes,
+                              4 rows staged in shared memory + gather warps,
+                              5 gather warps re-pitch each stage unit into a
+                              ring in the workspace (L2-resident), then TMA
+                              boxes -- rows whose pitch TMA cannot address */
   int32_t cta_pair;        /* 2: the conv runs on CTA pairs (cta_group::2, M = 256
                               per MMA), each SM holding half of every B block */
   int32_t stage_tiles;     /* M tiles fed by one A stage: 2 when two consecutive
@@ -133,7 +137,7 @@ typedef struct {
                               accumulator buffers only, bits 1-2 epilogue
                               ping-pong (0 auto, 1 off, 2 on), bit 3 no
                               multicast N-tile cluster */
-  int64_t pitched_w;       /* producer 3: workspace row width (>= W, % f == 0) */
+  int64_t pitched_w;       /* producers 3, 5: re-pitched row width (>= W, % f == 0) */
   int64_t workspace_bytes; /* device scratch wf_conv_fold_fwd_ws needs (0: none) */
   uint64_t useful_macs;    /* count_macs of the original conv */
   uint64_t issued_macs;    /* MACs the tensor cores execute (128-row tiles) */
@@ -183,8 +187,10 @@ wf_status wf_conv_fold_fwd(const void* x, const void* w_packed,
                            wf_dtype out_dtype, uint32_t epilogue, void* stream);
 
 /* Same, with the caller-owned device workspace plan->workspace_bytes long
- * (producer 3: rows whose pitch is not a 16-byte multiple, e.g. AlexNet's
- * 227-pixel rows, are re-pitched there first). wf_conv_fold_fwd is this call
+ * (rows whose pitch is not a 16-byte multiple, e.g. AlexNet's 227-pixel rows:
+ * producer 5 re-pitches each stage unit into a ring of slots there inside the
+ * kernel -- a few tens of MB, batch-independent; producer 3 re-pitches the
+ * whole batch there first). wf_conv_fold_fwd is this call
  * with workspace == NULL and fails with WF_INVALID_ARGUMENT for such plans. */
 wf_status wf_conv_fold_fwd_ws(const void* x, void* workspace, const void* w_packed, const float* b_rep, void* y,
                               const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype,

@@ -234,12 +234,13 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   // producer instead -- same shared-memory image, so results are bit-identical
   const bool tf32 = (in_t == WF_TF32);
   const int prod =
-      ((S.prod == 0 || S.prod == 3 || S.prod == 4) && (epilogue & WF_EPI_ROW_PRODUCER) && !tf32) ? 1 : S.prod;
+      ((S.prod == 0 || S.prod == 3 || S.prod == 4 || S.prod == 5) && (epilogue & WF_EPI_ROW_PRODUCER) && !tf32) ? 1
+                                                                                                              : S.prod;
   a.prod = prod;
   a.off_raw = a.off_bias + kMaxAccCols * 4;
   // raw staging: the planner's slots for its own producer; the row-ring
   // cross-check (prod 1 forced on a TMA / gather plan) sizes its ring here
-  a.raw_slots = (prod == S.prod) ? ((prod == 1 || prod == 2 || prod == 4) ? S.raw_slots : 0) : kRawSlots;
+  a.raw_slots = (prod == S.prod) ? ((prod == 1 || prod == 2 || prod == 4 || prod == 5) ? S.raw_slots : 0) : kRawSlots;
   a.raw_slot_bytes = (prod == S.prod) ? S.raw_slot_bytes : raw_slot_bytes_for(d.w * d.c * S.esize);
   if (prod == 1 && S.prod != 1) {  // forced: make room for the ring by dropping A stages
     while (a.stages > 2 && a.off_raw + a.raw_slots * a.raw_slot_bytes + 1024 > kSmemLimit) {
@@ -318,6 +319,19 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     L.rp_out = static_cast<int>(S.Wp * d.c * es);
     xt = workspace;
   }
+  // ---- producer 5: the gather warps re-pitch stage units into a ring of slots in the workspace
+  if (prod == 5) {
+    if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15u)) {
+      *err = "this plan needs a 16-byte aligned workspace of plan->workspace_bytes";
+      return WF_INVALID_ARGUMENT;
+    }
+    a.ring = static_cast<uint8_t*>(const_cast<void*>(workspace));
+    a.ring_rows = S.ring_rows;
+    a.ring_rowpitch = static_cast<int>(S.Wp * d.c * es);
+    a.amin_min = S.amin_min;
+    a.ring_slot_bytes = S.ring_slot_bytes;
+    xt = workspace;
+  }
   // ---- A descriptor high word and the SWIZZLE_32B layout parameters -------------
   a.sw32 = S.sw32 ? 1 : 0;
   a.a_desc_hi = S.sw32 ? ((6u << 29) | (1u << 14) | (256u >> 4))   // SWIZZLE_32B, version 1, SBO 256 B
@@ -333,11 +347,12 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     return WF_UNSUPPORTED;
   }
   // ---- input tensor maps (one 5-D view per H-stride residue) --------------------
-  const cuuint64_t rowpitch = static_cast<cuuint64_t>(prod == 3 ? S.Wp : d.w) * d.c * es;
+  const cuuint64_t rowpitch = static_cast<cuuint64_t>((prod == 3 || prod == 5) ? S.Wp : d.w) * d.c * es;
   const cuuint64_t pix = static_cast<cuuint64_t>(p.f) * d.c * es;
-  for (int b = 0; b < S.s && (prod == 0 || prod == 3); ++b) {
+  for (int b = 0; b < S.s && (prod == 0 || prod == 3 || prod == 5); ++b) {
     if (!S.has_res[b]) continue;
-    const cuuint64_t rows_b = static_cast<cuuint64_t>((d.h - b + S.s - 1) / S.s);
+    // producer 5: the "image" dimension indexes ring slots of ring_rows rows each
+    const cuuint64_t rows_b = static_cast<cuuint64_t>(((prod == 5 ? S.ring_rows : d.h) - b + S.s - 1) / S.s);
     if (S.sw32) {  // {pixel elements, folded col, input row of residue b, image}; 32-byte boxes
       cuuint64_t gdim4[4] = {static_cast<cuuint64_t>(p.f * d.c), static_cast<cuuint64_t>(p.wf), rows_b,
                              static_cast<cuuint64_t>(d.n)};
@@ -356,8 +371,10 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
       continue;
     }
     cuuint64_t gdim[5] = {static_cast<cuuint64_t>(16 / es), static_cast<cuuint64_t>(p.wf), rows_b,
-                          static_cast<cuuint64_t>(Q), static_cast<cuuint64_t>(d.n)};
-    cuuint64_t gstr[4] = {pix, rowpitch * S.s, 16, rowpitch * d.h};
+                          static_cast<cuuint64_t>(Q),
+                          static_cast<cuuint64_t>(prod == 5 ? static_cast<int64_t>(kRingCtas) * S.raw_slots : d.n)};
+    cuuint64_t gstr[4] = {pix, rowpitch * S.s, 16,
+                          prod == 5 ? static_cast<cuuint64_t>(S.ring_slot_bytes) : rowpitch * d.h};
     cuuint32_t box[5] = {static_cast<cuuint32_t>(16 / es), static_cast<cuuint32_t>(p.wbox),
                          static_cast<cuuint32_t>(p.nrows), static_cast<cuuint32_t>(Q), 1};
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
@@ -381,18 +398,22 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     *err = "the row producers run single-CTA plans";
     return WF_UNSUPPORTED;
   }
-  if (tf32 && (S.CH != 32 || prod == 1 || prod == 2 || prod == 4)) {
+  if (prod == 5 && grid > kRingCtas) {
+    *err = "more CTAs than the ring workspace was sized for";
+    return WF_UNSUPPORTED;
+  }
+  if (tf32 && (S.CH != 32 || prod == 1 || prod == 2 || prod == 4 || prod == 5)) {
     *err = "tf32 plans use 32-column epilogue chunks and the TMA producer";
     return WF_UNSUPPORTED;
   }
   const int kind = tf32 ? 1 : 0;
   // two N-tiles as a 2-CTA cluster sharing each A stage by multicast
   // (AlexNet 1.08-1.15x, VGG neutral; launch_opts bit 3 turns it off)
-  const bool mc = !(p.launch_opts & 8) && (prod == 0 || prod == 3) && S.pair == 1 && !tf32 && a.n_tiles == 2 &&
-                  a.ksplit == 1 && grid % 2 == 0;
+  const bool mc = !(p.launch_opts & 8) && (prod == 0 || prod == 3 || prod == 5) && S.pair == 1 && !tf32 &&
+                  a.n_tiles == 2 && a.ksplit == 1 && grid % 2 == 0;
   L.cluster = 1;
   if (mc) {
-    L.fn = conv_kernel_fn_mc(out_dtype, S.CH);
+    L.fn = (prod == 5) ? conv_kernel_fn_mc5(out_dtype) : conv_kernel_fn_mc(out_dtype, S.CH);
     L.cluster = 2;
   } else if ((prod == 0 || prod == 3) && S.pair == 2) {
     L.fn = conv_kernel_fn_pair(out_dtype, S.CH);
@@ -403,6 +424,8 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     L.fn = conv_kernel_fn<1>(kind, out_dtype, S.CH);
   } else if (prod == 4) {
     L.fn = conv_kernel_fn<4>(kind, out_dtype, S.CH);
+  } else if (prod == 5) {
+    L.fn = conv_kernel_fn<5>(kind, out_dtype, S.CH);
   } else {
     L.fn = conv_kernel_fn<2>(kind, out_dtype, S.CH);
   }
@@ -412,7 +435,8 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   }
   L.grid = grid;
   if (const char* e = std::getenv("WF_PDL")) L.pdl = e[0] != '0';
-  L.block = (prod == 4) ? 320 + 32 * kGatherWarps4 : ((prod == 1 || prod == 2) ? 320 + 32 * kGatherWarps : 320);
+  L.block = (prod == 4) ? 320 + 32 * kGatherWarps4
+                        : (prod == 5 ? 320 + 32 * kGatherWarps5 : ((prod == 1 || prod == 2) ? 320 + 32 * kGatherWarps : 320));
   L.smem = smem;
   cudaError_t e = ensure_smem(L.fn, L.device, smem);
   if (e != cudaSuccess) {

@@ -46,6 +46,9 @@ constexpr int kGatherWarps = 4;  // row-staged producer: transposer warps 10..13
 // direct gather producer (kProd 4): warps 10..17 (row loads are latency-bound:
 // more warps beat the 128-register cap of 16 warps)
 constexpr int kGatherWarps4 = 8;
+// L2-ring producer (kProd 5): warps 10..17 re-pitch each stage unit's input rows
+// into a ring slot in global memory; warp 0 then loads the A stage from it by TMA
+constexpr int kGatherWarps5 = 8;
 constexpr int kMaxKsplit = 8;    // A stages per M tile (im2col kh ranges)
 constexpr int kMaxStageRows = 64;  // folded raw rows per A stage (row producer)
 
@@ -85,6 +88,11 @@ struct ConvArgs {
   int lbo_a;                      // bytes between core-column regions
   int prod;                       // A producer (plan.hpp Schedule::prod)
   int off_raw, raw_slots, raw_slot_bytes;  // staged-row ring (kProd 1/2) / the two raw unit slots (kProd 4)
+                                           // / the L2 ring's slots per CTA (kProd 5, no shared memory)
+  uint8_t* ring;                  // kProd 5: this launch's ring (workspace), ring_slots slots per CTA
+  int ring_rows, ring_rowpitch;   // kProd 5: input rows per slot, re-pitched row bytes (16-byte multiple)
+  int amin_min;                   // kProd 5: slot row 0 = input row (oh0 + amin_min) * s
+  long long ring_slot_bytes;
   int rows_per_stage;             // folded: raw rows per A stage
   int log_wbox;                   // log2(Wbox)
   signed char row_b[kMaxStageRows], row_i[kMaxStageRows], row_a[kMaxStageRows];  // folded stage rows
@@ -636,7 +644,7 @@ __device__ __forceinline__ void arrive_at(uint32_t bar) {
 // unit issues half of the pieces; a stage is refilled only after both CTAs'
 // MMAs released it (multicast commits, empty barriers of count 2).
 template <int kKind, typename OutT, int CH, int kProd, int kPair = 1, int kMc = 0>
-__global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kGatherWarps4 : kGatherWarps), 1)
+__global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kGatherWarps4 : (kProd == 5 ? kGatherWarps5 : kGatherWarps)), 1)
     conv_fold_kernel(const __grid_constant__ ConvArgs a, const __grid_constant__ TmaMaps maps) {
   using namespace ptx;
   extern __shared__ uint8_t smem_raw[];
@@ -674,7 +682,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
       // TMA: one expect_tx; rows: one arrive per transposer / gather warp
-      mbar_init(bar_full + 8 * i, kProd == 0 ? 1 : (kProd == 4 ? kGatherWarps4 : kGatherWarps));
+      mbar_init(bar_full + 8 * i, (kProd == 0 || kProd == 5) ? 1 : (kProd == 4 ? kGatherWarps4 : kGatherWarps));
       mbar_init(bar_empty + 8 * i, (kMc && !prof(a, 0x2000)) ? 2 : 1);  // multicast: both CTAs' MMAs release the stage
     }
     for (int i = 0; i < a.n_acc; ++i) {
@@ -686,12 +694,14 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
     mbar_init(bar_b, 1);
     mbar_init(bar_bpeer, 1);
     for (int i = 0; i < a.raw_slots; ++i) {
-      mbar_init(bar_raw_full + 8 * i, 1);
-      mbar_init(bar_raw_empty + 8 * i, kProd == 4 ? kGatherWarps4 : 1);  // staged gather: every gather warp releases
+      // ring (kProd 5): every gather warp fills the slot, the MMA issuer frees it
+      // (multicast cluster: both CTAs' gather warps fill the shared slot, both MMA issuers free it)
+      mbar_init(bar_raw_full + 8 * i, (kProd == 5 && kMc) ? 2 : 1);
+      mbar_init(bar_raw_empty + 8 * i, kProd == 4 ? kGatherWarps4 : ((kProd == 5 && kMc) ? 2 : 1));
     }
     fence_barrier_init();
   }
-  if (kProd == 0 && warp == 0 && lane == 0) {
+  if ((kProd == 0 || kProd == 5) && warp == 0 && lane == 0) {
     for (int b = 0; b < a.s; ++b)
       if ((a.res_mask >> b) & 1u) {
         prefetch_tmap(&maps.in[b]);
@@ -714,7 +724,133 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
   griddep_launch_dependents();
   griddep_wait();
 
-  if (kProd == 4 && warp >= 10) {
+  if (kProd == 5 && warp >= 10) {
+    // ===================== L2-ring gather warps (warps 10..17) =====================
+    // Stage unit it of this CTA: the ring_rows input rows from (oh0 + amin_min)*s
+    // are read with coalesced 16-byte loads of their aligned blocks, realigned
+    // (neighbour block by shuffle, funnel shift by the row's misalignment) and
+    // stored as re-pitched rows (16-byte pitch, zero tail) into ring slot it % R
+    // of this CTA. The slot is handed to the TMA producer through an mbarrier
+    // after a generic -> async proxy fence; the MMA issuer frees it once the
+    // stage built from it has landed. Slots are rewritten every R units, so
+    // the ring stays in L2: x is read from HBM once, nothing extra is written.
+    // In the multicast N-tile cluster the two CTAs share one ring (per
+    // cluster): each re-pitches every other row of the slot and signals both.
+    const int gw = warp - 10;
+    constexpr int kStep = kMc ? 2 : 1;  // CTAs sharing the slot
+    constexpr int P = kGatherWarps5;
+    const uint8_t* const x = reinterpret_cast<const uint8_t*>(opq64(reinterpret_cast<long long>(a.x)));
+    const long long img_b = opq64(a.in_img_bytes);
+    const int rb = opq(static_cast<int>(a.in_row_bytes)), rp = opq(a.ring_rowpitch);
+    const int nblk = rp >> 4;  // 16-byte blocks of a re-pitched row
+    const int SR = opq(a.ring_rows), R = opq(a.raw_slots), H = opq(a.H), nimg = opq(a.n_img), s = opq(a.s);
+    const int amin0 = opq(a.amin_min);
+    const long long slot_b = opq64(a.ring_slot_bytes);
+    uint8_t* const ring = a.ring + static_cast<long long>(blockIdx.x / kStep) * R * slot_b;
+    // L2 prefetch of the input span of the unit two ahead (one bulk prefetch:
+    // a unit's rows are contiguous in x), so the row loads hit L2
+    const RowProd rpf = row_prod(a, 0u);
+    auto prefetch_unit = [&](int u) {
+      int n, oh0;
+      long long s0, s1;
+      unit_span(a, rpf, u, n, oh0, s0, s1);
+      if (s1 > s0) prefetch_l2_bulk(x + s0, static_cast<uint32_t>(s1 - s0));
+    };
+    const bool pf = gw == 0 && lane == 0;
+    // profiling (PROFILE builds): 0x8000 the gather warps skip their row loads (zeros), 0x10000 the proxy fence
+    const bool no_ld = prof(a, 0x8000), no_fence = prof(a, 0x10000);
+    if (pf)
+      for (int u = local; u < a.num_units && u < local + 2 * a.unit_stride; u += a.unit_stride) prefetch_unit(u);
+    int slot = 0;
+    uint32_t round = 0;
+    // profiling (0x80000, CTA 0, gather warp 0): cycles waiting for a free slot, loading + storing, fencing
+    const bool dbg = prof(a, 0x80000) && blockIdx.x == 0 && gw == 0 && lane == 0;
+    long long t_empty = 0, t_rows = 0, t_fence = 0, t_arrive = 0, t_ld = 0, t0 = 0, t_all = dbg ? clock64() : 0;
+    for (int u = local; u < a.num_units; u += a.unit_stride) {
+      if (pf && u + 2 * a.unit_stride < a.num_units) prefetch_unit(u + 2 * a.unit_stride);
+      if (dbg) t0 = clock64();
+      if constexpr (kMc) mbar_wait_cluster(bar_raw_empty + 8 * slot, (round & 1u) ^ 1u);
+      else mbar_wait(bar_raw_empty + 8 * slot, (round & 1u) ^ 1u);
+      if (dbg) { const long long t1 = clock64(); t_empty += t1 - t0; t0 = t1; }
+      int n, oh0;
+      tile_origin<1>(a, u, 0, 0u, n, oh0);
+      const int row0 = (oh0 + amin0) * s;
+      uint8_t* const dslot = ring + slot * slot_b;
+      for (int j0 = static_cast<int>(mrank) + kStep * gw; j0 < SR; j0 += 3 * kStep * P) {  // three rows in flight per warp
+        uint4 v[3][4];
+        int mis[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int j = j0 + q * kStep * P, ih = row0 + j;
+          const bool ok = j < SR && ih >= 0 && ih < H && n < nimg && !no_ld;
+          const long long rs = static_cast<long long>(n) * img_b + static_cast<long long>(ih) * rb;
+          mis[q] = ok ? static_cast<int>(rs & 15) : 0;
+          const uint8_t* blk = x + (rs - mis[q]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int kb = lane + 32 * i;  // aligned block kb of the row (blocks holding row bytes only)
+            v[q][i] = (ok && kb <= nblk && 16 * kb - mis[q] < rb) ? ld_global_nc_v4(blk + 16 * kb)
+                                                                  : make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+#if WFB_PROFILE
+        if (dbg) {  // wait for this batch's loads (a volatile move of the last block), then read the clock
+          const long long tl0 = clock64();
+          uint32_t dep;
+          asm volatile("mov.b32 %0, %1;" : "=r"(dep) : "r"(v[2][2].x ^ v[0][0].y));
+          t_ld += clock64() - tl0 + (dep & 0);
+        }
+#endif
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int j = j0 + q * kStep * P;
+          if (j >= SR) break;
+          uint4 t[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            t[i] = make_uint4(shfl_next(v[q][i].x, lane), shfl_next(v[q][i].y, lane), shfl_next(v[q][i].z, lane),
+                              shfl_next(v[q][i].w, lane));
+          const uint32_t sh = static_cast<uint32_t>(mis[q] & 3) * 8;
+          uint8_t* const drow = dslot + static_cast<long long>(j) * rp;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int ob = lane + 32 * i;  // output block: bytes [16 ob, 16 ob + 16) of the re-pitched row
+            if (ob >= nblk) continue;
+            const uint4 nx = (lane == 31) ? (i < 3 ? t[i + 1] : make_uint4(0u, 0u, 0u, 0u)) : t[i];
+            uint4 c;
+            switch (mis[q] >> 2) {  // warp-uniform
+              case 0: c = realign<0>(v[q][i], nx, sh); break;
+              case 1: c = realign<1>(v[q][i], nx, sh); break;
+              case 2: c = realign<2>(v[q][i], nx, sh); break;
+              default: c = realign<3>(v[q][i], nx, sh); break;
+            }
+            if (16 * ob + 16 > rb) c = edge_mask(c, 0, rb - 16 * ob);  // zero tail past W*C
+            st_global_v4(drow + 16 * ob, c);
+          }
+        }
+      }
+      if (dbg) { const long long t1 = clock64(); t_rows += t1 - t0; t0 = t1; }
+      if (!no_fence) fence_proxy_async_global();  // generic-proxy stores -> visible to the TMA reads of the slot
+      named_bar_sync(2, 32 * P);  // every gather warp's rows of the slot are written and fenced
+      if (dbg) t_fence += clock64() - t0;
+      if (gw == 0 && lane == 0) {  // one arrival per CTA (one release instead of one per warp)
+        if constexpr (kMc) {  // both CTAs' producers load from the slot (release at cluster scope)
+          mbar_arrive_cluster(mapa(bar_raw_full + 8 * slot, 0));
+          mbar_arrive_cluster(mapa(bar_raw_full + 8 * slot, 1));
+        } else {
+          mbar_arrive(bar_raw_full + 8 * slot);
+        }
+      }
+      if (dbg) { const long long t1 = clock64(); t_arrive += t1 - t0; }
+      if (++slot == R) { slot = 0; ++round; }
+    }
+#if WFB_PROFILE
+    if (dbg)
+      printf("ring gather warp0 cta0: %lld cycles: wait free slot %lld, rows (load+realign+store) %lld (of which load "
+             "latency %lld), fence+bar %lld, arrive %lld\n",
+             clock64() - t_all, t_empty, t_rows, t_ld, t_fence, t_arrive);
+#endif
+  } else if (kProd == 4 && warp >= 10) {
     // ===================== direct gather producer (warps 10..17) =====================
     const RowProd rp = row_prod(a, base + 768);
     const int gw = warp - 10;
@@ -909,11 +1045,27 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
       }
       const uint32_t tx = static_cast<uint32_t>((a.box_bytes + a.shift_box_bytes) * __popc(a.res_mask));
       int it = 0;
+      int rslot = 0;  // kProd 5: ring slot of this unit
+      uint32_t rround = 0;
+      const bool pdbg = prof(a, 0x80000) && blockIdx.x == 0;
+      long long p_ring = 0, p_stage = 0, p0 = 0, p_all = pdbg ? clock64() : 0;
       // profiling (0x800000, with 0x600000): the producer sits the launch out too
       for (int u = prof(a, 0x800000) ? a.num_units : local; u < a.num_units; u += a.unit_stride, ++it) {
         const int stage = it % a.stages;
         const uint32_t round = static_cast<uint32_t>(it / a.stages);
+        int slot_idx = 0;  // kProd 5: the slot's index in the ring tensor maps
+        if constexpr (kProd == 5) {
+          // the gather warps (of both CTAs in the multicast cluster) re-pitched the unit's rows
+          if (pdbg) p0 = clock64();
+          if constexpr (kMc) mbar_wait_cluster(bar_raw_full + 8 * rslot, rround & 1u);
+          else mbar_wait(bar_raw_full + 8 * rslot, rround & 1u);
+          if (pdbg) p_ring += clock64() - p0;
+          slot_idx = static_cast<int>(blockIdx.x) / (kMc ? 2 : 1) * a.raw_slots + rslot;
+          if (++rslot == a.raw_slots) { rslot = 0; ++rround; }
+        }
+        if (pdbg) p0 = clock64();
         mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
+        if (pdbg) p_stage += clock64() - p0;
         // pair: both CTAs' boxes complete on the leader's full barrier
         const uint32_t fbar = (kPair == 2) ? mapa(bar_full + 8 * stage, 0) : bar_full + 8 * stage;
         int n, oh0;
@@ -957,15 +1109,23 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
           if (kMc && !mc_self && ((j++ & 1) != static_cast<int>(mrank))) continue;  // the peer multicasts this residue
           if constexpr (kMc) {
             const uint16_t mask = mc_self ? static_cast<uint16_t>(1u << mrank) : static_cast<uint16_t>(0x3);
-            tma_load_5d_mc(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, fbar, mask);
+            // kProd 5: the cluster's ring slot (rows from slot row (amin[b] - amin_min)*s + b)
+            const int rrow = (kProd == 5) ? a.amin[b] - a.amin_min : oh0 + a.amin[b];
+            const int img = (kProd == 5) ? slot_idx : n;
+            tma_load_5d_mc(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, rrow, 0, img, fbar, mask);
             if (a.shift_box_bytes && !dbg_noshift)
-              tma_load_5d_mc(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1,
-                             oh0 + a.amin[b], 0, n, fbar, mask);
+              tma_load_5d_mc(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1, rrow, 0, img,
+                             fbar, mask);
           } else if constexpr (kPair == 2) {
             tma_load_5d_pair(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, fbar);
             if (a.shift_box_bytes && !dbg_noshift)
               tma_load_5d_pair(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1,
                                oh0 + a.amin[b], 0, n, fbar);
+          } else if constexpr (kProd == 5) {  // ring slot: residue-b rows from slot row (amin[b] - amin_min)*s + b
+            tma_load_5d(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, a.amin[b] - a.amin_min, 0, slot_idx, fbar);
+            if (a.shift_box_bytes && !dbg_noshift)
+              tma_load_5d(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1,
+                          a.amin[b] - a.amin_min, 0, slot_idx, fbar);
           } else {
             tma_load_5d(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, fbar);
             if (a.shift_box_bytes && !dbg_noshift)
@@ -974,6 +1134,11 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
           }
         }
       }
+#if WFB_PROFILE
+      if (pdbg)
+        printf("tma producer cta0: %d units, %lld cycles: wait ring slot %lld, wait free A stage %lld\n", it,
+               clock64() - p_all, p_ring, p_stage);
+#endif
       if constexpr (kMc) {
         // producer tail: wait for the final release of every stage in use --
         // the peer's last multicast commit lands on this CTA's empty
@@ -1016,6 +1181,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
     if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_all));
 #endif
     int tile = 0;
+    int ring_slot = 0;         // kProd 5: the unit's ring slot, freed once its A stage landed
     int stage_c = 0;           // A stage of the next sub-stage (kept incrementally: no division per tile)
     uint32_t round_c = 0;      // its fill round
     for (int u = local; u < num_units; u += unit_stride) {
@@ -1039,6 +1205,16 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
         const int e0 = (ksplit == 1) ? nt_e0 : a.ks_entry0[ks];
         const int entries = (ksplit == 1) ? nt_en : a.ks_entries[ks];
         if (k == 0 && !no_wait) mbar_wait(bar_full + 8 * stage, round & 1u);
+        if constexpr (kProd == 5) {
+          if (k == 0 && ks == 0 && leader) {
+            if constexpr (kMc) {  // the shared slot is free once both CTAs' stages landed
+              mbar_arrive_cluster(mapa(bar_raw_empty + 8 * ring_slot, 0));
+              mbar_arrive_cluster(mapa(bar_raw_empty + 8 * ring_slot, 1));
+            } else {
+              mbar_arrive(bar_raw_empty + 8 * ring_slot);
+            }
+          }
+        }
         if (dbg) { const long long t1 = clock64(); w_full += t1 - t0; t0 = t1; }
         tc_fence_after();
         const uint32_t a_lo = ((a_base + stage * stage_bytes + k * tile_shift) & 0x3FFFFu) >> 4;
@@ -1088,6 +1264,8 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
      }
      for (int ks = 0; ks < ksplit; ++ks)  // advance past the unit's sub-stages
        if (++stage_c == stages) { stage_c = 0; ++round_c; }
+     if constexpr (kProd == 5)
+       if (++ring_slot == a.raw_slots) ring_slot = 0;
     }
 #if WFB_PROFILE
     if (dbg && leader)
@@ -1296,7 +1474,7 @@ const void* kernel_ptr() {
 // kind: 0 kind::f16, 1 kind::tf32; out: output dtype; ch: epilogue chunk.
 template <int kProd>
 const void* conv_kernel_fn(int kind, wf_dtype out, int ch) {
-  if constexpr (kProd == 4) {  // kind::f16, 32-column chunks (448 threads: CH=64 would spill)
+  if constexpr (kProd == 4 || kProd == 5) {  // kind::f16, 32-column chunks (576 threads: CH=64 would spill)
     if (kind == 1 || ch != 32) return nullptr;
     if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 32, kProd>();
     if (out == WF_F16) return kernel_ptr<0, __half, 32, kProd>();
@@ -1325,10 +1503,13 @@ const void* conv_kernel_fn(int kind, wf_dtype out, int ch) {
 const void* conv_kernel_fn_pair(wf_dtype out, int ch);
 // 2-CTA N-tile cluster with multicast A loads, TMA producer, kind::f16.
 const void* conv_kernel_fn_mc(wf_dtype out, int ch);
+// the same cluster fed by the in-kernel L2 ring (kProd 5), 32-column chunks
+const void* conv_kernel_fn_mc5(wf_dtype out);
 
 extern template const void* conv_kernel_fn<0>(int, wf_dtype, int);
 extern template const void* conv_kernel_fn<1>(int, wf_dtype, int);
 extern template const void* conv_kernel_fn<2>(int, wf_dtype, int);
 extern template const void* conv_kernel_fn<4>(int, wf_dtype, int);
+extern template const void* conv_kernel_fn<5>(int, wf_dtype, int);
 
 }  // namespace wfb

@@ -26,4 +26,10 @@ const void* conv_kernel_fn_mc(wf_dtype out, int ch) {
   return kernel_ptr<0, float, 32, 0, 1, 1>();
 }
 
+const void* conv_kernel_fn_mc5(wf_dtype out) {
+  if (out == WF_BF16) return kernel_ptr<0, __nv_bfloat16, 32, 5, 1, 1>();
+  if (out == WF_F16) return kernel_ptr<0, __half, 32, 5, 1, 1>();
+  return kernel_ptr<0, float, 32, 5, 1, 1>();
+}
+
 }  // namespace wfb

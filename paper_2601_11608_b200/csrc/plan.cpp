@@ -390,11 +390,24 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     int want = g_prod_req;
     if (want < 0) {
       const char* eg = std::getenv("WF_GATHER");
-      want = (eg && eg[0] == '1') ? 4 : 3;
+      const char* er = std::getenv("WF_REPITCH");
+      const char* eq = std::getenv("WF_RING");
+      want = (eg && eg[0] == '1') ? 4 : ((eq && eq[0] == '1') ? 5 : 3);
+      (void)er;
     }
     // 4: 16-bit data, <= 128 row blocks, single-CTA plans
     if (want == 4 && in_dtype != WF_TF32 && S.esize == 2 && Q * Wbox + 2 <= 128 && rows <= 64 && pair_req != 1)
       S.prod = 4;
+    // 5: 16-bit data, a re-pitched row of <= 127 16-byte blocks (4 per gather lane), single-CTA plans
+    if (want == 5 && in_dtype != WF_TF32 && (Wp * d.c * S.esize) / 16 + 1 <= 128 && pair_req != 1) {
+      int amin_min = INT32_MAX, amax_max = INT32_MIN;
+      for (int b = 0; b < sh; ++b)
+        if (S.has_res[b]) { amin_min = std::min(amin_min, S.amin[b]); amax_max = std::max(amax_max, S.amax[b]); }
+      S.prod = 5;
+      S.amin_min = amin_min;
+      S.ring_rows = static_cast<int>((amax_max - amin_min + tps * OHt) * sh);
+      S.ring_slot_bytes = static_cast<int64_t>(S.ring_rows) * Wp * d.c * S.esize;
+    }
   }
 
   // ---- MMA groups ---------------------------------------------------------
@@ -419,6 +432,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // tf32 (fp32 outputs): 32-column chunks (8 fp32 = 32 B).
   S.CH = (in_dtype != WF_TF32 && S.Ng % 64 == 0) ? 64 : 32;
   if (S.prod == 4 && S.CH != 32) S.prod = 3;  // the gather kernel is built for 32-column epilogue chunks
+  if (S.prod == 5) S.CH = 32;  // 576 threads: the 64-column epilogue would spill at the register cap
   std::vector<int64_t> lo(G), hi(G);
   for (int64_t g = 0; g < G; ++g) {
     lo[g] = INT64_MAX;
@@ -595,7 +609,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // tools/probes/sw32_probe.cu). Otherwise the canonical no-swizzle layout of
   // 16-byte core columns ([q][row][folded col][16 B], + the shift region).
   S.sw32 = !S.kpair && !S.need_shift && Q >= 2 && in_dtype != WF_TF32;
-  if (S.sw32 && S.prod == 4) S.prod = 3;  // the gather warps write the no-swizzle layout only
+  if (S.sw32 && (S.prod == 4 || S.prod == 5)) S.prod = 3;  // the gather warps / ring maps: no-swizzle layout only
   if (S.sw32) {
     S.qs.clear();
     for (int64_t g = 0; g < G; ++g)
@@ -929,12 +943,14 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   p.table_bytes = (p.mma_entries * 24 + G * 4 + 127) / 128 * 128;
   p.packed_bytes = p.table_bytes + b_cursor;
   p.epi_chunk = S.CH;
-  S.raw_slots = (S.prod == 4) ? 2 : kRawSlots;
-  S.raw_slot_bytes = (S.prod == 4) ? static_cast<int>(unit_slot) : raw_slot_bytes_for(d.w * d.c * S.esize);
+  S.raw_slots = (S.prod == 4) ? 2 : (S.prod == 5 ? kRingSlots : kRawSlots);
+  S.raw_slot_bytes = (S.prod == 4) ? static_cast<int>(unit_slot)
+                                   : (S.prod == 5 ? 0 : raw_slot_bytes_for(d.w * d.c * S.esize));
   p.variant = WF_VARIANT_FOLD;
   p.producer = S.prod;
-  p.pitched_w = (S.prod == 3) ? S.Wp : 0;
-  p.workspace_bytes = (S.prod == 3) ? d.n * d.h * S.Wp * d.c * S.esize : 0;
+  p.pitched_w = (S.prod == 3 || S.prod == 5) ? S.Wp : 0;
+  p.workspace_bytes = (S.prod == 3) ? d.n * d.h * S.Wp * d.c * S.esize
+                                    : (S.prod == 5 ? static_cast<int64_t>(kRingCtas) * kRingSlots * S.ring_slot_bytes : 0);
   S.ohb = ceil_div(OH, OHt);
   S.num_mtiles = d.n * S.ohb;
   // CTA pairs (cta_group::2, M = 256): each SM holds and reads half of every

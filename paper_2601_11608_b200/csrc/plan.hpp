@@ -49,6 +49,10 @@ constexpr int kMaxNTiles = 16;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kStagingBytes = 0;  // epilogue writes straight from registers (no staging)
 constexpr int kRawSlots = 32;     // staged-row ring slots (row producer; >= the raw rows of a stage)
+// L2 ring of re-pitched stage units (producer 5): slots per CTA and the CTA
+// count the workspace is sized for (grids are <= the SM count: 148 on B200)
+constexpr int kRingSlots = 3;
+constexpr int kRingCtas = 160;
 constexpr int kCtrlBytes = 2048;  // barriers, TMEM slot, row table at the base of shared memory
 inline int raw_slot_bytes_for(int64_t row_bytes) { return static_cast<int>((row_bytes + 32 + 127) / 128 * 128); }
 
@@ -98,7 +102,9 @@ struct Schedule {
   int Ng = 64;                   // accumulator columns per group
   int CH = 64;                   // epilogue chunk (columns per 16x256b TMEM read)
   int prod = 0;                  // A producer: 0 TMA boxes, 1 row gather (folded), 2 row gather
-                                 // (im2col), 3 re-pitch into the workspace + TMA boxes
+                                 // (im2col), 3 re-pitch into the workspace + TMA boxes,
+                                 // 4 rows staged in shared memory + gather warps,
+                                 // 5 gather warps re-pitch each stage unit into an L2 ring + TMA boxes
   int64_t Wp = 0;                // input width the TMA view uses (re-pitched when != W)
   int pair = 1;                  // 2: CTA-pair (cta_group::2) MMAs, B blocks split across the pair
   int tps = 1;                   // M tiles per A stage (2: consecutive tiles share their input rows)
@@ -106,6 +112,9 @@ struct Schedule {
   int U = 0;                     // im2col: 32-byte K-steps per kh
   int ksplit = 1;                // A stages per M tile (im2col: kh ranges)
   int raw_slots = 0, raw_slot_bytes = 0;  // staged-row ring of the row producer (prod 1/2)
+  int ring_rows = 0;             // prod 5: input rows per ring slot (a stage unit's rows, re-pitched)
+  int64_t ring_slot_bytes = 0;   // prod 5: bytes per ring slot (ring_rows x Wp*C*elem)
+  int amin_min = 0;              // min over residues of amin (slot row 0 = input row (oh0 + amin_min) * s)
   std::vector<int> ks_kh0, ks_entry0, ks_entries, ks_chunks;
   int amin[kMaxResidues] = {0};
   int amax[kMaxResidues] = {0};

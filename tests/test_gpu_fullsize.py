@@ -320,18 +320,22 @@ def test_c_abi_pack_and_forward_via_ctypes(oracle):
                                                 (4, 45, 71, 5, 96, 1, 2, torch.float16),
                                                 (2, 33, 50, 3, 96, 2, 1, torch.bfloat16)],
                          ids=["alexnet_b64", "alexnet_b3", "w71_k5", "w50_k3"])
-def test_gather_producer_bitwise_vs_repitch(monkeypatch, n, h, w, k, co, s, p, dt):
-    """WF_GATHER=1 (plan time): unaligned rows staged in shared memory by bulk copies and realigned by the
-    gather warps, no workspace -- bit-identical to the re-pitch + TMA launch, and exact on integer data."""
+@pytest.mark.parametrize("prod", ["ring+tma", "gather"])
+def test_gather_producer_bitwise_vs_repitch(monkeypatch, n, h, w, k, co, s, p, dt, prod):
+    """Unaligned rows without the re-pitch pass -- WF_RING=1 (producer 5): gather warps re-pitch each
+    stage unit into an L2 ring the TMA boxes read; WF_GATHER=1 (producer 4): rows staged in shared
+    memory by bulk copies and realigned by the gather warps, no workspace. Both bit-identical to
+    the default re-pitch + TMA launch, and exact on integer data."""
     g = torch.Generator(device="cuda").manual_seed(n * h + w)
     x = torch.randint(-4, 5, (n, h, w, 3), generator=g, device="cuda").to(dt)
     wt = torch.randint(-4, 5, (k, k, 3, co), generator=g, device="cuda").to(dt)
     b = torch.randint(-4, 5, (co,), generator=g, device="cuda").float()
     ref_conv = wf.FoldedConv2d(wt, b, x.shape, stride=s, padding=p, dtype=dt)
     assert ref_conv.device_plan["producer"] == "repitch+tma"
-    monkeypatch.setenv("WF_GATHER", "1")
+    monkeypatch.setenv("WF_GATHER" if prod == "gather" else "WF_RING", "1")
     conv = wf.FoldedConv2d(wt, b, x.shape, stride=s, padding=p, dtype=dt)
-    assert conv.device_plan["producer"] == "gather" and conv.workspace is None
+    assert conv.device_plan["producer"] == prod
+    assert (conv.workspace is None) == (prod == "gather")
     y = conv(x, out_dtype=torch.float32)
     assert torch.equal(y, ref_conv(x, out_dtype=torch.float32))
     ref = conv_f64(x, wt, b, s, p)

@@ -397,7 +397,7 @@ def test_gather_producer_matches_tma_bitwise(golden_configs, name, kpair, monkey
     """The software-gather producer builds the same shared-memory A image as the TMA boxes."""
     monkeypatch.setenv("WF_KPAIR", kpair)
     y0, _, _, conv = _config_run(golden_configs, name, "")
-    assert conv.device_plan["producer"] in ("tma", "repitch+tma", "gather")
+    assert conv.device_plan["producer"] in ("tma", "repitch+tma", "ring+tma", "gather")
     y1, _, _, _ = _config_run(golden_configs, name, "", flags=0x4000)
     np.testing.assert_array_equal(y0, y1)
 

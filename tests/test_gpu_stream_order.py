@@ -1,0 +1,78 @@
+"""Stream order under programmatic dependent launch (PDL).
+
+The conv kernel is launched with programmatic stream serialization: its
+prologue may run while the previous kernel on the stream is still executing,
+and every global access waits on griddepcontrol.wait. These tests hammer the
+hazards that ordering must cover, comparing every result bitwise with a
+launch made in isolation (synchronised before and after):
+  - RAW on x: a torch kernel writes x, the conv reads it right after;
+  - WAR on x: the conv reads x, the next torch kernel overwrites it;
+  - WAW on y: consecutive convs write the same output buffer;
+  - RAW on y: a torch kernel reads y right after the conv wrote it;
+  - the re-pitch workspace (AlexNet W=227): re-pitch -> conv -> re-pitch ...
+"""
+import pytest
+import torch
+
+import paper_2601_11608_b200 as wf
+
+pytestmark = pytest.mark.gpu
+
+
+def _isolated(conv, x):
+    torch.cuda.synchronize()
+    y = conv(x.clone())
+    torch.cuda.synchronize()
+    return y.clone()
+
+
+@pytest.mark.parametrize("geom", [
+    # n, h, w, c, k, cout, stride, pad, dtype
+    (2, 224, 224, 3, 7, 64, 2, 3, torch.bfloat16),    # R50 conv1
+    (1, 224, 224, 3, 7, 64, 2, 3, torch.float32),     # R50 conv1 b1 TF32 (config 1)
+    (3, 227, 227, 3, 11, 96, 4, 0, torch.bfloat16),   # AlexNet (re-pitch workspace, 2-CTA cluster)
+])
+def test_back_to_back_launches_keep_stream_order(geom):
+    n, h, w, c, k, co, s, p, dt = geom
+    g = torch.Generator(device="cuda").manual_seed(77)
+    xs = [((torch.rand((n, h, w, c), generator=g, device="cuda") * 2 - 1)).to(dt) for _ in range(6)]
+    wt = ((torch.rand((k, k, c, co), generator=g, device="cuda") * 2 - 1) / (k * k * c) ** 0.5).to(dt)
+    b = torch.rand(co, generator=g, device="cuda") * 2 - 1
+    conv = wf.FoldedConv2d(wt, b, xs[0].shape, stride=s, padding=p, dtype=dt)
+    refs = [_isolated(conv, x) for x in xs]
+
+    x = torch.empty_like(xs[0])
+    y = conv(xs[0])
+    sums = torch.empty(len(xs), dtype=torch.float64, device="cuda")
+    outs = []
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for i, xi in enumerate(xs):
+            x.copy_(xi)                    # RAW on x (torch kernel -> conv), WAR vs the previous conv
+            conv(x, out=y)                 # WAW on y (previous conv wrote it too)
+            sums[i] = y.double().sum()     # RAW on y (conv -> torch kernel)
+            if rep == 2:
+                outs.append(y.clone())
+        torch.cuda.synchronize()
+        for i, r in enumerate(refs):
+            assert sums[i].item() == r.double().sum().item(), f"rep {rep} input {i}: checksum differs"
+    for i, (o, r) in enumerate(zip(outs, refs)):
+        assert torch.equal(o, r), f"input {i}: back-to-back result differs from the isolated launch"
+
+
+def test_consecutive_convs_into_distinct_outputs():
+    """Conv after conv with no torch kernel in between (PDL chain of our own launches)."""
+    dt = torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(5)
+    xs = [(torch.rand((4, 224, 224, 3), generator=g, device="cuda") * 2 - 1).to(dt) for _ in range(8)]
+    wt = ((torch.rand((7, 7, 3, 64), generator=g, device="cuda") * 2 - 1) / 12).to(dt)
+    b = torch.rand(64, generator=g, device="cuda") * 2 - 1
+    conv = wf.FoldedConv2d(wt, b, xs[0].shape, stride=2, padding=3, dtype=dt)
+    refs = [_isolated(conv, x) for x in xs]
+    ys = [torch.empty_like(refs[0]) for _ in xs]
+    torch.cuda.synchronize()
+    for x, y in zip(xs, ys):
+        conv(x, out=y)
+    torch.cuda.synchronize()
+    for i, (y, r) in enumerate(zip(ys, refs)):
+        assert torch.equal(y, r), f"launch {i} differs"

@@ -105,6 +105,12 @@ def test_alexnet_plan_repitches_or_gathers_unaligned_rows(monkeypatch):
     assert (d["f"], d["r"], d["producer"]) == (8, 2, "repitch+tma")
     assert d["pitched_w"] == 232 and d["workspace_bytes"] == 512 * 227 * 232 * 3 * 2
     assert d["wf"] == 29 and d["wfo"] == 28 and d["ow"] == 55
+    # WF_RING=1 (producer 5): gather warps re-pitch each stage unit (8 output rows -> 40 input
+    # rows) into a ring of 3 slots per CTA in the workspace, sized for 160 CTAs, whatever the batch
+    monkeypatch.setenv("WF_RING", "1")
+    d = wf.plan_fold([512, 227, 227, 3], [11, 11, 3, 96], 4, 4, 0, 0, dtype="bf16")["device"]
+    assert d["producer"] == "ring+tma" and d["workspace_bytes"] == 160 * 3 * 40 * 232 * 3 * 2
+    monkeypatch.delenv("WF_RING")
     # WF_GATHER=1: rows staged in shared memory and realigned by gather warps, no workspace
     monkeypatch.setenv("WF_GATHER", "1")
     d = wf.plan_fold([512, 227, 227, 3], [11, 11, 3, 96], 4, 4, 0, 0, dtype="bf16")["device"]
@@ -125,8 +131,9 @@ def test_unfolded_variant_plan():
 
 
 def test_generalized_legality_reasons():
-    # 64-column epilogue chunks: the gather kernel is not built for them -> re-pitch + TMA
+    # unaligned rows: the re-pitch pass + TMA by default
     assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=16)["device"]["producer"] == "repitch+tma"
+    assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=4, dtype="tf32")["device"]["producer"] == "repitch+tma"
     assert wf.plan_fold([1, 32, 30, 3], [3, 3, 3, 16], factor=4, dtype="tf32")["device"]["pitched_w"] == 32
     assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], 2, 3, factor=16)["reason"] == "StrideOnFoldAxis"
     assert wf.plan_fold([1, 32, 32, 3], [3, 3, 3, 16], factor=4)["reason"] == "UnalignedPixel"
