@@ -125,7 +125,9 @@ typedef struct {
                               4 rows staged in shared memory + gather warps,
                               5 gather warps re-pitch each stage unit into a
                               ring in the workspace (L2-resident), then TMA
-                              boxes -- rows whose pitch TMA cannot address */
+                              boxes, 6 gather warps load the rows straight from
+                              x (L2-prefetched) into the A layout -- rows whose
+                              pitch TMA cannot address */
   int32_t cta_pair;        /* 2: the conv runs on CTA pairs (cta_group::2, M = 256
                               per MMA), each SM holding half of every B block */
   int32_t stage_tiles;     /* M tiles fed by one A stage: 2 when two consecutive

@@ -33,67 +33,100 @@ namespace wfb {
 // One warp per row (grid-stride over rows). Lane L of a round owns output
 // chunk k = base + L = input-row bytes [16k, 16k+16): it loads the aligned
 // 16-byte chunk k of the row's aligned superset once (coalesced, 512 B per
-// warp-round), takes chunk k+1 from lane L+1 by shuffle (lane 31 loads it),
+// warp-round), takes chunk k+1 from lane L+1 by shuffle (lane 31 from lane 0
+// of the next round),
 // and funnel-shifts the pair by the row's misalignment -- every input byte is
 // read once and every output byte written once. Bytes past rb_in are zero.
-__device__ __forceinline__ uint32_t pick8(const uint32_t (&q)[8], int i) {
-  uint32_t v = q[0];
+// Bytes [4*Q4 + bs/8, +16) of the 32-byte pair (a, b): the row's word offset
+// Q4 is a template parameter (uniform per row), so no indexed selects.
+template <int Q4>
+__device__ __forceinline__ void shift_out(const uint4& a, const uint4& b, uint32_t bs, uint32_t (&w)[4]) {
+  const uint32_t q[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-  for (int t = 1; t < 8; ++t) v = (i == t) ? q[t] : v;  // selects, no local-memory indexing
-  return v;
+  for (int t = 0; t < 4; ++t) w[t] = __funnelshift_r(q[t + Q4], q[t + Q4 + 1], bs);  // bs = 0: q[t + Q4]
 }
 
+// One row's chunks, loaded (kRounds rounds of 32 + the chunk after them for
+// lane 0, all in flight at once) and then shifted and stored: lane 31's right
+// neighbour comes from lane 0 of the next round by shuffle, so no load waits
+// on another. Rows shorter than 32 * kRounds chunks take one round trip.
+constexpr int kRepitchRounds = 3;
+struct RowChunks {
+  uint4 c[kRepitchRounds + 1];
+};
+
+__device__ __forceinline__ void repitch_load(const uint4* a0, int s0, int nin, int lane, bool valid, RowChunks& rc) {
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+  for (int j = 0; j <= kRepitchRounds; ++j) {
+    const int k = s0 + 32 * j + lane;
+    rc.c[j] = (valid && k < nin && (j < kRepitchRounds || lane == 0)) ? __ldg(a0 + k) : z;
+  }
+}
+
+template <int Q4>
+__device__ __forceinline__ void repitch_store(const RowChunks& rc, uint8_t* dst, int s0, int cpr, int rb_in,
+                                              uint32_t bs, int lane) {
+#pragma unroll
+  for (int j = 0; j < kRepitchRounds; ++j) {
+    const int k = s0 + 32 * j + lane;
+    const int src = (lane + 1) & 31;
+    uint4 n;
+    n.x = __shfl_sync(0xffffffffu, (lane == 0) ? rc.c[j + 1].x : rc.c[j].x, src);
+    n.y = __shfl_sync(0xffffffffu, (lane == 0) ? rc.c[j + 1].y : rc.c[j].y, src);
+    n.z = __shfl_sync(0xffffffffu, (lane == 0) ? rc.c[j + 1].z : rc.c[j].z, src);
+    n.w = __shfl_sync(0xffffffffu, (lane == 0) ? rc.c[j + 1].w : rc.c[j].w, src);
+    if (k >= cpr) continue;
+    uint32_t w[4];
+    shift_out<Q4>(rc.c[j], n, bs, w);
+    const int o = 16 * k;
+    if (o + 16 > rb_in) {  // zero the bytes past the input row
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (o + 4 * t + b < rb_in) m |= 0xFFu << (8 * b);
+        w[t] &= m;
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + o) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__device__ __forceinline__ void repitch_store_any(const RowChunks& rc, uint8_t* dst, int s0, int cpr, int rb_in,
+                                                  int sh, int lane) {
+  const uint32_t bs = static_cast<uint32_t>(sh & 3) * 8;
+  switch (sh >> 2) {  // warp-uniform
+    case 0: repitch_store<0>(rc, dst, s0, cpr, rb_in, bs, lane); break;
+    case 1: repitch_store<1>(rc, dst, s0, cpr, rb_in, bs, lane); break;
+    case 2: repitch_store<2>(rc, dst, s0, cpr, rb_in, bs, lane); break;
+    default: repitch_store<3>(rc, dst, s0, cpr, rb_in, bs, lane); break;
+  }
+}
+
+// Two rows per warp in flight (grid-stride pairs of rows).
 __global__ void __launch_bounds__(256) repitch_kernel(const uint8_t* __restrict__ x, uint8_t* __restrict__ y,
                                                       long long rows, int rb_in, int rb_out) {
-  constexpr int kRounds = 4;  // rounds of 32 chunks loaded before any is stored (memory-level parallelism)
   const int lane = threadIdx.x & 31;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const int cpr = rb_out >> 4;
-  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-  for (long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+  for (long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += 2 * nwarps) {
+    const long long r2 = r + nwarps;
+    const bool has2 = r2 < rows;
     const uintptr_t src = reinterpret_cast<uintptr_t>(x) + r * rb_in;
+    const uintptr_t src2 = reinterpret_cast<uintptr_t>(x) + (has2 ? r2 : r) * rb_in;
     const uint4* a0 = reinterpret_cast<const uint4*>(src & ~static_cast<uintptr_t>(15));
-    const int sh = static_cast<int>(src & 15u);
-    const int nin = (sh + rb_in + 15) >> 4;  // aligned chunks that hold the row
-    uint8_t* dst = y + r * rb_out;
-    for (int s0 = 0; s0 < cpr; s0 += 32 * kRounds) {
-      uint4 c[kRounds];
-#pragma unroll
-      for (int j = 0; j < kRounds; ++j) {
-        const int k = s0 + 32 * j + lane;
-        c[j] = (k < nin) ? __ldg(a0 + k) : z;
-      }
-#pragma unroll
-      for (int j = 0; j < kRounds; ++j) {
-        const int k = s0 + 32 * j + lane;
-        uint4 n;
-        n.x = __shfl_down_sync(0xffffffffu, c[j].x, 1);
-        n.y = __shfl_down_sync(0xffffffffu, c[j].y, 1);
-        n.z = __shfl_down_sync(0xffffffffu, c[j].z, 1);
-        n.w = __shfl_down_sync(0xffffffffu, c[j].w, 1);
-        if (lane == 31) n = (k + 1 < nin) ? __ldg(a0 + k + 1) : z;
-        if (k >= cpr) continue;
-        const uint32_t q[8] = {c[j].x, c[j].y, c[j].z, c[j].w, n.x, n.y, n.z, n.w};
-        const int ws = sh >> 2, bs = (sh & 3) * 8;
-        uint32_t w[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const uint32_t lo = pick8(q, t + ws), hi = pick8(q, t + ws + 1);
-          w[t] = bs ? __funnelshift_r(lo, hi, bs) : lo;
-        }
-        const int o = 16 * k;
-        if (o + 16 > rb_in) {  // zero the bytes past the input row
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            uint32_t m = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              if (o + 4 * t + b < rb_in) m |= 0xFFu << (8 * b);
-            w[t] &= m;
-          }
-        }
-        *reinterpret_cast<uint4*>(dst + o) = make_uint4(w[0], w[1], w[2], w[3]);
-      }
+    const uint4* a2 = reinterpret_cast<const uint4*>(src2 & ~static_cast<uintptr_t>(15));
+    const int sh = static_cast<int>(src & 15u), sh2 = static_cast<int>(src2 & 15u);
+    const int nin = (sh + rb_in + 15) >> 4, nin2 = (sh2 + rb_in + 15) >> 4;  // aligned chunks holding the row
+    for (int s0 = 0; s0 < cpr; s0 += 32 * kRepitchRounds) {
+      RowChunks c1, c2;
+      repitch_load(a0, s0, nin, lane, true, c1);
+      repitch_load(a2, s0, nin2, lane, has2, c2);
+      repitch_store_any(c1, y + r * rb_out, s0, cpr, rb_in, sh, lane);
+      if (has2) repitch_store_any(c2, y + r2 * rb_out, s0, cpr, rb_in, sh2, lane);
     }
   }
 }

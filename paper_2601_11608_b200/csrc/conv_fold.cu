@@ -234,7 +234,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   // producer instead -- same shared-memory image, so results are bit-identical
   const bool tf32 = (in_t == WF_TF32);
   const int prod =
-      ((S.prod == 0 || S.prod == 3 || S.prod == 4 || S.prod == 5) && (epilogue & WF_EPI_ROW_PRODUCER) && !tf32) ? 1
+      ((S.prod == 0 || S.prod >= 3) && (epilogue & WF_EPI_ROW_PRODUCER) && !tf32) ? 1
                                                                                                               : S.prod;
   a.prod = prod;
   a.off_raw = a.off_bias + kMaxAccCols * 4;
@@ -254,7 +254,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   a.rows_per_stage = 0;
   a.log_wbox = 0;
   while ((1 << a.log_wbox) < a.Wbox) ++a.log_wbox;
-  for (int b = 0; b < S.s && (prod == 1 || prod == 4); ++b) {  // folded raw rows of one stage (row producers)
+  for (int b = 0; b < S.s && (prod == 1 || prod == 4 || prod == 6); ++b) {  // folded raw rows of one stage (row producers)
     if (!S.has_res[b]) continue;
     const int rows = S.amax[b] - S.amin[b] + static_cast<int>(p.tile_rows) * S.tps;
     for (int i = 0; i < rows; ++i) {
@@ -394,7 +394,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   }
 
   const int grid = a.n_tiles * a.ctas_per_ntile;
-  if (S.pair == 2 && (prod == 1 || prod == 2 || prod == 4)) {
+  if (S.pair == 2 && (prod == 1 || prod == 2 || prod == 4 || prod == 6)) {
     *err = "the row producers run single-CTA plans";
     return WF_UNSUPPORTED;
   }
@@ -402,7 +402,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     *err = "more CTAs than the ring workspace was sized for";
     return WF_UNSUPPORTED;
   }
-  if (tf32 && (S.CH != 32 || prod == 1 || prod == 2 || prod == 4 || prod == 5)) {
+  if (tf32 && (S.CH != 32 || prod == 1 || prod == 2 || prod >= 4)) {
     *err = "tf32 plans use 32-column epilogue chunks and the TMA producer";
     return WF_UNSUPPORTED;
   }
@@ -422,7 +422,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     L.fn = conv_kernel_fn<0>(kind, out_dtype, S.CH);
   } else if (prod == 1) {
     L.fn = conv_kernel_fn<1>(kind, out_dtype, S.CH);
-  } else if (prod == 4) {
+  } else if (prod == 4 || prod == 6) {  // 6: the producer-4 kernel with a.prod == 6 (rows loaded from x)
     L.fn = conv_kernel_fn<4>(kind, out_dtype, S.CH);
   } else if (prod == 5) {
     L.fn = conv_kernel_fn<5>(kind, out_dtype, S.CH);
@@ -435,7 +435,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   }
   L.grid = grid;
   if (const char* e = std::getenv("WF_PDL")) L.pdl = e[0] != '0';
-  L.block = (prod == 4) ? 320 + 32 * kGatherWarps4
+  L.block = (prod == 4 || prod == 6) ? 320 + 32 * kGatherWarps4
                         : (prod == 5 ? 320 + 32 * kGatherWarps5 : ((prod == 1 || prod == 2) ? 320 + 32 * kGatherWarps : 320));
   L.smem = smem;
   cudaError_t e = ensure_smem(L.fn, L.device, smem);

@@ -526,7 +526,7 @@ struct GatherRow {
 // the raw slot holding input bytes [s0, ...). Everything but the block index
 // is warp-uniform; per-block bounds are 32-bit offsets from the row start.
 __device__ __forceinline__ void gather_load(const RowProd& p, int n, int oh0, int r, int lane, int nit,
-                                            uint32_t slot, long long s0, GatherRow& g) {
+                                            uint32_t slot, long long s0, GatherRow& g, bool direct) {
   const uint32_t e = ptx::ld_shared_u32(p.row_tab + 4 * r);
   const int ih = (oh0 + static_cast<int>(static_cast<int8_t>(e >> 16))) * p.s + static_cast<int>(e & 0xFF);
   g.roff = (e & 0xFF) * p.region_bytes + ((e >> 8) & 0xFF) * p.Wbox * 16;
@@ -537,12 +537,16 @@ __device__ __forceinline__ void gather_load(const RowProd& p, int n, int oh0, in
   g.s2 = mis;
   const int rel0 = wrel - mis;                          // first block, relative to the row start
   const uint32_t sb = slot + static_cast<uint32_t>(row + rel0 - s0);  // its slot address (16-byte aligned)
+  const uint8_t* const gb = p.x + (row + rel0);                        // direct (a.prod 6): the block in x
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int brel = rel0 + 16 * (lane + 32 * i);
     // only blocks holding row bytes are read (an aligned block never crosses a page)
     const bool ok = valid && i < nit && brel > -16 && brel < p.rb;
-    g.v[i] = ok ? ptx::ld_shared_v4(sb + 16 * (lane + 32 * i)) : make_uint4(0u, 0u, 0u, 0u);
+    if (direct)
+      g.v[i] = ok ? ptx::ld_global_nc_v4(gb + 16 * (lane + 32 * i)) : make_uint4(0u, 0u, 0u, 0u);
+    else
+      g.v[i] = ok ? ptx::ld_shared_v4(sb + 16 * (lane + 32 * i)) : make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -879,6 +883,18 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
     const uint32_t a_base = base + a.off_a, raw_base = base + a.off_raw;
     GatherRow g0, g1;
     constexpr int P = kGatherWarps4;
+    // a.prod 6 (direct): no raw slots -- rows are read straight from x, whose
+    // unit spans gather warp 0 prefetches into L2 two units ahead
+    const bool direct = a.prod == 6;
+    const bool pf = direct && gw == 0 && lane == 0;
+    auto prefetch_unit = [&](int u) {
+      int n, oh0;
+      long long s0, s1;
+      unit_span(a, rp, u, n, oh0, s0, s1);
+      if (s1 > s0) prefetch_l2_bulk(rp.x + s0, static_cast<uint32_t>(s1 - s0));
+    };
+    if (pf)
+      for (int u = local; u < units && u < local + 2 * stride; u += stride) prefetch_unit(u);
     int it = 0;
     for (int u = local; u < units; u += stride, ++it) {
       const int stage = it % nstages;
@@ -888,11 +904,15 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
       long long s0, s1;
       unit_span(a, rp, u, n, oh0, s0, s1);
       const uint32_t slot = raw_base + rs * rp.raw_slot_bytes;
-      mbar_wait(bar_raw_full + 8 * rs, static_cast<uint32_t>(it >> 1) & 1u);
+      if (direct) {
+        if (pf && u + 2 * stride < units) prefetch_unit(u + 2 * stride);
+      } else {
+        mbar_wait(bar_raw_full + 8 * rs, static_cast<uint32_t>(it >> 1) & 1u);
+      }
       // two rows in flight: load one while the other is realigned and stored
       int r = gw;
-      if (r < rps) gather_load(rp, n, oh0, r, lane, nit, slot, s0, g0);
-      if (r + P < rps) gather_load(rp, n, oh0, r + P, lane, nit, slot, s0, g1);
+      if (r < rps) gather_load(rp, n, oh0, r, lane, nit, slot, s0, g0, direct);
+      if (r + P < rps) gather_load(rp, n, oh0, r + P, lane, nit, slot, s0, g1, direct);
       mbar_wait(bar_empty + 8 * stage, (round & 1u) ^ 1u);
       const uint32_t dst = a_base + stage * stage_bytes;
       auto store = [&](const GatherRow& g) {
@@ -901,14 +921,14 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
       };
       for (; r < rps; r += 2 * P) {
         store(g0);
-        if (r + 2 * P < rps) gather_load(rp, n, oh0, r + 2 * P, lane, nit, slot, s0, g0);
+        if (r + 2 * P < rps) gather_load(rp, n, oh0, r + 2 * P, lane, nit, slot, s0, g0, direct);
         if (r + P < rps) {
           store(g1);
-          if (r + 3 * P < rps) gather_load(rp, n, oh0, r + 3 * P, lane, nit, slot, s0, g1);
+          if (r + 3 * P < rps) gather_load(rp, n, oh0, r + 3 * P, lane, nit, slot, s0, g1, direct);
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_raw_empty + 8 * rs);  // the slot's rows are consumed
+      if (lane == 0 && !direct) mbar_arrive(bar_raw_empty + 8 * rs);  // the slot's rows are consumed
       fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_full + 8 * stage);
@@ -929,9 +949,9 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
         unit_span(a, rp, u, n, oh0, s0, s1);
         if (s1 > s0) prefetch_l2_bulk(rp.x + s0, static_cast<uint32_t>(s1 - s0));
       };
-      for (int u = local; u < units && u < local + 2 * stride; u += stride) prefetch_unit(u);
+      for (int u = local; u < units && u < local + 2 * stride && a.prod != 6; u += stride) prefetch_unit(u);
       int it = 0;
-      for (int u = local; u < units; u += stride, ++it) {
+      for (int u = local; u < units && a.prod != 6; u += stride, ++it) {  // (6: the gather warps read x)
         const int rs = it & 1;
         mbar_wait(bar_raw_empty + 8 * rs, (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
         if (u + 2 * stride < units) prefetch_unit(u + 2 * stride);

@@ -56,6 +56,7 @@ py::dict raw_dict(const wf_fold_plan& p) {
                   : p.producer == 2 ? "im2col"
                   : p.producer == 3 ? "repitch+tma"
                   : p.producer == 5 ? "ring+tma"
+                  : p.producer == 6 ? "gather-direct"
                                     : "gather";
   d["pitched_w"] = p.pitched_w; d["workspace_bytes"] = p.workspace_bytes; d["cta_pair"] = p.cta_pair; d["stage_tiles"] = p.stage_tiles; d["kstep_mode"] = p.kstep_mode;
   d["in_dtype"] = p.in_dtype; d["launch_opts"] = p.launch_opts; d["useful_macs"] = p.useful_macs; d["issued_macs"] = p.issued_macs;

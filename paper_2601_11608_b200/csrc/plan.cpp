@@ -392,12 +392,13 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
       const char* eg = std::getenv("WF_GATHER");
       const char* er = std::getenv("WF_REPITCH");
       const char* eq = std::getenv("WF_RING");
-      want = (eg && eg[0] == '1') ? 4 : ((eq && eq[0] == '1') ? 5 : 3);
+      want = (eg && eg[0] == '1') ? 4 : ((eg && eg[0] == '2') ? 6 : ((eq && eq[0] == '1') ? 5 : 3));
       (void)er;
     }
     // 4: 16-bit data, <= 128 row blocks, single-CTA plans
-    if (want == 4 && in_dtype != WF_TF32 && S.esize == 2 && Q * Wbox + 2 <= 128 && rows <= 64 && pair_req != 1)
-      S.prod = 4;
+    if ((want == 4 || want == 6) && in_dtype != WF_TF32 && S.esize == 2 && Q * Wbox + 2 <= 128 && rows <= 64 &&
+        pair_req != 1)
+      S.prod = static_cast<int>(want);  // 6: the same gather warps loading the rows straight from x (L2-prefetched)
     // 5: 16-bit data, a re-pitched row of <= 127 16-byte blocks (4 per gather lane), single-CTA plans
     if (want == 5 && in_dtype != WF_TF32 && (Wp * d.c * S.esize) / 16 + 1 <= 128 && pair_req != 1) {
       int amin_min = INT32_MAX, amax_max = INT32_MIN;
@@ -432,7 +433,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // tf32 (fp32 outputs): 32-column chunks (8 fp32 = 32 B).
   S.CH = (in_dtype != WF_TF32 && S.Ng % 64 == 0) ? 64 : 32;
   if (S.prod == 4 && S.CH != 32) S.prod = 3;  // the gather kernel is built for 32-column epilogue chunks
-  if (S.prod == 5) S.CH = 32;  // 576 threads: the 64-column epilogue would spill at the register cap
+  if (S.prod == 5 || S.prod == 6) S.CH = 32;  // 576 threads: the 64-column epilogue would spill at the register cap
   std::vector<int64_t> lo(G), hi(G);
   for (int64_t g = 0; g < G; ++g) {
     lo[g] = INT64_MAX;
@@ -609,7 +610,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // tools/probes/sw32_probe.cu). Otherwise the canonical no-swizzle layout of
   // 16-byte core columns ([q][row][folded col][16 B], + the shift region).
   S.sw32 = !S.kpair && !S.need_shift && Q >= 2 && in_dtype != WF_TF32;
-  if (S.sw32 && (S.prod == 4 || S.prod == 5)) S.prod = 3;  // the gather warps / ring maps: no-swizzle layout only
+  if (S.sw32 && (S.prod == 4 || S.prod == 5 || S.prod == 6)) S.prod = 3;  // the gather warps / ring maps: no-swizzle layout only
   if (S.sw32) {
     S.qs.clear();
     for (int64_t g = 0; g < G; ++g)
@@ -943,9 +944,9 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   p.table_bytes = (p.mma_entries * 24 + G * 4 + 127) / 128 * 128;
   p.packed_bytes = p.table_bytes + b_cursor;
   p.epi_chunk = S.CH;
-  S.raw_slots = (S.prod == 4) ? 2 : (S.prod == 5 ? kRingSlots : kRawSlots);
+  S.raw_slots = (S.prod == 4) ? 2 : (S.prod == 5 ? kRingSlots : (S.prod == 6 ? 0 : kRawSlots));
   S.raw_slot_bytes = (S.prod == 4) ? static_cast<int>(unit_slot)
-                                   : (S.prod == 5 ? 0 : raw_slot_bytes_for(d.w * d.c * S.esize));
+                                   : ((S.prod == 5 || S.prod == 6) ? 0 : raw_slot_bytes_for(d.w * d.c * S.esize));
   p.variant = WF_VARIANT_FOLD;
   p.producer = S.prod;
   p.pitched_w = (S.prod == 3 || S.prod == 5) ? S.Wp : 0;

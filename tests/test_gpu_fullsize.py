@@ -320,11 +320,12 @@ def test_c_abi_pack_and_forward_via_ctypes(oracle):
                                                 (4, 45, 71, 5, 96, 1, 2, torch.float16),
                                                 (2, 33, 50, 3, 96, 2, 1, torch.bfloat16)],
                          ids=["alexnet_b64", "alexnet_b3", "w71_k5", "w50_k3"])
-@pytest.mark.parametrize("prod", ["ring+tma", "gather"])
+@pytest.mark.parametrize("prod", ["ring+tma", "gather", "gather-direct"])
 def test_gather_producer_bitwise_vs_repitch(monkeypatch, n, h, w, k, co, s, p, dt, prod):
     """Unaligned rows without the re-pitch pass -- WF_RING=1 (producer 5): gather warps re-pitch each
     stage unit into an L2 ring the TMA boxes read; WF_GATHER=1 (producer 4): rows staged in shared
-    memory by bulk copies and realigned by the gather warps, no workspace. Both bit-identical to
+    memory by bulk copies and realigned by the gather warps, no workspace; WF_GATHER=2 (producer 6):
+    the same gather warps loading the rows straight from x (L2-prefetched). All bit-identical to
     the default re-pitch + TMA launch, and exact on integer data."""
     g = torch.Generator(device="cuda").manual_seed(n * h + w)
     x = torch.randint(-4, 5, (n, h, w, 3), generator=g, device="cuda").to(dt)
@@ -332,10 +333,13 @@ def test_gather_producer_bitwise_vs_repitch(monkeypatch, n, h, w, k, co, s, p, d
     b = torch.randint(-4, 5, (co,), generator=g, device="cuda").float()
     ref_conv = wf.FoldedConv2d(wt, b, x.shape, stride=s, padding=p, dtype=dt)
     assert ref_conv.device_plan["producer"] == "repitch+tma"
-    monkeypatch.setenv("WF_GATHER" if prod == "gather" else "WF_RING", "1")
+    if prod == "ring+tma":
+        monkeypatch.setenv("WF_RING", "1")
+    else:
+        monkeypatch.setenv("WF_GATHER", "1" if prod == "gather" else "2")
     conv = wf.FoldedConv2d(wt, b, x.shape, stride=s, padding=p, dtype=dt)
     assert conv.device_plan["producer"] == prod
-    assert (conv.workspace is None) == (prod == "gather")
+    assert (conv.workspace is None) == (prod != "ring+tma")
     y = conv(x, out_dtype=torch.float32)
     assert torch.equal(y, ref_conv(x, out_dtype=torch.float32))
     ref = conv_f64(x, wt, b, s, p)
