@@ -551,6 +551,11 @@ def run_gpu(args) -> None:
         variants["fold_speedup_vs_unfolded"] = ums / ms_step
         variants["zeropad_byte_ratio_bound"] = (IN_BYTES_PER_IMG * 8 / 3 + OUT_BYTES_PER_IMG) / (
             IN_BYTES_PER_IMG + OUT_BYTES_PER_IMG)
+        variants["unfolded_note"] = (
+            "unfolded Cin=3 builds an explicit im2col A tile with transposer warps (6-byte pixels: no TMA im2col "
+            "box); it moves the same HBM bytes as the fold but runs at the hbm_roofline_frac shown, bound by its "
+            "gather, so fold_speedup_vs_unfolded measures that gather; zeropad_cin8 (TMA, same kernel) is the "
+            "hardware-fair baseline")
         del convz, convu
         torch.cuda.empty_cache()
 
@@ -570,6 +575,18 @@ def run_gpu(args) -> None:
                "d2h_bytes_per_step": yh.numel() * 2 * world, "ms_per_step": ems, "steps": es,
                "images_per_rank": ne,
                "path": "FoldedConv2d.run_host (pinned host -> H2D -> folded conv -> D2H, chunked on 2 streams)"}
+        # the PCIe ceiling of that leg on this box: plain pinned copies of one chunk, each direction alone
+        m = min(ne, args.e2e_chunk)
+        sync = lambda: torch.cuda.synchronize(dev)  # noqa: E731
+        d2h_ms = _timed(lambda: yh[:m].copy_(y[:m], non_blocking=True), 5, 1, stream, sync)
+        h2d_ms = _timed(lambda: x[:m].copy_(xh[:m], non_blocking=True), 5, 1, stream, sync)
+        d2h_gbs = yh[:m].numel() * 2 / (d2h_ms / 1e3) / 1e9
+        h2d_gbs = xh[:m].numel() * 2 / (h2d_ms / 1e3) / 1e9
+        floor_ms = yh.numel() * 2 / d2h_gbs / 1e6  # the output's D2H alone at the copy-engine rate
+        e2e["pcie"] = {"d2h_gbs": d2h_gbs, "h2d_gbs": h2d_gbs, "d2h_floor_ms": floor_ms,
+                       "floor_over_e2e": floor_ms / ems,
+                       "note": "pinned-copy rates measured on this box; the e2e step cannot beat its "
+                               "output's device-to-host copy"}
         del xh, yh
 
     # ---- CPU baseline: rank 0, every N (the other ranks wait at the final barrier) --

@@ -37,12 +37,13 @@ CONFIGS = {  # name: (N, H, W, C, K, Cout, stride, pad, dtype, relu)  -- BASELIN
 
 
 def peaks():
-    """MEASURED_PEAKS.json (driver-written), else the B200_PROFILING.md fallback."""
+    """(HBM GB/s, bf16 TFLOP/s, source): MEASURED_PEAKS.json (driver-written), else the
+    B200_PROFILING.md fallback, labelled as such."""
     try:
         p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"])
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "MEASURED_PEAKS.json"
     except (OSError, KeyError, ValueError):
-        return 6650.0, 1590.0
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
 def oracle():
@@ -168,7 +169,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "configs.json"))
     ap.add_argument("--only", default="")
     args = ap.parse_args()
-    hbm, tc = peaks()
+    hbm, tc, peak_src = peaks()
     orc = oracle()
     dev = torch.device("cuda", 0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -240,7 +241,7 @@ def main():
     if not args.only or "gemm" in args.only:
         results["tall_skinny_gemm"] = bench_gemm(args.iters, hbm)
         results["tall_skinny_gemm_shapes"] = bench_gemm_shapes(args.iters, hbm)
-    results["_peaks"] = {"hbm_gbs": hbm, "bf16_tflops": tc, "source": "MEASURED_PEAKS.json"}
+    results["_peaks"] = {"hbm_gbs": hbm, "bf16_tflops": tc, "source": peak_src}
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(results, open(args.out, "w"), indent=1)
 
