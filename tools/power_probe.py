@@ -3,7 +3,7 @@
   python tools/power_probe.py [n] [seconds]
 
 For every flag set, runs the folded conv back to back for `seconds` while
-nvidia-smi samples power.draw and clocks.sm every 100 ms; prints ms/launch,
+nvidia-smi samples power.draw.instant and clocks.sm every 100 ms; prints ms/launch,
 median W and MHz, and mJ per image. Profiling switches (conv_kernel.cuh):
 0x100 no MMAs, 0x200 no epilogue, 0x1000 no A loads.
 """
@@ -28,7 +28,7 @@ for flags in FLAGS:
     for _ in range(3):
         conv._forward(x, out=y, flags=max(flags, 0))
     torch.cuda.synchronize()
-    smi = subprocess.Popen(["nvidia-smi", "--query-gpu=power.draw,clocks.sm", "--format=csv,noheader,nounits",
+    smi = subprocess.Popen(["nvidia-smi", "--query-gpu=power.draw.instant,clocks.sm", "--format=csv,noheader,nounits",
                             "-lms", "100"], stdout=subprocess.PIPE, text=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.time()
