@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -71,6 +72,9 @@ struct PreparedLaunch {
   const void* fn = nullptr;
   int grid = 0, block = 0, smem = 0, cluster = 1;
   bool pdl = true;  // programmatic dependent launch (WF_PDL=0 turns it off; read at prepare time)
+  // operand epoch of this entry's last launch (~0: never launched): a launch
+  // after a pack / bias write goes without PDL (note_operand_write)
+  mutable std::atomic<uint64_t> epoch_seen{~0ull};
   // producer 3: re-pitch x into the workspace first
   bool repitch = false;
   long long rp_rows = 0;
@@ -225,6 +229,20 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   a.epi_pp = (max_cols <= 128 && a.n_tiles == 1 && S.pair == 1) ? 1 : 0;
   if (const int pp = (p.launch_opts >> 1) & 3) a.epi_pp = (pp == 2 && S.pair == 1) ? 1 : 0;
   a.epi_flags = static_cast<int>(epilogue);
+  // Single-pass launches (every CTA gets at most one stage unit, e.g. batch 1):
+  // extra A stages and accumulator buffers only cost shared memory and TMEM.
+  // With one stage set (ksplit stages) and one accumulator per tile of the unit,
+  // two CTAs fit on an SM, so under programmatic dependent launch the next
+  // launch's CTAs become resident, initialise and load their B operand while
+  // this launch still runs.
+  if (a.num_units <= a.unit_stride && S.pair == 1 && !(p.launch_opts & 1)) {
+    a.stages = std::max(1, std::min(a.stages, S.ksplit));  // (a.ksplit is filled in further down)
+    while (a.n_acc > 1 && a.n_acc / 2 >= a.tps) {
+      a.n_acc /= 2;
+      --a.acc_shift;
+    }
+    a.tmem_cols = std::max(32u, static_cast<unsigned>(a.n_acc) * a.acc_stride);
+  }
   // shared-memory carve-up (offsets from the 1024-aligned base)
   a.off_a = kCtrlBytes;
   a.off_b = a.off_a + a.stages * a.stage_bytes + kTileM * 16;
@@ -446,7 +464,9 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   return WF_OK;
 }
 
-cudaError_t launch_prepared(const PreparedLaunch& L, cudaStream_t st) {
+std::atomic<uint64_t> g_operand_epoch{0};
+
+cudaError_t launch_prepared(const PreparedLaunch& L, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(L.grid);
   cfg.blockDim = dim3(L.block);
@@ -461,7 +481,7 @@ cudaError_t launch_prepared(const PreparedLaunch& L, cudaStream_t st) {
     attr[n].val.clusterDim.z = 1;
     ++n;
   }
-  if (L.pdl) {  // the kernel's prologue overlaps the previous grid (griddepcontrol.wait guards every access)
+  if (pdl) {  // the kernel's prologue (+ B load) overlaps the previous grid (griddepcontrol.wait guards the rest)
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;
@@ -510,13 +530,18 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     wf_status rs = launch_repitch(x, const_cast<void*>(workspace), L->rp_rows, L->rp_in, L->rp_out, st, err);
     if (rs != WF_OK) return rs;
   }
-  const cudaError_t e = launch_prepared(*L, st);
+  const uint64_t ep = g_operand_epoch.load(std::memory_order_acquire);
+  const bool pdl = L->pdl && L->epoch_seen.exchange(ep, std::memory_order_acq_rel) == ep;
+  const cudaError_t e = launch_prepared(*L, st, pdl);
   if (e != cudaSuccess) {
     *err = std::string("conv_fold_kernel launch failed: ") + cudaGetErrorString(e);
     return WF_CUDA_ERROR;
   }
   return WF_OK;
 }
+
+void note_operand_write() { g_operand_epoch.fetch_add(1, std::memory_order_acq_rel); }
+uint64_t operand_epoch() { return g_operand_epoch.load(std::memory_order_acquire); }
 
 int sm_count(int device) {
   static std::mutex mu;

@@ -722,11 +722,15 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // Programmatic dependent launch: everything above (launch, barrier init, TMEM
-  // allocation, tensor-map prefetch) overlaps the previous grid's tail; every
-  // global read (x, packed filter, bias, workspace) and every store of y comes
-  // after the wait. The next grid may start its own prologue from here on.
+  // allocation, tensor-map prefetch) overlaps the previous grid's tail, and so
+  // does the producer's bulk copy of the packed filter (B): every other global
+  // access -- x, the workspace, the bias, every store of y -- comes after
+  // griddepcontrol.wait in the thread that makes it. B is written only by the
+  // pack kernel; the first launch after any pack runs without the PDL
+  // attribute (host side, conv_fold.cu), so that B is complete when read.
+  // The next grid may start its own prologue from here on.
   griddep_launch_dependents();
-  griddep_wait();
+  if (warp >= 2) griddep_wait();  // epilogue and gather warps (warp 0: after B; warp 1 touches no global memory)
 
   if (kProd == 5 && warp >= 10) {
     // ===================== L2-ring gather warps (warps 10..17) =====================
@@ -941,6 +945,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
       mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
       for (int off = 0; off < bb; off += 32768)
         bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
+      griddep_wait();  // B overlaps the previous grid; x / workspace come after the wait
       const RowProd rp = row_prod(a, base + 768);
       const int stride = a.unit_stride, units = a.num_units;
       auto prefetch_unit = [&](int u) {  // L2 prefetch of a later unit's span
@@ -980,6 +985,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
         mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
         for (int off = 0; off < bb; off += 32768)
           bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
+      griddep_wait();  // B overlaps the previous grid; x / workspace come after the wait
         int slot_it = 0;
         const bool no_loads = prof(a, 0x1000);
         for (int mt = local; mt < a.num_units; mt += a.unit_stride)  // stage units (= M tiles unless tps 2)
@@ -1059,6 +1065,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
       mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
       for (int off = 0; off < bb; off += 32768)
         bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
+      griddep_wait();  // B overlaps the previous grid; x / workspace come after the wait
       if (kPair == 2 && rank != 0) {  // tell the leader's MMA issuer that our B half landed
         mbar_wait(bar_b, 0);
         mbar_arrive_cluster(mapa(bar_bpeer, 0));

@@ -38,6 +38,13 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
                       cudaStream_t st, int num_sms, LaunchCache* cache, std::string* err);
 int sm_count(int device);
 
+// Every launch that writes a conv operand the kernel reads before its
+// griddepcontrol.wait (the packed filter, the replicated bias) bumps this
+// process-wide epoch; the next conv launch after a bump is made without the
+// programmatic-dependent-launch attribute, so it cannot overlap that write.
+void note_operand_write();
+uint64_t operand_epoch();
+
 // Exact-order fp32 direct conv (reference conv2d semantics, with padding).
 // groups > 1: grouped conv of a block-diagonal dense filter (diagonal blocks only).
 wf_status launch_conv_direct(const wf_conv_desc& d, const float* x, const float* w, float* y, int groups,

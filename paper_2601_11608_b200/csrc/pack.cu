@@ -131,6 +131,7 @@ __global__ void expand_dense_kernel(const float* __restrict__ w, float* __restri
 
 wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, const float* b, void* packed,
                       float* b_rep, cudaStream_t st, std::string* err) {
+  note_operand_write();  // the next conv launch must not overlap this write (programmatic dependent launch)
   const wf_fold_plan& p = S.plan;
   // schedule table first: the pack kernel and the conv kernel both read it.
   // header = schedule table + slot order. A pageable-source cudaMemcpyAsync
@@ -210,6 +211,7 @@ wf_status launch_pack(const Schedule& S, const wf_conv_desc& d, const void* w, c
 }
 
 wf_status launch_replicate_bias(const float* b, int cout, int r, float* out, cudaStream_t st, std::string* err) {
+  note_operand_write();
   replicate_bias_kernel<<<(cout * r + 255) / 256, 256, 0, st>>>(b, out, cout, r);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

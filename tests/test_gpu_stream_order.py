@@ -76,3 +76,29 @@ def test_consecutive_convs_into_distinct_outputs():
     torch.cuda.synchronize()
     for i, (y, r) in enumerate(zip(ys, refs)):
         assert torch.equal(y, r), f"launch {i} differs"
+
+
+def test_repack_then_forward_sees_the_new_filter():
+    """The producer loads the packed filter (B) before griddepcontrol.wait; the launch right after a pack
+    (or bias replication) therefore goes without the PDL attribute. Repack different weights into the SAME
+    buffers between back-to-back launches and check each launch used the filter packed just before it."""
+    dt = torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = (torch.rand((2, 224, 224, 3), generator=g, device="cuda") * 2 - 1).to(dt)
+    ws = [((torch.rand((7, 7, 3, 64), generator=g, device="cuda") * 2 - 1) / 12).to(dt) for _ in range(2)]
+    bs = [torch.rand(64, generator=g, device="cuda") * 2 - 1 for _ in range(2)]
+    refs = [_isolated(wf.FoldedConv2d(w, b, x.shape, stride=2, padding=3, dtype=dt), x) for w, b in zip(ws, bs)]
+    conv = wf.FoldedConv2d(ws[0], bs[0], x.shape, stride=2, padding=3, dtype=dt)
+    y = conv(x)
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    torch.cuda.synchronize()
+    for i in range(12):
+        k = i % 2
+        conv.core.pack(ws[k].data_ptr(), bs[k].data_ptr(), conv.packed.data_ptr(), conv.b_rep.data_ptr(), st)
+        conv(x, out=y)       # right after the pack: no PDL overlap
+        conv(x, out=y)       # PDL again, same operands
+        outs.append((k, y.clone()))
+    torch.cuda.synchronize()
+    for i, (k, o) in enumerate(outs):
+        assert torch.equal(o, refs[k]), f"launch {i}: not the filter packed just before it"
