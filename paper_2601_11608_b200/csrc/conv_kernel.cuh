@@ -132,6 +132,22 @@ __device__ __forceinline__ bool prof(const ConvArgs& a, int bit) {
 #endif
 }
 
+// Launch timeline of CTA 0 (PROFILE builds, TMA producer, switch 0x8000): %globaltimer
+// stamps of each role's milestones in the control area, printed at exit.
+__device__ __forceinline__ void tl_mark(const ConvArgs& a, uint8_t* gbase, int slot) {
+#if WFB_PROFILE
+  if ((a.epi_flags & 0x8000) && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    reinterpret_cast<unsigned long long*>(gbase + 1536)[slot] = t;
+  }
+#else
+  (void)a;
+  (void)gbase;
+  (void)slot;
+#endif
+}
+
 template <typename OutT>
 __device__ __forceinline__ uint32_t pack2(float lo, float hi);
 template <>
@@ -677,6 +693,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
   const int local = cl / a.n_tiles;                               // first M-tile unit of this CTA
   const int ncols = a.nt_cols[ntile];
   const int col0 = a.nt_col0[ntile];
+  if (threadIdx.x == 0) tl_mark(a, gbase, 0);  // entry
 
   if (kProd == 1 || kProd == 4)  // folded stage-row table of the row producers (b | i << 8 | a << 16)
     for (int r = threadIdx.x; r < a.rows_per_stage; r += blockDim.x)
@@ -729,6 +746,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
   // pack kernel; the first launch after any pack runs without the PDL
   // attribute (host side, conv_fold.cu), so that B is complete when read.
   // The next grid may start its own prologue from here on.
+  if (threadIdx.x == 0) tl_mark(a, gbase, 1);  // prologue done
   griddep_launch_dependents();
   if (warp >= 2) griddep_wait();  // epilogue and gather warps (warp 0: after B; warp 1 touches no global memory)
 
@@ -1065,7 +1083,9 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
       mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bb));
       for (int off = 0; off < bb; off += 32768)
         bulk_g2s(base + a.off_b + off, gb + off, static_cast<uint32_t>(min(32768, bb - off)), bar_b);
+      tl_mark(a, gbase, 2);  // B issued
       griddep_wait();  // B overlaps the previous grid; x / workspace come after the wait
+      tl_mark(a, gbase, 3);  // previous grid done
       if (kPair == 2 && rank != 0) {  // tell the leader's MMA issuer that our B half landed
         mbar_wait(bar_b, 0);
         mbar_arrive_cluster(mapa(bar_bpeer, 0));
@@ -1189,6 +1209,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
     const bool leader = elect_one() && rank == 0;  // pair: the leader CTA issues for both SMs
     if (kPair == 2 && rank != 0) goto mma_done;
     mbar_wait(bar_b, 0);
+    if (leader) tl_mark(a, gbase, 4);  // B landed
     if constexpr (kPair == 2) mbar_wait_cluster(bar_bpeer, 0);
     {
     // Per-tile scalars read once (laundering them into registers with opq()
@@ -1232,6 +1253,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
         const int e0 = (ksplit == 1) ? nt_e0 : a.ks_entry0[ks];
         const int entries = (ksplit == 1) ? nt_en : a.ks_entries[ks];
         if (k == 0 && !no_wait) mbar_wait(bar_full + 8 * stage, round & 1u);
+        if (leader && tile == 0 && ks == 0) tl_mark(a, gbase, 5);  // first A stage landed
         if constexpr (kProd == 5) {
           if (k == 0 && ks == 0 && leader) {
             if constexpr (kMc) {  // the shared slot is free once both CTAs' stages landed
@@ -1287,6 +1309,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
         }
       }
       if (leader) commit_to<kPair>(bar_tfull + 8 * acc);
+      if (leader) tl_mark(a, gbase, 6);  // last MMA of the tile issued
       __syncwarp();
      }
      for (int ks = 0; ks < ksplit; ++ks)  // advance past the unit's sub-stages
@@ -1398,6 +1421,7 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
       const int n = vn_u;
       const int oh0 = (a.tps > 1) ? (vrem_u * a.tps + k) * a.OHt : vrem_u * a.OHt;
       mbar_wait(bar_tfull + 8 * acc, acc_round & 1u);
+      if (warp == 2 && lane == 0 && it_tile == 0) tl_mark(a, gbase, 7);  // accumulator ready
       tc_fence_after();
       if (dbg_skip_epi || n_it == 0) {
         tc_fence_before();
@@ -1477,11 +1501,23 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
     }
   }
 
+  if (warp == 2 && lane == 0) tl_mark(a, gbase, 8);  // epilogue warp 2 done (stores issued)
   tc_fence_before();
   // pair: the leader's MMAs wrote this CTA's TMEM; multicast: no CTA leaves
   // while the peer may still commit to its barriers
   if constexpr (kPair == 2 || kMc) cluster_sync();
   else __syncthreads();
+#if WFB_PROFILE
+  if ((a.epi_flags & 0x8000) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long* t = reinterpret_cast<const unsigned long long*>(gbase + 1536);
+    unsigned long long te;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+    printf("timeline cta0 (ns after entry): prologue %llu | B issued %llu | prev grid done %llu | B landed %llu | "
+           "A landed %llu | last MMA issued %llu | acc ready %llu | epilogue done %llu | exit sync %llu\n",
+           t[1] - t[0], t[2] - t[0], t[3] - t[0], t[4] - t[0], t[5] - t[0], t[6] - t[0], t[7] - t[0], t[8] - t[0],
+           te - t[0]);
+  }
+#endif
   if (warp == 1) {
     tc_fence_after();
     if constexpr (kPair == 2) tmem_dealloc_pair(tmem_base, a.tmem_cols);
