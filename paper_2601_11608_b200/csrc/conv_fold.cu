@@ -78,7 +78,7 @@ struct PreparedLaunch {
   // producer 3: re-pitch x into the workspace first
   bool repitch = false;
   long long rp_rows = 0;
-  int rp_in = 0, rp_out = 0;
+  int rp_in = 0, rp_out = 0, rp_planes = 0;
 
   bool same(const void* x_, const void* ws_, const void* pk_, const float* b_, void* y_, wf_dtype o_, uint32_t e_,
             int sms_, int dev_) const {
@@ -335,6 +335,15 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     L.rp_rows = d.n * d.h;
     L.rp_in = static_cast<int>(d.w * d.c * es);
     L.rp_out = static_cast<int>(S.Wp * d.c * es);
+    // core-column planes (the TMA boxes then read whole folded-column runs of one
+    // core column instead of 16-byte pieces): no-swizzle single-CTA / multicast
+    // plans whose box run fits the 256-element box limit; WF_PLANES=0 turns it off
+    const char* ep = std::getenv("WF_PLANES");
+    const bool planes = !(ep && ep[0] == '0') && !S.sw32 && S.pair == 1 && p.wbox * (16 / es) <= 256;
+    if (planes) {
+      L.rp_planes = S.Q;
+      a.planes_e2 = 16 / es;
+    }
     xt = workspace;
   }
   // ---- producer 5: the gather warps re-pitch stage units into a ring of slots in the workspace
@@ -384,6 +393,30 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r4 != CUDA_SUCCESS) {
         *err = "cuTensorMapEncodeTiled(input, swizzle 32B) failed: " + std::to_string(static_cast<int>(r4));
+        return WF_CUDA_ERROR;
+      }
+      continue;
+    }
+    if (prod == 3 && a.planes_e2) {  // {elements of a plane row, input row of residue b, plane, image}
+      const cuuint64_t plane_bytes = static_cast<cuuint64_t>(p.wf) * 16;
+      cuuint64_t gdim4[4] = {static_cast<cuuint64_t>(p.wf) * a.planes_e2, rows_b, static_cast<cuuint64_t>(Q),
+                             static_cast<cuuint64_t>(d.n)};
+      cuuint64_t gstr4[3] = {rowpitch * S.s, plane_bytes, rowpitch * d.h};
+      cuuint32_t box4[4] = {static_cast<cuuint32_t>(p.wbox * a.planes_e2), static_cast<cuuint32_t>(p.nrows),
+                            static_cast<cuuint32_t>(Q), 1};
+      cuuint32_t estr4[4] = {1, 1, 1, 1};
+      void* gaddr4 = const_cast<uint8_t*>(static_cast<const uint8_t*>(xt) + b * rowpitch);
+      CUresult r4 = encode(&maps.in[b], tmap_type(in_t), 4, gaddr4, gdim4, gstr4, box4, estr4,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r4 == CUDA_SUCCESS && S.need_shift) {
+        box4[2] = 1;  // plane 0 only, one folded column further
+        r4 = encode(&maps.in_shift[b], tmap_type(in_t), 4, gaddr4, gdim4, gstr4, box4, estr4,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      }
+      if (r4 != CUDA_SUCCESS) {
+        *err = "cuTensorMapEncodeTiled(input, core-column planes) failed: " + std::to_string(static_cast<int>(r4));
         return WF_CUDA_ERROR;
       }
       continue;
@@ -527,7 +560,8 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     }
   }
   if (L->repitch) {
-    wf_status rs = launch_repitch(x, const_cast<void*>(workspace), L->rp_rows, L->rp_in, L->rp_out, st, err);
+    wf_status rs =
+        launch_repitch(x, const_cast<void*>(workspace), L->rp_rows, L->rp_in, L->rp_out, L->rp_planes, st, err);
     if (rs != WF_OK) return rs;
   }
   const uint64_t ep = g_operand_epoch.load(std::memory_order_acquire);

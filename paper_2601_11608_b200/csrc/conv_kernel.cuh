@@ -68,6 +68,9 @@ struct ConvArgs {
   unsigned a_desc_hi;             // A descriptor bits 32..63: SBO, version, layout (no swizzle / SWIZZLE_32B)
   int tps, uph, tile_shift;       // M tiles per A stage, stage units per image (tps > 1), A bytes between tiles
   int sw32, nq, qregion_bytes;    // SWIZZLE_32B A: one 32-byte-piece box per in-pixel offset
+  int planes_e2;                  // > 0: the workspace holds core-column planes [q][folded col][16 B]
+                                  // (re-pitch pass), 4-D boxes with whole-run inner pieces; value =
+                                  // elements per 16-byte core column
   int qcoord[4];                  // sw32: element coordinate (in the pixel) of each region's box
   int qbyte[4];                   // sw32: the same offset in bytes
   int nt_bbytes[kMaxNTiles];
@@ -1159,6 +1162,13 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
             // kProd 5: the cluster's ring slot (rows from slot row (amin[b] - amin_min)*s + b)
             const int rrow = (kProd == 5) ? a.amin[b] - a.amin_min : oh0 + a.amin[b];
             const int img = (kProd == 5) ? slot_idx : n;
+            if (kProd != 5 && a.planes_e2) {  // core-column planes: {folded-col run, row, plane, image}
+              tma_load_4d_mc(dst + b * a.region_bytes, &maps.in[b], a.c0 * a.planes_e2, rrow, 0, img, fbar, mask);
+              if (a.shift_box_bytes && !dbg_noshift)
+                tma_load_4d_mc(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], (a.c0 + 1) * a.planes_e2,
+                               rrow, 0, img, fbar, mask);
+              continue;
+            }
             tma_load_5d_mc(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, rrow, 0, img, fbar, mask);
             if (a.shift_box_bytes && !dbg_noshift)
               tma_load_5d_mc(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1, rrow, 0, img,
@@ -1173,6 +1183,11 @@ __global__ void __launch_bounds__(kProd == 0 ? 320 : 320 + 32 * (kProd == 4 ? kG
             if (a.shift_box_bytes && !dbg_noshift)
               tma_load_5d(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], 0, a.c0 + 1,
                           a.amin[b] - a.amin_min, 0, slot_idx, fbar);
+          } else if (a.planes_e2) {  // core-column planes: {folded-col run, row, plane, image}
+            tma_load_4d(dst + b * a.region_bytes, &maps.in[b], a.c0 * a.planes_e2, oh0 + a.amin[b], 0, n, fbar);
+            if (a.shift_box_bytes && !dbg_noshift)
+              tma_load_4d(dst + b * a.region_bytes + a.shift_off, &maps.in_shift[b], (a.c0 + 1) * a.planes_e2,
+                          oh0 + a.amin[b], 0, n, fbar);
           } else {
             tma_load_5d(dst + b * a.region_bytes, &maps.in[b], 0, a.c0, oh0 + a.amin[b], 0, n, fbar);
             if (a.shift_box_bytes && !dbg_noshift)

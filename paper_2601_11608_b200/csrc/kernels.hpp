@@ -54,9 +54,10 @@ wf_status launch_bias_add(const float* y, const float* b, float* out, long long 
                           std::string* err);
 wf_status launch_blockdiag_check(const float* wd, int KH, int KW, int Cif, int Cof, int groups,
                                  unsigned long long* scratch, long long* first_bad, cudaStream_t st, std::string* err);
-// Device fold for unaligned rows: copy x (rows of rb_in bytes) into ws (rows of rb_out, zero tail).
-wf_status launch_repitch(const void* x, void* ws, long long rows, int rb_in, int rb_out, cudaStream_t st,
-                         std::string* err);
+// Device fold for unaligned rows: copy x (rows of rb_in bytes) into ws (rows of rb_out, zero tail);
+// planes > 0: each workspace row as `planes` core-column planes [q][folded col][16 B].
+wf_status launch_repitch(const void* x, void* ws, long long rows, int rb_in, int rb_out, int planes,
+                         cudaStream_t st, std::string* err);
 wf_status launch_replicate_bias(const float* b, int cout, int r, float* out, cudaStream_t st, std::string* err);
 
 }  // namespace wfb
