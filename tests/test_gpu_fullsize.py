@@ -320,7 +320,7 @@ def test_c_abi_pack_and_forward_via_ctypes(oracle):
                                                 (4, 45, 71, 5, 96, 1, 2, torch.float16),
                                                 (2, 33, 50, 3, 96, 2, 1, torch.bfloat16)],
                          ids=["alexnet_b64", "alexnet_b3", "w71_k5", "w50_k3"])
-@pytest.mark.parametrize("prod", ["ring+tma", "gather", "gather-direct"])
+@pytest.mark.parametrize("prod", ["ring+tma", "gather", "gather-direct", "repitch-rows"])
 def test_gather_producer_bitwise_vs_repitch(monkeypatch, n, h, w, k, co, s, p, dt, prod):
     """Unaligned rows without the re-pitch pass -- WF_RING=1 (producer 5): gather warps re-pitch each
     stage unit into an L2 ring the TMA boxes read; WF_GATHER=1 (producer 4): rows staged in shared
@@ -335,11 +335,13 @@ def test_gather_producer_bitwise_vs_repitch(monkeypatch, n, h, w, k, co, s, p, d
     assert ref_conv.device_plan["producer"] == "repitch+tma"
     if prod == "ring+tma":
         monkeypatch.setenv("WF_RING", "1")
+    elif prod == "repitch-rows":  # the re-pitch workspace in row layout instead of core-column planes
+        monkeypatch.setenv("WF_PLANES", "0")
     else:
         monkeypatch.setenv("WF_GATHER", "1" if prod == "gather" else "2")
     conv = wf.FoldedConv2d(wt, b, x.shape, stride=s, padding=p, dtype=dt)
-    assert conv.device_plan["producer"] == prod
-    assert (conv.workspace is None) == (prod != "ring+tma")
+    assert conv.device_plan["producer"] == ("repitch+tma" if prod == "repitch-rows" else prod)
+    assert (conv.workspace is None) == (prod not in ("ring+tma", "repitch-rows"))
     y = conv(x, out_dtype=torch.float32)
     assert torch.equal(y, ref_conv(x, out_dtype=torch.float32))
     ref = conv_f64(x, wt, b, s, p)
