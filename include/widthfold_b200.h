@@ -137,8 +137,11 @@ typedef struct {
   int32_t launch_opts;     /* launch tuning decided at plan time (never read
                               from the environment at launch): bit 0 two TMEM
                               accumulator buffers only, bits 1-2 epilogue
-                              ping-pong (0 auto, 1 off, 2 on), bit 3 no
-                              multicast N-tile cluster */
+                              ping-pong (0 default = off, 1 off, 2 on), bit 3
+                              / bit 4 force the multicast N-tile cluster off /
+                              on (plans with two N-tiles; default on only for
+                              TMA boxes straight from x over >= 2 H-stride
+                              residues) */
   int64_t pitched_w;       /* producers 3, 5: re-pitched row width (>= W, % f == 0) */
   int64_t workspace_bytes; /* device scratch wf_conv_fold_fwd_ws needs (0: none) */
   uint64_t useful_macs;    /* count_macs of the original conv */

@@ -224,9 +224,11 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   a.n_acc = (a.acc_stride <= 128 && !(p.launch_opts & 1)) ? 4 : 2;
   a.acc_shift = (a.n_acc == 4) ? 2 : 1;
   a.tmem_cols = a.n_acc * a.acc_stride;
-  // epilogue ping-pong for a single narrow N-tile (MNv2: 128 columns, +3%);
-  // wider tiles lose with it (R50 -13%, VGG -25%). launch_opts overrides.
-  a.epi_pp = (max_cols <= 128 && a.n_tiles == 1 && S.pair == 1) ? 1 : 0;
+  // epilogue ping-pong (the two warp groups alternate tiles): round 1 found it
+  // +3% for a single narrow N-tile (MNv2, 128 columns) and -13% / -25% for R50 / VGG.
+  // Round 2 (PDL, epilogue-staged bias): MNv2 0.205 -> 0.195 ms without it, so
+  // it is opt-in (launch_opts bits 1-2 = 2, WF_EPI_PP=1 at plan time).
+  a.epi_pp = 0;
   if (const int pp = (p.launch_opts >> 1) & 3) a.epi_pp = (pp == 2 && S.pair == 1) ? 1 : 0;
   a.epi_flags = static_cast<int>(epilogue);
   // Single-pass launches (every CTA gets at most one stage unit, e.g. batch 1):
@@ -459,8 +461,13 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   }
   const int kind = tf32 ? 1 : 0;
   // two N-tiles as a 2-CTA cluster sharing each A stage by multicast
-  // (AlexNet 1.08-1.15x, VGG neutral; launch_opts bit 3 turns it off)
-  const bool mc = !(p.launch_opts & 8) && (prod == 0 || prod == 3 || prod == 5) && S.pair == 1 && !tf32 &&
+  // Default: on for TMA boxes of 16-byte pieces straight from x over >= 2 H-stride
+  // residues (R50 f=16 "Cout=512": 3.86 -> 3.50 ms with it), off otherwise (VGG,
+  // stride 1: 0.322 -> 0.298 ms without it; AlexNet's core-column-plane
+  // workspace: 0.773 -> 0.766 ms without it). launch_opts bit 4 / bit 3 force on / off.
+  const bool mc_default = (prod == 0 && S.s >= 2);
+  const bool mc_on = (p.launch_opts & 16) ? true : ((p.launch_opts & 8) ? false : mc_default);
+  const bool mc = mc_on && (prod == 0 || prod == 3 || prod == 5) && S.pair == 1 && !tf32 &&
                   a.n_tiles == 2 && a.ksplit == 1 && grid % 2 == 0;
   L.cluster = 1;
   if (mc) {

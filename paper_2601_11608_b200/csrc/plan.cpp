@@ -258,7 +258,8 @@ static wf_status make_schedule_variant(const wf_conv_desc& d, int64_t f_req, int
   for (int cand : {4, 2}) {
     const bool want = (tps_req > 0) ? tps_req == cand
                                     : (env_tps ? env_tps == cand
-                                               : cand == 2 && s1.ohb >= cand && d.n * ceil_div(s1.ohb, cand) >= 4 * 148);
+                                               : cand == 2 && s1.ohb >= cand && d.n * ceil_div(s1.ohb, cand) >= 4 * 148 &&
+                                                     d.stride_h > 1);  // H stride 1 (VGG): one tile per stage measured faster
     if (!want || !(s1.prod == 0 || s1.prod >= 3) || s1.pair != 1) continue;
     Schedule s2;
     std::string e2;
@@ -1119,13 +1120,14 @@ wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Sched
 
 // Launch tuning knobs, decided once per plan (wf_fold_plan::launch_opts): the
 // launch path never reads the environment. WF_NACC=2 two accumulator
-// buffers, WF_EPI_PP=0/1 epilogue ping-pong off/on, WF_MCAST=0 no multicast
-// N-tile cluster.
+// buffers, WF_EPI_PP=0/1 epilogue ping-pong off/on, WF_MCAST=1/0 force the
+// multicast N-tile cluster on/off (default decided at launch preparation:
+// conv_fold.cu; profiles/r2t_knobs_ab.log).
 static int32_t launch_opts_from_env() {
   int32_t o = 0;
   if (const char* e = std::getenv("WF_NACC")) o |= (e[0] == '2') ? 1 : 0;
   if (const char* e = std::getenv("WF_EPI_PP")) o |= (e[0] == '1') ? (2 << 1) : (e[0] == '0' ? (1 << 1) : 0);
-  if (const char* e = std::getenv("WF_MCAST")) o |= (e[0] == '0') ? 8 : 0;
+  if (const char* e = std::getenv("WF_MCAST")) o |= (e[0] == '0') ? 8 : (e[0] == '1' ? 16 : 0);
   return o;
 }
 

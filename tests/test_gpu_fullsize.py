@@ -140,15 +140,16 @@ def test_headline_r50_b8192_bf16_every_image_exact(oracle):
     np.testing.assert_array_equal(y[-1:].float().cpu().numpy(), oracle.conv_padded(xs, ws, bs, 2, 3))
 
 
-def test_alexnet_multicast_full_batch_vs_oracle(oracle):
-    """The multicast N-tile cluster (AlexNet's default launch) on real data vs the oracle, spread images."""
+def test_alexnet_multicast_full_batch_vs_oracle(oracle, monkeypatch):
+    """The multicast N-tile cluster (opt-in WF_MCAST=1) on real data vs the oracle, spread images."""
+    monkeypatch.setenv("WF_MCAST", "1")
     rng = np.random.default_rng(96)
     n = 64
     x = torch.from_numpy(rng.uniform(-1, 1, (n, 227, 227, 3)).astype(np.float32)).cuda().bfloat16()
     w = torch.from_numpy((rng.uniform(-1, 1, (11, 11, 3, 96)) / 18).astype(np.float32)).cuda().bfloat16()
     b = torch.from_numpy(rng.uniform(-1, 1, (96,)).astype(np.float32)).cuda()
     conv = wf.FoldedConv2d(w, b, x.shape, stride=4, padding=0, dtype=torch.bfloat16)
-    assert conv.device_plan["n_tiles"] == 2 and not (conv.device_plan["launch_opts"] & 8)
+    assert conv.device_plan["n_tiles"] == 2 and (conv.device_plan["launch_opts"] & 16)
     y = conv(x).float().cpu().numpy()
     ws, bs = w.float().cpu().numpy(), b.cpu().numpy()
     for i in (0, 21, 42, 63):

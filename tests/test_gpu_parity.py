@@ -492,17 +492,21 @@ def test_reference_acceptance_sweep_on_device():
 
 @pytest.mark.parametrize("n,h,k,co,s,p", [(64, 227, 11, 96, 4, 0), (7, 227, 11, 96, 4, 0), (16, 224, 3, 64, 1, 1)])
 def test_multicast_cluster_matches_single_cta(monkeypatch, n, h, k, co, s, p):
-    """Two-N-tile plans run as a 2-CTA cluster sharing A stages by TMA multicast
-    (the default); WF_MCAST=0 forces the single-CTA launch. Bit-identical."""
+    """Two-N-tile plans can run as a 2-CTA cluster sharing A stages by TMA multicast
+    (opt-in WF_MCAST=1, read at plan time) instead of one CTA per N-tile (the
+    default, WF_MCAST=0 forces it). Bit-identical."""
     torch.manual_seed(5)
     x = torch.randn(n, h, h, 3, device="cuda").to(torch.bfloat16)
     w = (torch.randn(k, k, 3, co, device="cuda") * 0.1).to(torch.bfloat16)
     b = torch.randn(co, device="cuda")
+    monkeypatch.setenv("WF_MCAST", "1")
     conv = wf.FoldedConv2d(w, b, x.shape, stride=s, padding=p, dtype=torch.bfloat16)
-    assert conv.device_plan["n_tiles"] == 2
+    assert conv.device_plan["n_tiles"] == 2 and conv.device_plan["launch_opts"] & 16
     y_mc = conv(x)
     monkeypatch.setenv("WF_MCAST", "0")
-    y_one = conv(x)
+    conv_one = wf.FoldedConv2d(w, b, x.shape, stride=s, padding=p, dtype=torch.bfloat16)
+    assert conv_one.device_plan["launch_opts"] & 8
+    y_one = conv_one(x)
     torch.cuda.synchronize()
     assert torch.equal(y_mc, y_one)
     ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(3, 2, 0, 1), b, stride=s,

@@ -1,4 +1,4 @@
-"""Multicast 2-CTA N-tile cluster (default; WF_MCAST=0 turns it off) vs the single-CTA launch: bitwise
+"""Multicast 2-CTA N-tile cluster (opt-in WF_MCAST=1 at plan time) vs the single-CTA launch: bitwise
 output equality on plans with two N-tiles, then launch times.
 Usage: python tools/mc_check.py"""
 import os
