@@ -12,6 +12,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --cs
    python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu --no-verify --no-configs --no-variants > gpurun_out/launches_bench.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_fold -s 2 -c 1 -o gpurun_out/prof_r50_n2048 -f \
    python tools/prof_conv.py r50 2048 0 0 3 > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_fold -s 2 -c 1 -o gpurun_out/prof_vgg_b256 -f python tools/prof_conv.py vgg 256 0 0 3 > gpurun_out/ncu_full_vgg.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_fold -s 2 -c 1 -o gpurun_out/prof_alex_b512 -f \
    python tools/prof_conv.py alex 512 0 0 3 > gpurun_out/ncu_full_alex.log 2>&1
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:conv_fold -s 1 -c 1 --csv --log-file gpurun_out/traffic_r50_n8192.csv \
