@@ -183,9 +183,14 @@ wf_status wf_expand_filter_dense(const float* w, const wf_conv_desc* desc,
  * epilogue: WF_EPI_* flags; WF_EPI_BIAS needs b_rep from wf_expand_filter_pack.
  * No allocations; asynchronous on `stream` (a cudaStream_t). The kernel is
  * launched with programmatic stream serialization: its prologue (barrier
- * init, TMEM allocation) may overlap the previous kernel on the stream, and
- * every global access waits on griddepcontrol.wait, so stream order holds
- * (environment WF_PDL=0 at first use of a plan/buffer set turns it off). */
+ * init, TMEM allocation, the bulk copy of w_packed) may overlap the previous
+ * kernel on the stream; every other global access (x, workspace, b_rep, y)
+ * waits on griddepcontrol.wait, so stream order holds for them. w_packed and
+ * b_rep are read early because only wf_expand_filter_pack /
+ * wf_replicate_bias write them: the first conv launch after either call is
+ * made without the attribute. Write them any other way (a memcpy into the
+ * buffers) and synchronize the stream before the next conv. The environment
+ * variable WF_PDL=0 at first use of a plan/buffer set turns PDL off. */
 wf_status wf_conv_fold_fwd(const void* x, const void* w_packed,
                            const float* b_rep, void* y,
                            const wf_conv_desc* desc, const wf_fold_plan* plan,
