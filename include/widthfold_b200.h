@@ -185,12 +185,12 @@ wf_status wf_expand_filter_dense(const float* w, const wf_conv_desc* desc,
  * launched with programmatic stream serialization: its prologue (barrier
  * init, TMEM allocation, the bulk copy of w_packed) may overlap the previous
  * kernel on the stream; every other global access (x, workspace, b_rep, y)
- * waits on griddepcontrol.wait, so stream order holds for them. w_packed and
- * b_rep are read early because only wf_expand_filter_pack /
- * wf_replicate_bias write them: the first conv launch after either call is
- * made without the attribute. Write them any other way (a memcpy into the
- * buffers) and synchronize the stream before the next conv. The environment
- * variable WF_PDL=0 at first use of a plan/buffer set turns PDL off. */
+ * waits on griddepcontrol.wait, so stream order holds for them. w_packed is
+ * read early because only wf_expand_filter_pack writes it: the first conv
+ * launch after a pack (or a wf_replicate_bias) is made without the attribute.
+ * Write w_packed any other way (a memcpy into the buffer) and synchronize the
+ * stream before the next conv. The environment variable WF_PDL=0 at first use
+ * of a plan/buffer set turns PDL off. */
 wf_status wf_conv_fold_fwd(const void* x, const void* w_packed,
                            const float* b_rep, void* y,
                            const wf_conv_desc* desc, const wf_fold_plan* plan,
