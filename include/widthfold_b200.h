@@ -77,7 +77,13 @@ typedef enum { WF_FOLD_APPLY = 0, WF_FOLD_FALLBACK = 1 } wf_fold_status;
  * row-gather producer instead (same shared-memory image, bit-identical
  * output). Any other bit is rejected with WF_INVALID_ARGUMENT (profiling
  * switches exist only in a WFB_PROFILE=1 build of the library). */
-typedef enum { WF_EPI_NONE = 0, WF_EPI_BIAS = 1, WF_EPI_RELU = 2, WF_EPI_ROW_PRODUCER = 0x4000 } wf_epilogue;
+typedef enum {
+  WF_EPI_NONE = 0,
+  WF_EPI_BIAS = 1,
+  WF_EPI_RELU = 2,
+  WF_EPI_PREPITCHED = 4,  /* the workspace already holds x re-pitched (wf_repitch_input): skip that pass */
+  WF_EPI_ROW_PRODUCER = 0x4000
+} wf_epilogue;
 
 /* Kernel variant: the width-folded conv, or the same tcgen05 kernel on the
  * unfolded Cin=C input (explicit im2col A tiles) for the comparison. The
@@ -210,6 +216,14 @@ wf_status wf_conv_fold_fwd_ws(const void* x, void* workspace, const void* w_pack
  * (src/refconv.cpp:34-80) bit-for-bit (kh -> kw -> ci, no FMA) plus explicit
  * zero padding. The reference-semantics path for shapes/precisions the folded
  * tcgen05 kernel does not cover, and the engine of grouped_conv. */
+/* The re-pitch pass of a plan with a workspace (producer 3) on its own:
+ * writes x into workspace exactly as wf_conv_fold_fwd_ws would before its conv.
+ * With WF_EPI_PREPITCHED the conv then skips the pass, so a caller can
+ * re-pitch the next chunk of a batch on a second stream while the current
+ * chunk is convolved. No-op (WF_OK) for plans without a workspace. */
+wf_status wf_repitch_input(const void* x, void* workspace, const wf_conv_desc* desc, const wf_fold_plan* plan,
+                           void* stream);
+
 wf_status wf_conv_direct_fwd(const float* x, const float* w, float* y, const wf_conv_desc* desc, void* stream);
 
 /* Grouped exact-order fp32 conv (widthfold::grouped_conv, src/blockdiag.cpp:138-187):

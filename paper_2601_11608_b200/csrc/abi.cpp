@@ -76,7 +76,7 @@ wf_status cached_schedule(const wf_conv_desc& d, const wf_fold_plan& p, std::sha
 #define WFB_PROFILE 0
 #endif
 constexpr uint32_t kEpilogueAccepted =
-    WF_EPI_BIAS | WF_EPI_RELU | WF_EPI_ROW_PRODUCER | (WFB_PROFILE ? 0xFFFF00u : 0u);
+    WF_EPI_BIAS | WF_EPI_RELU | WF_EPI_PREPITCHED | WF_EPI_ROW_PRODUCER | (WFB_PROFILE ? 0xFFFF00u : 0u);
 
 wf_status fail(wf_status st, const std::string& msg) {
   g_last_error = msg;
@@ -206,6 +206,20 @@ wf_status wf_conv_fold_fwd(const void* x, const void* w_packed, const float* b_r
                            const wf_conv_desc* desc, const wf_fold_plan* plan, wf_dtype out_dtype, uint32_t epilogue,
                            void* stream) {
   return wf_conv_fold_fwd_ws(x, nullptr, w_packed, b_rep, y, desc, plan, out_dtype, epilogue, stream);
+}
+
+wf_status wf_repitch_input(const void* x, void* workspace, const wf_conv_desc* desc, const wf_fold_plan* plan,
+                           void* stream) {
+  if (!x || !desc || !plan) return fail(WF_INVALID_ARGUMENT, "null argument");
+  if (plan->workspace_bytes == 0 || plan->producer != 3) return WF_OK;
+  if (!workspace) return fail(WF_INVALID_ARGUMENT, "this plan needs a workspace of plan->workspace_bytes");
+  std::shared_ptr<SchedEntry> E;
+  std::string err;
+  wf_status st = cached_schedule(*desc, *plan, &E, &err);
+  if (st != WF_OK) return fail(st, err);
+  st = wfb::launch_repitch_input(E->S, *desc, x, workspace, static_cast<cudaStream_t>(stream), &err);
+  if (st != WF_OK) return fail(st, err);
+  return WF_OK;
 }
 
 wf_status wf_conv_direct_fwd(const float* x, const float* w, float* y, const wf_conv_desc* desc, void* stream) {

@@ -89,6 +89,16 @@ struct PreparedLaunch {
 
 namespace {
 
+// Core-column planes in the re-pitch workspace (the TMA boxes then read whole
+// folded-column runs of one core column instead of 16-byte pieces):
+// no-swizzle single-CTA / multicast plans whose box run fits the 256-element
+// box limit; WF_PLANES=0 turns it off. One definition for the conv launch and
+// wf_repitch_input, so both agree on the layout.
+bool repitch_planes(const Schedule& S, int es) {
+  const char* ep = std::getenv("WF_PLANES");
+  return !(ep && ep[0] == '0') && !S.sw32 && S.pair == 1 && S.plan.wbox * (16 / es) <= 256;
+}
+
 // cudaFuncAttributeMaxDynamicSharedMemorySize is per (device context,
 // function): remembered per device, under a lock.
 cudaError_t ensure_smem(const void* fn, int device, int smem) {
@@ -337,12 +347,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
     L.rp_rows = d.n * d.h;
     L.rp_in = static_cast<int>(d.w * d.c * es);
     L.rp_out = static_cast<int>(S.Wp * d.c * es);
-    // core-column planes (the TMA boxes then read whole folded-column runs of one
-    // core column instead of 16-byte pieces): no-swizzle single-CTA / multicast
-    // plans whose box run fits the 256-element box limit; WF_PLANES=0 turns it off
-    const char* ep = std::getenv("WF_PLANES");
-    const bool planes = !(ep && ep[0] == '0') && !S.sw32 && S.pair == 1 && p.wbox * (16 / es) <= 256;
-    if (planes) {
+    if (repitch_planes(S, es)) {
       L.rp_planes = S.Q;
       a.planes_e2 = 16 / es;
     }
@@ -566,7 +571,7 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
       if (cache->entries.size() > LaunchCache::kMax) cache->entries.pop_back();
     }
   }
-  if (L->repitch) {
+  if (L->repitch && !(epilogue & WF_EPI_PREPITCHED)) {
     wf_status rs =
         launch_repitch(x, const_cast<void*>(workspace), L->rp_rows, L->rp_in, L->rp_out, L->rp_planes, st, err);
     if (rs != WF_OK) return rs;
@@ -579,6 +584,18 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
     return WF_CUDA_ERROR;
   }
   return WF_OK;
+}
+
+wf_status launch_repitch_input(const Schedule& S, const wf_conv_desc& d, const void* x, void* workspace,
+                               cudaStream_t st, std::string* err) {
+  if (S.prod != 3) return WF_OK;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 15u) || (reinterpret_cast<uintptr_t>(x) & 15u)) {
+    *err = "x and the workspace must be 16-byte aligned";
+    return WF_INVALID_ARGUMENT;
+  }
+  const int es = S.esize;
+  return launch_repitch(x, workspace, d.n * d.h, static_cast<int>(d.w * d.c * es), static_cast<int>(S.Wp * d.c * es),
+                        repitch_planes(S, es) ? S.Q : 0, st, err);
 }
 
 void note_operand_write() { g_operand_epoch.fetch_add(1, std::memory_order_acq_rel); }

@@ -422,5 +422,12 @@ PYBIND11_MODULE(_core, m) {
           },
           py::arg("x"), py::arg("packed"), py::arg("b_rep"), py::arg("y"), py::arg("out_dtype"), py::arg("bias"),
           py::arg("relu"), py::arg("stream"), py::arg("extra_flags") = 0, py::arg("workspace") = 0)
+      .def(
+          "repitch",
+          [](const wf::FoldedConv& c, std::uintptr_t x, std::uintptr_t workspace, std::uintptr_t stream) {
+            py::gil_scoped_release nogil;
+            c.repitch(P(x), workspace ? P(workspace) : nullptr, P(stream));
+          },
+          py::arg("x"), py::arg("workspace"), py::arg("stream"))
       .def_property_readonly("workspace_bytes", &wf::FoldedConv::workspace_bytes);
 }

@@ -249,9 +249,14 @@ void FoldedConv::pack(const void* w, const float* b, void* packed, float* b_rep,
 void FoldedConv::forward(const void* x, const void* packed, const float* b_rep, void* y, Dtype out_dtype, bool bias,
                          bool relu, void* stream, std::uint32_t extra_flags, void* workspace) const {
   std::uint32_t epi = (bias ? static_cast<std::uint32_t>(WF_EPI_BIAS) : 0u) |
-                     (relu ? static_cast<std::uint32_t>(WF_EPI_RELU) : 0u) | (extra_flags & 0xFFFF00u);
+                     (relu ? static_cast<std::uint32_t>(WF_EPI_RELU) : 0u) |
+                     (extra_flags & (0xFFFF00u | static_cast<std::uint32_t>(WF_EPI_PREPITCHED)));
   throw_on(wf_conv_fold_fwd_ws(x, workspace, packed, bias ? b_rep : nullptr, y, &desc_, &raw_,
                                static_cast<wf_dtype>(out_dtype), epi, stream));
+}
+
+void FoldedConv::repitch(const void* x, void* workspace, void* stream) const {
+  throw_on(wf_repitch_input(x, workspace, &desc_, &raw_, stream));
 }
 
 }  // namespace widthfold

@@ -78,6 +78,9 @@ class FoldedConv {
   // y = ReLU?(conv(x) + b?) ; x in in_dtype, y in out_dtype, NHWC.
   void forward(const void* x, const void* packed, const float* b_rep, void* y, Dtype out_dtype, bool bias, bool relu,
                void* stream, std::uint32_t extra_flags = 0, void* workspace = nullptr) const;
+  // The re-pitch pass alone into `workspace` (wf_repitch_input); forward() with
+  // WF_EPI_PREPITCHED in extra_flags then skips it.
+  void repitch(const void* x, void* workspace, void* stream) const;
 
  private:
   ConvSpec spec_;

@@ -37,6 +37,9 @@ wf_status launch_conv(const Schedule& S, const wf_conv_desc& d, const void* x, c
                       const void* packed, const float* b_rep, void* y, wf_dtype out_dtype, uint32_t epilogue,
                       cudaStream_t st, int num_sms, LaunchCache* cache, std::string* err);
 int sm_count(int device);
+// The re-pitch pass of a producer-3 schedule on its own (wf_repitch_input).
+wf_status launch_repitch_input(const Schedule& S, const wf_conv_desc& d, const void* x, void* workspace,
+                               cudaStream_t st, std::string* err);
 
 // Every launch that writes a conv operand the kernel reads before its
 // griddepcontrol.wait (the packed filter, the replicated bias) bumps this

@@ -73,3 +73,23 @@ def test_with_batch_equals_fresh_plan(n_parent, n_child):
     m = min(n_parent, n_child)
     yp = parent(x[:n_parent].contiguous(), out_dtype=torch.float32)
     assert torch.equal(yc[:m], yp[:m])
+
+
+def test_repitch_input_then_prepitched_conv_equals_one_call():
+    """wf_repitch_input + WF_EPI_PREPITCHED (the re-pitch pass split from the conv) == the single call,
+    bitwise, on AlexNet rows; and on a plan without a workspace the split pass is a no-op."""
+    x, w, b = _int_case(16, 227, 11, 96, torch.bfloat16, seed=99)
+    conv = wf.FoldedConv2d(w, b, x.shape, stride=4, padding=0, dtype=torch.bfloat16)
+    assert conv.device_plan["producer"] == "repitch+tma" and conv.workspace is not None
+    ref = conv(x, out_dtype=torch.float32)
+    y = torch.full_like(ref, float("nan"))
+    st = torch.cuda.current_stream().cuda_stream
+    conv.workspace.zero_()
+    conv.core.repitch(x.data_ptr(), conv.workspace.data_ptr(), st)
+    conv._forward(x, out=y, out_dtype=torch.float32, flags=4)  # WF_EPI_PREPITCHED
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)
+    x2, w2, b2 = _int_case(2, 64, 7, 64, torch.bfloat16, seed=5)
+    c2 = wf.FoldedConv2d(w2, b2, x2.shape, stride=2, padding=3, dtype=torch.bfloat16)
+    assert c2.workspace is None
+    c2.core.repitch(x2.data_ptr(), 0, st)  # no workspace: nothing to do
