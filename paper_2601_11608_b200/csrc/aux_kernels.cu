@@ -114,17 +114,12 @@ __device__ __forceinline__ void repitch_store_any(const RowChunks& rc, uint8_t* 
   }
 }
 
-// Two rows per warp in flight (grid-stride pairs of rows). Plane layout with
-// `staged`: each warp assembles its two output rows in shared memory (the
-// chunks land at their plane positions) and then writes each row with
-// contiguous, fully coalesced 16-byte stores.
+// Two rows per warp in flight (grid-stride pairs of rows). (Assembling the plane
+// layout's rows in shared memory to store them contiguously measured slower
+// than these scattered 16-byte stores: AlexNet b512 73 vs 61 us.)
 __global__ void __launch_bounds__(256) repitch_kernel(const uint8_t* __restrict__ x, uint8_t* __restrict__ y,
-                                                      long long rows, int rb_in, int rb_out, int Q, int plane_bytes,
-                                                      int staged) {
-  extern __shared__ __align__(16) uint8_t rowbuf[];
+                                                      long long rows, int rb_in, int rb_out, int Q, int plane_bytes) {
   const int lane = threadIdx.x & 31;
-  uint8_t* const sb1 = rowbuf + (threadIdx.x >> 5) * 2 * rb_out;
-  uint8_t* const sb2 = sb1 + rb_out;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const int cpr = rb_out >> 4;
   for (long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows;
@@ -137,22 +132,14 @@ __global__ void __launch_bounds__(256) repitch_kernel(const uint8_t* __restrict_
     const uint4* a2 = reinterpret_cast<const uint4*>(src2 & ~static_cast<uintptr_t>(15));
     const int sh = static_cast<int>(src & 15u), sh2 = static_cast<int>(src2 & 15u);
     const int nin = (sh + rb_in + 15) >> 4, nin2 = (sh2 + rb_in + 15) >> 4;  // aligned chunks holding the row
-    uint8_t* const d1 = staged ? sb1 : y + r * rb_out;
-    uint8_t* const d2 = staged ? sb2 : y + r2 * rb_out;
+    uint8_t* const d1 = y + r * rb_out;
+    uint8_t* const d2 = y + r2 * rb_out;
     for (int s0 = 0; s0 < cpr; s0 += 32 * kRepitchRounds) {
       RowChunks c1, c2;
       repitch_load(a0, s0, nin, lane, true, c1);
       repitch_load(a2, s0, nin2, lane, has2, c2);
       repitch_store_any(c1, d1, s0, cpr, rb_in, sh, lane, Q, plane_bytes);
       if (has2) repitch_store_any(c2, d2, s0, cpr, rb_in, sh2, lane, Q, plane_bytes);
-    }
-    if (staged) {
-      __syncwarp();
-      for (int c = lane; c < cpr; c += 32) {
-        reinterpret_cast<uint4*>(y + r * rb_out)[c] = reinterpret_cast<const uint4*>(sb1)[c];
-        if (has2) reinterpret_cast<uint4*>(y + r2 * rb_out)[c] = reinterpret_cast<const uint4*>(sb2)[c];
-      }
-      __syncwarp();
     }
   }
 }
@@ -161,12 +148,8 @@ wf_status launch_repitch(const void* x, void* ws, long long rows, int rb_in, int
                          cudaStream_t st, std::string* err) {
   const int threads = 256;  // 8 warps, one row each at a time
   const int blocks = static_cast<int>(std::min<long long>((rows + 7) / 8, 148LL * 8));
-  // staging the plane layout's rows in shared memory (coalesced row stores) measured slower than the
-  // direct scattered 16-byte stores (AlexNet b512: 73 vs 61 us); kept off
-  const int staged = 0;
-  repitch_kernel<<<blocks, threads, staged ? 16 * rb_out : 0, st>>>(
-      static_cast<const uint8_t*>(x), static_cast<uint8_t*>(ws), rows, rb_in, rb_out, planes,
-      planes > 0 ? rb_out / planes : 0, staged);
+  repitch_kernel<<<blocks, threads, 0, st>>>(static_cast<const uint8_t*>(x), static_cast<uint8_t*>(ws), rows, rb_in,
+                                             rb_out, planes, planes > 0 ? rb_out / planes : 0);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("repitch_kernel: ") + cudaGetErrorString(e);
