@@ -13,7 +13,18 @@ from paper_2601_11608_b200 import _core  # noqa: E402
 
 N = 2048
 USEFUL = 2 * N * 112 * 112 * 64 * 7 * 7 * 3  # R50 conv1, count_macs x 2
-PEAK_GBS, PEAK_TF = 6650.0, 1590.0           # B200_PROFILING.md fallback (MEASURED_PEAKS.json absent here)
+def _peaks():
+    """MEASURED_PEAKS.json (driver-written), else the B200_PROFILING.md fallback, labelled."""
+    import json
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "MEASURED_PEAKS.json"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+PEAK_GBS, PEAK_TF, PEAK_SRC = _peaks()
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
            "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed",
@@ -41,7 +52,8 @@ def main(tag):
     }
     lines = ["# R50 conv1, n=2048, bf16: three variants of the same tcgen05 kernel (ncu --set full, one launch)", "",
              "ncu times are cold-cache, serialised, one launch under the profiler (clock-control none).", "",
-             "| variant | time ms | DRAM read+write GB | DRAM GB/s (frac of 6650) | tensor pipe % | TC smem wavefronts % | useful TFLOP/s | issued TFLOP/s | useful/issued | instructions |",
+             f"Peaks: HBM {PEAK_GBS:.1f} GB/s, bf16 {PEAK_TF:.1f} TF/s ({PEAK_SRC}).", "",
+             f"| variant | time ms | DRAM read+write GB | DRAM GB/s (frac of {PEAK_GBS:.0f}) | tensor pipe % | TC smem wavefronts % | useful TFLOP/s (frac of {PEAK_TF:.0f}) | issued TFLOP/s | useful/issued | instructions |",
              "|---|---|---|---|---|---|---|---|---|---|"]
     for v in ("fold", "zeropad", "unfolded"):
         rep = os.path.join(ROOT, "gpurun_out", f"prof_var_{v}.ncu-rep")
@@ -55,7 +67,7 @@ def main(tag):
         tp = val.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "n/a")
         tcw = val.get("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "n/a")
         lines.append(f"| {v} | {t * 1e3:.3f} | {by / 1e9:.2f} | {by / t / 1e9:.0f} ({by / t / 1e9 / PEAK_GBS:.2f}) | {tp} | "
-                     f"{tcw} | {USEFUL / t / 1e12:.0f} | {issued / t / 1e12:.0f} | {USEFUL / issued:.3f} | "
+                     f"{tcw} | {USEFUL / t / 1e12:.0f} ({USEFUL / t / 1e12 / PEAK_TF:.3f}) | {issued / t / 1e12:.0f} | {USEFUL / issued:.3f} | "
                      f"{val.get('smsp__inst_executed.sum', 'n/a')} |")
     out = os.path.join(ROOT, "profiles", f"{tag}_ncu_variants.md")
     open(out, "w").write("\n".join(lines) + "\n")
