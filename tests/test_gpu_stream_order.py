@@ -102,3 +102,35 @@ def test_repack_then_forward_sees_the_new_filter():
     torch.cuda.synchronize()
     for i, (k, o) in enumerate(outs):
         assert torch.equal(o, refs[k]), f"launch {i}: not the filter packed just before it"
+
+
+def test_graph_captured_chain_keeps_order():
+    """A CUDA graph capturing [copy x_i -> conv -> checksum of y] for several inputs: the conv nodes carry
+    programmatic edges (PDL) and must still see each copy and be seen by each checksum."""
+    dt = torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(21)
+    xs = [(torch.rand((2, 224, 224, 3), generator=g, device="cuda") * 2 - 1).to(dt) for _ in range(4)]
+    wt = ((torch.rand((7, 7, 3, 64), generator=g, device="cuda") * 2 - 1) / 12).to(dt)
+    b = torch.rand(64, generator=g, device="cuda") * 2 - 1
+    conv = wf.FoldedConv2d(wt, b, xs[0].shape, stride=2, padding=3, dtype=dt)
+    refs = [_isolated(conv, x).double().sum() for x in xs]
+    x = torch.empty_like(xs[0])
+    y = conv(xs[0])
+    sums = torch.zeros(len(xs), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            for i, xi in enumerate(xs):
+                x.copy_(xi)
+                conv(x, out=y)
+                sums[i] = y.double().sum()
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(3):
+        sums.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        for i, r in enumerate(refs):
+            assert sums[i].item() == r.item(), f"graph replay: input {i} checksum differs"
