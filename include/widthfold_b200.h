@@ -220,7 +220,8 @@ wf_status wf_conv_fold_fwd_ws(const void* x, void* workspace, const void* w_pack
  * writes x into workspace exactly as wf_conv_fold_fwd_ws would before its conv.
  * With WF_EPI_PREPITCHED the conv then skips the pass, so a caller can
  * re-pitch the next chunk of a batch on a second stream while the current
- * chunk is convolved. No-op (WF_OK) for plans without a workspace. */
+ * chunk is convolved. No-op (WF_OK) unless the plan re-pitches its input
+ * (plan->producer == 3); WF_EPI_PREPITCHED is ignored by other plans. */
 wf_status wf_repitch_input(const void* x, void* workspace, const wf_conv_desc* desc, const wf_fold_plan* plan,
                            void* stream);
 
