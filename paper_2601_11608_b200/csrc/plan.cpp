@@ -611,14 +611,22 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // tools/probes/sw32_probe.cu). Otherwise the canonical no-swizzle layout of
   // 16-byte core columns ([q][row][folded col][16 B], + the shift region).
   S.sw32 = !S.kpair && !S.need_shift && Q >= 2 && in_dtype != WF_TF32;
-  if (S.sw32 && (S.prod == 4 || S.prod == 5 || S.prod == 6)) S.prod = 3;  // the gather warps / ring maps: no-swizzle layout only
+  S.qs.clear();
   if (S.sw32) {
-    S.qs.clear();
     for (int64_t g = 0; g < G; ++g)
       for (int64_t st : U[g])
         if (std::find(S.qs.begin(), S.qs.end(), static_cast<int>(st % Q)) == S.qs.end())
           S.qs.push_back(static_cast<int>(st % Q));
     std::sort(S.qs.begin(), S.qs.end());
+    // the launch holds at most 4 region coordinates (ConvArgs::qcoord): wider
+    // pixels (e.g. stride 3 -> f = 24, 9 core columns) keep the no-swizzle layout
+    if (S.qs.size() > 4) {
+      S.sw32 = false;
+      S.qs.clear();
+    }
+  }
+  if (S.sw32 && (S.prod == 4 || S.prod == 5 || S.prod == 6)) S.prod = 3;  // the gather warps / ring maps: no-swizzle layout only
+  if (S.sw32) {
     S.lbo_a = 16;  // unused by SWIZZLE_32B K-major descriptors
     S.qregion_bytes = static_cast<int>((NR * Wbox * 32 + 1023) / 1024 * 1024);
     S.region_bytes = static_cast<int>(S.qs.size()) * S.qregion_bytes;
