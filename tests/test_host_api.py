@@ -165,3 +165,12 @@ def test_auto_schedule_choices_for_the_bench_workloads(monkeypatch):
     # batch 1: one output group per N-tile (more CTAs for a latency-bound launch)
     p = A.plan_fold(A.make_desc(1, 224, 224, 3, 7, 7, 64, 2, 2, 3, 3), 0, 0, A.WF_TF32).as_dict()
     assert p["n_tiles"] == 2 and p["stage_tiles"] == 1
+
+
+def test_wide_pixel_covers_keep_the_no_swizzle_layout():
+    """Stride 3 forces f = 24 (9 core columns per folded pixel); a 32-byte-cover schedule would need more
+    SWIZZLE_32B regions than a launch holds (4), so the planner keeps the no-swizzle layout (found by
+    tests/test_gpu_fuzz.py: the launch used to fail with 'too many SWIZZLE_32B regions')."""
+    from paper_2601_11608_b200 import _abi as A
+    d = A.schedule_describe(A.make_desc(2, 33, 24, 3, 1, 1, 64, 3, 3, 0, 0), 0, 0, A.WF_BF16)
+    assert d["f"] == 24 and d["Q"] == 9 and d["sw32"] == 0
