@@ -92,7 +92,7 @@ struct PMma {
 // (kh+1, c)); the odd ones out are matched by a min-cost DP over their runs'
 // hulls, a last single one pairs with a zero (mask 0) neighbour column.
 std::vector<PMma> build_kpair(const std::vector<int>& ord, const std::vector<int64_t>& lo,
-                              const std::vector<int64_t>& hi, int KH, int Ng) {
+                              const std::vector<int64_t>& hi, int KH, int Ng, int64_t max_col) {
   const int ns = static_cast<int>(ord.size());
   int64_t cmin = INT64_MAX, cmax = -1;
   for (int g : ord) { cmin = std::min(cmin, lo[g]); cmax = std::max(cmax, hi[g]); }
@@ -164,8 +164,12 @@ std::vector<PMma> build_kpair(const std::vector<int>& ord, const std::vector<int
   }
   for (const auto& pr : match) {
     const Left& x = left[pr.first];
-    if (pr.second < 0) {  // partner: a neighbouring core column of the same row (finite data), B zero
-      const int c2 = x.c > 0 ? x.c - 1 : x.c + 1;
+    if (pr.second < 0) {
+      // partner: a neighbouring core column of the same window row (loaded,
+      // finite data) with zero B rows; a one-column window row pairs the
+      // column with itself (LBO 0) -- a column outside the window could read
+      // past the loaded A rows, and 0 * NaN from unloaded shared memory is NaN
+      const int c2 = x.c > 0 ? x.c - 1 : (x.c + 1 <= max_col ? x.c + 1 : x.c);
       out.push_back({x.run.s0, x.run.len, {x.kh, x.kh}, {x.c, c2}, {(1u << x.run.len) - 1u, 0u}});
       continue;
     }
@@ -548,7 +552,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   // measured-cycle cost model says it is cheaper (WF_KPAIR=0/1 forces it).
   const int64_t KHn = d.kh;
   auto kpair_mmas = [&](const std::vector<int>& ord) {  // ord: slot -> group
-    return build_kpair(ord, lo, hi, static_cast<int>(KHn), S.Ng);
+    return build_kpair(ord, lo, hi, static_cast<int>(KHn), S.Ng, max_col);
   };
   auto kpair_cost = [&](const std::vector<int>& ord) {
     int64_t c = 0;

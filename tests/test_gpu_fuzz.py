@@ -133,3 +133,27 @@ def test_random_geometry_and_knobs_exact(case, monkeypatch):
     bad = (y.double() != ref)
     assert not bad.any(), (f"{int(bad.sum())} of {bad.numel()} outputs differ with {KNOBS[knob]}; plan "
                            f"{ {key: conv.device_plan[key] for key in ('f', 'r', 'group_size', 'n_tiles', 'producer', 'kstep_mode', 'stage_tiles', 'wbox')} }")
+
+
+TOL = {"bf16": 1e-2, "f16": 1e-2, "tf32": 1e-3}
+
+
+@pytest.mark.parametrize("case", CASES[:48], ids=[f"real_n{c[0]}_{c[1]}x{c[2]}x{c[3]}_k{c[4]}s{c[5]}p{c[6]}_co{c[7]}_{c[8]}"
+                                                  f"_{c[10]}" for c in CASES[:48]])
+def test_random_geometry_real_data_within_tolerance(case):
+    """Real-valued data: normwise max|y - ref| / max|ref| within the north-star tolerance (bf16/fp16 1e-2,
+    TF32 1e-3) of a float64 conv of the same (device-representable) inputs."""
+    n, h, w, c, k, s, p, co, dt, relu, variant = case
+    g = torch.Generator(device="cuda").manual_seed(zlib.crc32(repr(case).encode()) ^ 0x5A5A)
+    tdt = TDT[dt]
+    x = (torch.rand((n, h, w, c), generator=g, device="cuda") * 2 - 1).to(tdt)
+    wt = ((torch.rand((k, k, c, co), generator=g, device="cuda") * 2 - 1) / (k * k * c) ** 0.5).to(tdt)
+    b = torch.rand((co,), generator=g, device="cuda") * 2 - 1
+    try:
+        conv = wf.FoldedConv2d(wt, b, x.shape, stride=s, padding=p, dtype=tdt, variant=variant)
+    except wf.UnsupportedError as e:
+        pytest.skip(f"fold not applicable: {e}")
+    y = conv(x, relu=relu, out_dtype=torch.float32).double()
+    ref = _f64(x, wt, b, s, p, relu)
+    err = ((y - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
+    assert err <= TOL[dt], f"normwise rel err {err:.3e} > {TOL[dt]}"

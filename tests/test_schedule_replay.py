@@ -180,3 +180,22 @@ def test_schedule_replay_random_geometries(oracle, geom):
     x = rng.integers(-3, 4, (N, Hh, Ww, 3)).astype(np.float32)
     w = rng.integers(-3, 4, (KH, KW, 3, Co)).astype(np.float32)
     replay(oracle, x, w, s, p, dt)
+
+
+@pytest.mark.parametrize("geom", [(1, 1, 64, 1, 0, 47, 32, 4, "bf16"), (1, 1, 32, 1, 0, 12, 16, 8, "f16"),
+                                  (3, 3, 64, 1, 1, 20, 16, 8, "bf16"), (5, 5, 96, 2, 2, 24, 32, 4, "bf16"),
+                                  (1, 1, 64, 2, 0, 16, 32, 2, "tf32"), (3, 3, 32, 1, 1, 14, 24, 2, "bf16")],
+                         ids=lambda g: "k{}s{}p{}c{}C{}{}".format(g[0], g[3], g[4], g[2], g[7], g[8]))
+def test_schedule_replay_other_channel_counts(oracle, geom):
+    """Cin != 3, including one-core-column window rows (a 1x1 conv on 16-byte folded pixels): every MMA
+    of a valid output row reads only loaded A (the replay marks unloaded bytes NaN; a zero-B partner
+    column outside the window used to read past the stage -- found by the real-data GPU fuzz)."""
+    KH, KW, Co, s, p, H, W, C, dt = geom
+    d = A.make_desc(1, H, W, C, KH, KW, Co, s, s, p, p)
+    plan = A.plan_fold(d, 0, 0, DT[dt])
+    if plan.status != A.WF_FOLD_APPLY:
+        pytest.skip(f"fold falls back: {A.REASONS[plan.reason]}")
+    rng = np.random.default_rng(KH * 100 + W + C)
+    x = rng.integers(-3, 4, (1, H, W, C)).astype(np.float32)
+    w = rng.integers(-3, 4, (KH, KW, C, Co)).astype(np.float32)
+    replay(oracle, x, w, s, p, dt)
