@@ -157,3 +157,30 @@ def test_random_geometry_real_data_within_tolerance(case):
     ref = _f64(x, wt, b, s, p, relu)
     err = ((y - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
     assert err <= TOL[dt], f"normwise rel err {err:.3e} > {TOL[dt]}"
+
+
+@pytest.mark.parametrize("case", CASES2[:64], ids=[f"real_n{c[0]}_{c[1]}x{c[2]}x{c[3]}_k{c[4]}x{c[5]}_s{c[6]}x{c[7]}"
+                                                   f"_p{c[8]}x{c[9]}_co{c[10]}_{c[11]}_knob{c[13]}" for c in CASES2[:64]])
+def test_random_geometry_and_knobs_real_data(case, monkeypatch):
+    """Real-valued data through the knob set: within tolerance and free of NaN (a schedule that read
+    unloaded shared memory would multiply garbage by zero filter taps and could produce NaN)."""
+    n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, relu, knob = case
+    for key, val in KNOBS[knob].items():
+        monkeypatch.setenv(key, val)
+    g = torch.Generator(device="cuda").manual_seed(zlib.crc32(repr(case).encode()) ^ 0xA5A5)
+    tdt = TDT[dt]
+    x = (torch.rand((n, h, w, c), generator=g, device="cuda") * 2 - 1).to(tdt)
+    wt = ((torch.rand((kh, kw, c, co), generator=g, device="cuda") * 2 - 1) / (kh * kw * c) ** 0.5).to(tdt)
+    b = torch.rand((co,), generator=g, device="cuda") * 2 - 1
+    try:
+        conv = wf.FoldedConv2d(wt, b, x.shape, stride=(sh, sw), padding=(ph, pw), dtype=tdt)
+    except wf.UnsupportedError as e:
+        pytest.skip(f"fold not applicable: {e}")
+    y = conv(x, relu=relu, out_dtype=torch.float32).double()
+    ref = torch.nn.functional.conv2d(x.double().permute(0, 3, 1, 2), wt.double().permute(3, 2, 0, 1), b.double(),
+                                     stride=(sh, sw), padding=(ph, pw)).permute(0, 2, 3, 1)
+    if relu:
+        ref = torch.relu(ref)
+    assert torch.isfinite(y).all()
+    err = ((y - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
+    assert err <= TOL[dt], f"normwise rel err {err:.3e} > {TOL[dt]} with {KNOBS[knob]}"
