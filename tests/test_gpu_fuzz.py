@@ -184,3 +184,44 @@ def test_random_geometry_and_knobs_real_data(case, monkeypatch):
     assert torch.isfinite(y).all()
     err = ((y - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
     assert err <= TOL[dt], f"normwise rel err {err:.3e} > {TOL[dt]} with {KNOBS[knob]}"
+
+
+def _cases3(count=40, seed=31337):
+    """Larger batches of small images: many tiles per CTA (A-stage ring, accumulator buffers and barrier
+    phases wrap many times) for unusual plans."""
+    rng = random.Random(seed)
+    out = []
+    while len(out) < count:
+        n, h, w = rng.randint(64, 320), rng.randint(6, 40), rng.randint(6, 64)
+        c, k, s = rng.choice([1, 2, 3, 4]), rng.choice([1, 3, 5, 7]), rng.randint(1, 3)
+        p = rng.randint(0, k // 2)
+        co, dt = rng.choice([32, 64, 96, 128, 192]), rng.choice(["bf16", "f16", "tf32"])
+        if (h + 2 * p - k) // s + 1 < 1 or (w + 2 * p - k) // s + 1 < 1:
+            continue
+        out.append((n, h, w, c, k, s, p, co, dt, rng.random() < 0.3, rng.randrange(len(KNOBS))))
+    return out
+
+
+CASES3 = _cases3()
+
+
+@pytest.mark.parametrize("case", CASES3, ids=[f"n{c[0]}_{c[1]}x{c[2]}x{c[3]}_k{c[4]}s{c[5]}p{c[6]}_co{c[7]}_{c[8]}"
+                                               f"_knob{c[10]}" for c in CASES3])
+def test_random_steady_state_exact(case, monkeypatch):
+    n, h, w, c, k, s, p, co, dt, relu, knob = case
+    for key, val in KNOBS[knob].items():
+        monkeypatch.setenv(key, val)
+    g = torch.Generator(device="cuda").manual_seed(zlib.crc32(repr(case).encode()))
+    tdt = TDT[dt]
+    x = torch.randint(-3, 4, (n, h, w, c), generator=g, device="cuda").to(tdt)
+    wt = torch.randint(-3, 4, (k, k, c, co), generator=g, device="cuda").to(tdt)
+    b = torch.randint(-8, 9, (co,), generator=g, device="cuda").float()
+    try:
+        conv = wf.FoldedConv2d(wt, b, x.shape, stride=s, padding=p, dtype=tdt)
+    except wf.UnsupportedError as e:
+        pytest.skip(f"fold not applicable: {e}")
+    y = conv(x, relu=relu, out_dtype=torch.float32)
+    ref = _f64(x, wt, b, s, p, relu)
+    bad = (y.double() != ref).reshape(n, -1).any(dim=1)
+    assert not bad.any(), (f"images {bad.nonzero().flatten().tolist()[:8]} differ with {KNOBS[knob]}; plan "
+                           f"{ {key: conv.device_plan[key] for key in ('f', 'r', 'n_tiles', 'producer', 'kstep_mode', 'stage_tiles', 'wbox')} }")
