@@ -153,10 +153,13 @@ def test_random_geometry_real_data_within_tolerance(case):
         conv = wf.FoldedConv2d(wt, b, x.shape, stride=s, padding=p, dtype=tdt, variant=variant)
     except wf.UnsupportedError as e:
         pytest.skip(f"fold not applicable: {e}")
-    y = conv(x, relu=relu, out_dtype=torch.float32).double()
+    # every output type the epilogue writes (bf16 / fp16 rounding counts against the tolerance)
+    odt = (torch.float32, torch.bfloat16, torch.float16)[zlib.crc32(repr(case).encode()) % 3]
+    y = conv(x, relu=relu, out_dtype=odt).double()
     ref = _f64(x, wt, b, s, p, relu)
     err = ((y - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
-    assert err <= TOL[dt], f"normwise rel err {err:.3e} > {TOL[dt]}"
+    tol = TOL[dt] if odt == torch.float32 else 1e-2
+    assert err <= tol, f"normwise rel err {err:.3e} > {tol} (out {odt})"
 
 
 @pytest.mark.parametrize("case", CASES2[:64], ids=[f"real_n{c[0]}_{c[1]}x{c[2]}x{c[3]}_k{c[4]}x{c[5]}_s{c[6]}x{c[7]}"
