@@ -22,6 +22,7 @@ WF_F32, WF_TF32, WF_BF16, WF_F16 = 0, 1, 2, 3
 WF_FOLD_APPLY, WF_FOLD_FALLBACK = 0, 1
 # wf_epilogue
 WF_EPI_NONE, WF_EPI_BIAS, WF_EPI_RELU = 0, 1, 2
+WF_EPI_PREPITCHED = 4  # the workspace already holds x re-pitched (wf_repitch_input)
 WF_EPI_ROW_PRODUCER = 0x4000  # cross-check: the row-gather producer builds the TMA A layout
 
 # FoldReason strings, same order as include/widthfold/fold.hpp:14-23 and
@@ -34,7 +35,7 @@ REASONS = [
 EXPORTED = [
     "wf_plan_fold", "wf_plan_unfolded", "wf_packed_filter_bytes", "wf_expand_filter_pack", "wf_expand_filter_dense",
     "wf_conv_fold_fwd", "wf_conv_fold_fwd_ws", "wf_set_num_sms", "wf_last_error", "wf_abi_version",
-    "wf_schedule_describe", "wf_cast_f32", "wf_conv_grouped_fwd",
+    "wf_schedule_describe", "wf_cast_f32", "wf_conv_grouped_fwd", "wf_repitch_input",
 ]
 
 
@@ -100,6 +101,8 @@ def lib() -> ctypes.CDLL:
         L.wf_conv_fold_fwd_ws.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(ConvDesc),
                                           POINTER(FoldPlan), c_int, c_uint32, c_void_p]
         L.wf_conv_fold_fwd_ws.restype = c_int
+        L.wf_repitch_input.argtypes = [c_void_p, c_void_p, POINTER(ConvDesc), POINTER(FoldPlan), c_void_p]
+        L.wf_repitch_input.restype = c_int
         L.wf_set_num_sms.argtypes = [c_int]
         L.wf_set_num_sms.restype = None
         L.wf_last_error.argtypes = []
