@@ -442,10 +442,15 @@ def run_gpu(args) -> None:
     rank, local, world = shard.dist_env()
     if world != args.gpus:
         raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus} (launch N ranks for N GPUs)")
+    # WF_BENCH_SHARE_GPU=1 (launcher check on a box with fewer GPUs than ranks): ranks share the GPUs
+    # round-robin and the scalars travel over gloo -- the numbers are then NOT a scaling measurement
+    shared = os.environ.get("WF_BENCH_SHARE_GPU") == "1" and world > torch.cuda.device_count()
+    local = local % torch.cuda.device_count() if shared else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    coll = "cpu" if shared else dev  # where the (verification / timing) collectives' tensors live
     if world > 1:
-        shard.init("nccl")
+        shard.init("gloo" if shared else "nccl")
     if args.weak:   # N_IMG images per rank
         lo, hi = rank * N_IMG, (rank + 1) * N_IMG
         total = N_IMG * world
@@ -486,7 +491,7 @@ def run_gpu(args) -> None:
         ev1.record(stream)
         barrier()
     ms_local = ev0.elapsed_time(ev1)
-    ms_total = shard.max_over_ranks(ms_local, dev)
+    ms_total = shard.max_over_ranks(ms_local, coll)
     ms_step = ms_total / args.steps
     value = total / (ms_step / 1e3)
     clocks = clk.summary()
@@ -498,7 +503,7 @@ def run_gpu(args) -> None:
         orc = _oracle()
         idxs = sorted({0, n // 2, n - 1}) if n else []
         errs = _verify_images(conv, x, y, wt, bias, STRIDE, PAD, False, idxs, orc)
-        per_rank = shard.gather_scalars([float(lo), float(max(errs) if errs else 0.0), float(len(errs))], dev)
+        per_rank = shard.gather_scalars([float(lo), float(max(errs) if errs else 0.0), float(len(errs))], coll)
         verify = {"images_per_rank": "first, middle, last image of each shard",
                   "max_rel_err": max(r[1] for r in per_rank), "tol": VERIFY_TOL,
                   "images_checked": int(sum(r[2] for r in per_rank)),
@@ -511,7 +516,7 @@ def run_gpu(args) -> None:
         xw = (torch.rand((N_IMG, H, W, C), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
         cw = conv.with_batch(N_IMG)
         yw = torch.empty(cw.output_shape, dtype=torch.bfloat16, device=dev)
-        wms = shard.max_over_ranks(_timed(lambda: cw(xw, out=yw), args.steps, warm, stream, barrier), dev)
+        wms = shard.max_over_ranks(_timed(lambda: cw(xw, out=yw), args.steps, warm, stream, barrier), coll)
         weak = {"images_per_rank": N_IMG, "global_batch": N_IMG * world, "ms_per_step": wms,
                 "value": N_IMG * world / (wms / 1e3), "unit": "images/s"}
         del xw, yw, cw
@@ -527,12 +532,12 @@ def run_gpu(args) -> None:
         wz[:, :, :C] = wt
         convz = wf.FoldedConv2d(wz, bias, xz.shape, stride=STRIDE, padding=PAD, dtype=torch.bfloat16)
         zms = shard.max_over_ranks(_timed(lambda: convz(xz, out=y), max(5, args.steps // 4), 3, stream, barrier),
-                                   dev)
+                                   coll)
         del xz, wz
         convu = wf.FoldedConv2d(wt, bias, x.shape, stride=STRIDE, padding=PAD, dtype=torch.bfloat16,
                                 variant="unfolded")
         ums = shard.max_over_ranks(_timed(lambda: convu(x, out=y), max(3, args.steps // 20), 2, stream, barrier),
-                                   dev)
+                                   coll)
         for name, ms_, c_, inb in (("fold", ms_step, conv, IN_BYTES_PER_IMG),
                                    ("zeropad_cin8", zms, convz, IN_BYTES_PER_IMG * 8 // 3),
                                    ("unfolded_cin3", ums, convu, IN_BYTES_PER_IMG)):
@@ -570,7 +575,7 @@ def run_gpu(args) -> None:
         barrier()
         es = max(1, min(args.steps, args.e2e_steps))
         ems = shard.max_over_ranks(
-            _timed(lambda: conv.run_host(xh, yh, chunk=args.e2e_chunk), es, 0, stream, barrier), dev)
+            _timed(lambda: conv.run_host(xh, yh, chunk=args.e2e_chunk), es, 0, stream, barrier), coll)
         e2e = {"value": ne * world / (ems / 1e3), "unit": "images/s", "h2d_bytes_per_step": xh.numel() * 2 * world,
                "d2h_bytes_per_step": yh.numel() * 2 * world, "ms_per_step": ems, "steps": es,
                "images_per_rank": ne,
@@ -635,6 +640,8 @@ def run_gpu(args) -> None:
         "config": {"workload": WORKLOAD, "global_batch": total, "per_gpu_batch": n, "image": [H, W, C],
                    "filter": [K, K, C, COUT], "stride": STRIDE, "padding": PAD, "epilogue": "bias",
                    "fold_factor": conv.device_plan["f"], "parallelism": f"batch-shard{world}",
+                   **({"shared_gpu": f"{world} ranks on {torch.cuda.device_count()} GPU(s): launcher check, "
+                                     "not a scaling measurement"} if shared else {}),
                    "l2": "no flush: per-step input 2.47 GB/N and output 13.15 GB/N exceed the 126 MB L2"},
         "useful_tflops": useful_tf,
         "tensor_roofline_frac": useful_tf / world / peaks["bf16_tflops"],
