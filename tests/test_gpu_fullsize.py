@@ -347,3 +347,23 @@ def test_gather_producer_bitwise_vs_repitch(monkeypatch, n, h, w, k, co, s, p, d
     assert torch.equal(y, ref_conv(x, out_dtype=torch.float32))
     ref = conv_f64(x, wt, b, s, p)
     assert torch.equal(y.double(), ref)
+
+
+@pytest.mark.parametrize("geom", [
+    # n, H, W, K, Cout, stride, pad  (large images: 64-bit offsets, many tiles per image)
+    (1, 1024, 1024, 7, 64, 2, 3),
+    (2, 1536, 960, 3, 64, 1, 1),
+    (80, 1024, 1024, 7, 64, 2, 3),   # 2.7 GB of bf16 output: byte offsets past 2^31
+])
+def test_large_images_exact(geom):
+    """Large images and a > 1 GB output: values in {-1, 0, 1} keep every output an exact bf16 integer."""
+    n, H, W, K, Co, s, p = geom
+    g = torch.Generator(device="cuda").manual_seed(H + W + n)
+    x = torch.randint(-1, 2, (n, H, W, 3), generator=g, device="cuda").bfloat16()
+    w = torch.randint(-1, 2, (K, K, 3, Co), generator=g, device="cuda").bfloat16()
+    b = torch.randint(-2, 3, (Co,), generator=g, device="cuda").float()
+    conv = wf.FoldedConv2d(w, b, x.shape, stride=s, padding=p, dtype=torch.bfloat16)
+    y = conv(x)
+    for lo in range(0, n, 4):
+        ref = conv_f64(x[lo:lo + 4], w, b, s, p)
+        assert torch.equal(y[lo:lo + 4].double(), ref), f"images {lo}..{lo + 3} differ"
