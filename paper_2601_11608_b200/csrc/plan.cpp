@@ -312,7 +312,10 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     const int64_t base = std::lcm<int64_t>(base_align, sw);
     wf_fold_plan first{};
     bool have = false;
-    for (int64_t cand = base; cand <= d.w; cand += base) {
+    // no factor past 255 core columns per folded pixel can plan (the Q + 1 <= 256
+    // limit below), so the search is bounded whatever W is
+    const int64_t f_max = std::min<int64_t>(d.w, 255 * 16 / std::max<int64_t>(pix, 1));
+    for (int64_t cand = base; cand <= f_max; cand += base) {
       Schedule tmp;
       std::string e2;
       wf_status s2 = make_schedule(d, cand, gs_req, in_dtype, &tmp, &e2, kpair_req, pair_req);
