@@ -437,6 +437,22 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   }
   const int64_t G = r / gs;
   S.Ng = static_cast<int>(gs * d.cout);
+  // Two A stages must fit in shared memory even with no B operand and the smallest
+  // region layout (SWIZZLE_32B with one core-column offset, 16-bit inputs only);
+  // otherwise the N-tiling below fails for every budget -- decided here, before the
+  // K-step searches, which dominate planning time for wide folded pixels
+  int64_t b_room = 0;  // B bytes one SM can hold beside two A stages (an upper bound)
+  {
+    const int64_t plain = Q * NR * Wbox * 16;
+    const int64_t region_lb = (in_dtype == WF_TF32) ? plain : std::min<int64_t>(plain, (NR * Wbox * 32 + 1023) / 1024 * 1024);
+    const int64_t fixed_lb = kCtrlBytes + kStagingBytes + kTileM * 16 + 128 + kMaxAccCols * 4 + 1024;
+    b_room = kSmemLimit - fixed_lb - 2 * sh * region_lb;
+    if (b_room < 0) {
+      S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
+      *out = S;
+      return WF_OK;
+    }
+  }
   // 2-byte outputs: 64-column chunks (16 bf16 = 32 B per thread and row);
   // tf32 (fp32 outputs): 32-column chunks (8 fp32 = 32 B).
   S.CH = (in_dtype != WF_TF32 && S.Ng % 64 == 0) ? 64 : 32;
@@ -450,6 +466,31 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
       const int64_t off = ((-c0) * f + j * sw - d.pad_w) * d.c;
       lo[g] = std::min(lo[g], off / E2);
       hi[g] = std::max(hi[g], (off + d.kw * d.c - 1) / E2);
+    }
+  }
+  // A group's B operand holds at least one K-step per two (kh, core column) cells of its window
+  // (kpair's best case), and an N-tile's B is at most min(the 128 KB budget, the room beside two
+  // A stages) per SM. When one group exceeds that, or all of them need more than kMaxNTiles
+  // tiles, the N-tiling below fails for every budget: give up before the cover search, which
+  // is the planner's expensive part for wide windows
+  {
+    const int64_t pr = (pair_req == 1) ? 2 : 1;
+    const int64_t cap = pr * std::min<int64_t>(128 * 1024, b_room);
+    int64_t total = 0;
+    bool fits = cap > 0;
+    for (int64_t g = 0; g < G && fits; ++g) {
+      const int64_t lb = (d.kh * (hi[g] - lo[g] + 1) + 1) / 2 * static_cast<int64_t>(S.Ng) * 32;
+      fits = lb <= cap;
+      total += lb;
+    }
+    // and an N-tile holds whole groups of at most max_tile_cols accumulator columns (as below)
+    const int64_t mt_est = d.n * ceil_div(OH, OHt);
+    const int64_t tile_cols = (mt_est * 2 <= 148 && G > 1) ? S.Ng : kMaxAccCols;
+    const int64_t per_tile = tile_cols / S.Ng;
+    if (!fits || total > kMaxNTiles * cap || per_tile < 1 || ceil_div(G, per_tile) > kMaxNTiles) {
+      S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
+      *out = S;
+      return WF_OK;
     }
   }
   // ---- 32-byte K-steps ("units": core columns (c, c+1)) covering each group's window
@@ -494,9 +535,14 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
     return best;
   };
   if (Q >= 2) {
-    // all minimal non-straddling covers of [l, h]
+    // minimal non-straddling covers of [l, h]: two choices per K-step, so a wide
+    // group window (e.g. 7 folded outputs of 8 fp32 channels: 52 core columns)
+    // has 2^26 of them -- enumerate at most kMaxCovers (the joint search below
+    // looks at <= 4096 combinations anyway)
+    constexpr size_t kMaxCovers = 64;
     std::function<void(int64_t, int64_t, std::vector<int64_t>&, std::vector<std::vector<int64_t>>&)> covers =
         [&](int64_t p, int64_t h, std::vector<int64_t>& cur, std::vector<std::vector<int64_t>>& outv) {
+          if (outv.size() >= kMaxCovers) return;
           if (p > h) {
             outv.push_back(cur);
             return;
@@ -526,7 +572,7 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
         std::vector<size_t> idx(ng, 0);
         std::vector<std::vector<int64_t>> best_us;
         int64_t best = INT64_MAX;
-        for (int guard = 0; guard < 4096; ++guard) {
+        for (int guard = 0; guard < 512; ++guard) {
           std::vector<std::vector<int64_t>> us(ng);
           for (int64_t k = 0; k < ng; ++k) us[k] = cand[k][idx[k]];
           const int64_t c = best_order_cost(us);
