@@ -152,6 +152,7 @@ wf_status prepare_conv(const Schedule& S, const wf_conv_desc& d, PreparedLaunch&
   EncodeTiledFn encode = get_encode(err);
   if (!encode) return WF_CUDA_ERROR;
 
+  static_assert(kMaxTable == kMaxEntries, "the planner's entry limit is the kernel's table size");
   if (S.entries.size() > static_cast<size_t>(kMaxTable)) {
     *err = "schedule too long for the constant bank";
     return WF_UNSUPPORTED;

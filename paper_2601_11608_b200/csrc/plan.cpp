@@ -1000,6 +1000,11 @@ wf_status make_schedule_tps(const wf_conv_desc& d, int64_t f_req, int64_t gs_req
   p.tile_rows = OHt;
   p.wbox = Wbox;
   p.nrows = NR;
+  if (S.entries.size() > static_cast<size_t>(kMaxEntries)) {  // e.g. 11x11 fp32 windows on wide pixels
+    S.plan = fallback(WF_REASON_NOT_PROFITABLE, f);
+    *out = S;
+    return WF_OK;
+  }
   p.mma_entries = static_cast<int64_t>(S.entries.size());
   // packed header: schedule table, the slot -> group order (int32 each), then
   // the (core column 0, core column 1) words of every entry
@@ -1133,7 +1138,7 @@ wf_status make_schedule_unfolded(const wf_conv_desc& d, wf_dtype in_dtype, Sched
   S.stages = 0;
   for (int st2 = 4; st2 >= 2; --st2)
     if (fixed + static_cast<int64_t>(st2) * S.stage_bytes <= kSmemLimit) { S.stages = st2; break; }
-  if (S.stages == 0 || S.entries.size() > 384) {
+  if (S.stages == 0 || S.entries.size() > static_cast<size_t>(kMaxEntries)) {
     S.plan = fallback(WF_REASON_NOT_PROFITABLE, 1);
     *out = S;
     return WF_OK;

@@ -46,6 +46,7 @@ constexpr int kTileM = 128;           // tcgen05 M (cta_group::1)
 constexpr int kMaxAccCols = 256;      // accumulator columns per N-tile (x2 buffers)
 constexpr int kMaxResidues = 8;
 constexpr int kMaxNTiles = 16;
+constexpr int kMaxEntries = 384;     // schedule entries per launch (the kernel's constant-bank table)
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kStagingBytes = 0;  // epilogue writes straight from registers (no staging)
 constexpr int kRawSlots = 32;     // staged-row ring slots (row producer; >= the raw rows of a stage)
