@@ -134,3 +134,55 @@ def test_graph_captured_chain_keeps_order():
         torch.cuda.synchronize()
         for i, r in enumerate(refs):
             assert sums[i].item() == r.item(), f"graph replay: input {i} checksum differs"
+
+
+def test_layer_chain_reads_the_previous_conv_output():
+    """conv -> conv -> conv where each layer's input IS the previous layer's output buffer (no torch kernel
+    in between): every layer's prologue overlaps the previous grid under PDL and only its griddepcontrol.wait
+    orders the read of x after the producer's stores. Compared bitwise with the same chain synchronised
+    between layers, eagerly and captured in a CUDA graph."""
+    dt = torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(31)
+    shapes = [  # (cin, cout, k, stride, pad, relu)
+        (3, 32, 3, 1, 1, True), (32, 64, 3, 1, 1, True), (64, 32, 3, 2, 1, False), (32, 32, 1, 1, 0, True)]
+    n, h = 4, 64
+    convs, shape = [], (n, h, h, 3)
+    for cin, cout, k, s, p, relu in shapes:
+        w = ((torch.rand((k, k, cin, cout), generator=g, device="cuda") * 2 - 1) / (k * k * cin) ** 0.5).to(dt)
+        b = torch.rand(cout, generator=g, device="cuda") * 0.2 - 0.1
+        conv = wf.FoldedConv2d(w, b, shape, stride=s, padding=p, dtype=dt)
+        convs.append((conv, relu))
+        shape = conv.output_shape
+    xs = [(torch.rand((n, h, h, 3), generator=g, device="cuda") * 2 - 1).to(dt) for _ in range(5)]
+
+    def chain(x, sync):
+        for conv, relu in convs:
+            x = conv(x, relu=relu)
+            if sync:
+                torch.cuda.synchronize()
+        return x
+
+    refs = [chain(x, True).clone() for x in xs]
+    torch.cuda.synchronize()
+    outs = [chain(x, False) for x in xs for _ in range(2)]
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        assert torch.equal(o, refs[i // 2]), f"eager chain {i}: differs from the synchronised chain"
+    # the same chain in a graph (static buffers), replayed for every input
+    x_in = torch.empty_like(xs[0])
+    bufs = [torch.empty(c.output_shape, dtype=dt, device="cuda") for c, _ in convs]
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            cur = x_in
+            for (conv, relu), buf in zip(convs, bufs):
+                conv(cur, relu=relu, out=buf)
+                cur = buf
+    torch.cuda.current_stream().wait_stream(side)
+    for i, x in enumerate(xs):
+        x_in.copy_(x)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(bufs[-1], refs[i]), f"graph chain {i}: differs from the synchronised chain"
