@@ -7,6 +7,7 @@ is spent, each with a random planner knob, and checks every case two ways:
 Failures are printed with the case and the device plan; the last line is a JSON summary.
 
     python tools/fuzz_soak.py --seconds 900 --seed 1000
+    python tools/fuzz_soak.py --seconds 300 --threads 8 --plans 96   # concurrent launches over many plans
 """
 import argparse
 import json
@@ -103,13 +104,72 @@ def run_case(case):
                 os.environ[k] = v
 
 
+def thread_soak(seconds, seed, n_threads, n_convs):
+    """Host threads on their own streams launching a pool of random plans (more than the C-ABI's 64-entry
+    schedule cache, so entries are evicted while other threads launch from them); every result must equal
+    the one computed up front, bitwise."""
+    import threading
+    rng = random.Random(seed)
+    pool = []
+    while len(pool) < n_convs:
+        case = draw(rng)
+        n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, relu, knob, odt = case
+        if n * h * w * co > 40_000_000:
+            continue
+        tdt = TDT[dt]
+        g = torch.Generator(device="cuda").manual_seed(zlib.crc32(repr(case).encode()))
+        x = torch.randint(-3, 4, (n, h, w, c), generator=g, device="cuda").to(tdt)
+        wt = torch.randint(-3, 4, (kh, kw, c, co), generator=g, device="cuda").to(tdt)
+        b = torch.randint(-8, 9, (co,), generator=g, device="cuda").float()
+        try:
+            conv = wf.FoldedConv2d(wt, b, x.shape, stride=(sh, sw), padding=(ph, pw), dtype=tdt)
+        except wf.UnsupportedError:
+            continue
+        pool.append((case, conv, x, conv(x, relu=relu, out_dtype=torch.float32)))
+    torch.cuda.synchronize()
+    errors, counts = [], [0] * n_threads
+    t_end = time.time() + seconds
+
+    def worker(ti):
+        r = random.Random(seed * 100 + ti)
+        stream = torch.cuda.Stream()
+        mine = {}
+        try:
+            with torch.cuda.stream(stream):
+                while time.time() < t_end and not errors:
+                    k = r.randrange(len(pool))
+                    case, conv, x, ref = pool[k]
+                    if k not in mine:  # a private clone: its own workspace (re-pitch plans)
+                        mine[k] = conv.with_batch(x.shape[0])
+                    y = mine[k](x, relu=case[12], out_dtype=torch.float32)
+                    stream.synchronize()
+                    if not torch.equal(y, ref):
+                        errors.append((ti, case))
+                    counts[ti] += 1
+        except Exception as e:
+            errors.append((ti, repr(e)[:300]))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(n_threads)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    print(json.dumps({"mode": "threads", "threads": n_threads, "plans": len(pool), "launches": sum(counts),
+                      "seconds": seconds, "failures": errors[:10]}), flush=True)
+    return 1 if errors else 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=600)
     ap.add_argument("--seed", type=int, default=1000)
     ap.add_argument("--max-cases", type=int, default=10 ** 9)
     ap.add_argument("--trace", action="store_true", help="print every case before running it")
+    ap.add_argument("--threads", type=int, default=0, help="thread soak over a pool of plans instead")
+    ap.add_argument("--plans", type=int, default=96)
     args = ap.parse_args()
+    if args.threads:
+        return thread_soak(args.seconds, args.seed, args.threads, args.plans)
     rng = random.Random(args.seed)
     t0 = time.time()
     counts = {"pass": 0, "skip": 0, "fail": 0}
