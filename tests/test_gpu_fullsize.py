@@ -367,3 +367,28 @@ def test_large_images_exact(geom):
     for lo in range(0, n, 4):
         ref = conv_f64(x[lo:lo + 4], w, b, s, p)
         assert torch.equal(y[lo:lo + 4].double(), ref), f"images {lo}..{lo + 3} differ"
+
+
+@pytest.mark.parametrize("env", [{}, {"WF_GATHER": "1"}, {"WF_GATHER": "2"}, {"WF_RING": "1"}],
+                         ids=["repitch", "gather", "gather_direct", "ring"])
+def test_alexnet_input_past_4gb_every_producer(monkeypatch, env):
+    """AlexNet conv1 at batch 16384: a 5.07 GB input (past 32-bit byte offsets), a 5.2 GB re-pitch workspace
+    and a 19 GB fp32 output; the first, second, middle and last two images exact on integer data under every
+    unaligned-row producer."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    torch.cuda.empty_cache()
+    n = 16384
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randint(-3, 4, (n, 227, 227, 3), generator=g, device="cuda", dtype=torch.int8).to(torch.bfloat16)
+    w = torch.randint(-3, 4, (11, 11, 3, 96), generator=g, device="cuda").to(torch.bfloat16)
+    b = torch.randint(-8, 9, (96,), generator=g, device="cuda").float()
+    conv = wf.FoldedConv2d(w, b, x.shape, stride=4, padding=0, dtype=torch.bfloat16)
+    y = conv(x, out_dtype=torch.float32)
+    with torch.backends.cudnn.flags(enabled=False):  # exact float64 reference
+        for i in [0, 1, n // 2, n - 2, n - 1]:
+            ref = torch.nn.functional.conv2d(x[i:i + 1].double().permute(0, 3, 1, 2), w.double().permute(3, 2, 0, 1),
+                                             b.double(), stride=4).permute(0, 2, 3, 1)
+            assert torch.equal(y[i:i + 1].double(), ref), f"image {i} ({conv.device_plan['producer']})"
+    del x, y, conv
+    torch.cuda.empty_cache()
