@@ -27,6 +27,7 @@ TOL = {"bf16": 1e-2, "f16": 1e-2, "tf32": 1e-3}
 KNOBS = [{}, {"WF_KPAIR": "0"}, {"WF_KPAIR": "1"}, {"WF_TPS": "1"}, {"WF_TPS": "2"}, {"WF_MCAST": "1"},
          {"WF_MCAST": "0"}, {"WF_GATHER": "1"}, {"WF_GATHER": "2"}, {"WF_RING": "1"}, {"WF_PLANES": "0"},
          {"WF_NACC": "2"}, {"WF_EPI_PP": "1"}, {"WF_PDL": "0"}, {"WF_CTA_PAIR": "1"}]
+args_wide = False  # --wide: also Cout 320-1024 (several N-tiles per plan)
 PLAN_KEYS = ("f", "r", "group_size", "n_tiles", "producer", "kstep_mode", "stage_tiles", "wbox", "cta_pair")
 
 
@@ -38,15 +39,17 @@ def draw(rng):
             n, h, w = rng.randint(1, 6), rng.randint(4, 80), rng.randint(4, 260)
         elif kind < 0.9:  # many tiles per CTA (ring / barrier phase wrap-around)
             n, h, w = rng.randint(32, 320), rng.randint(6, 48), rng.randint(6, 72)
-        else:  # ImageNet-sized rows
+        elif kind < 0.97:  # ImageNet-sized rows
             n, h, w = rng.randint(1, 3), rng.randint(100, 240), rng.randint(200, 240)
+        else:  # very wide rows
+            n, h, w = rng.randint(1, 3), rng.randint(4, 24), rng.randint(256, 4096)
         c = rng.choice([1, 2, 3, 3, 3, 4, 6, 8])
         kh, kw = rng.choice([1, 2, 3, 5, 7, 11]), rng.choice([1, 2, 3, 5, 7, 11])
         sh, sw = rng.randint(1, 4), rng.randint(1, 4)
         ph, pw = rng.randint(0, kh // 2), rng.randint(0, kw // 2)
         if (h + 2 * ph - kh) // sh + 1 < 1 or (w + 2 * pw - kw) // sw + 1 < 1:
             continue
-        co = rng.choice([32, 64, 96, 128, 160, 192, 256])
+        co = rng.choice([32, 64, 96, 128, 160, 192, 256] + ([320, 384, 512, 1024] if args_wide else []))
         dt = rng.choice(["bf16", "f16", "tf32"])
         odt = rng.choice(["f32", "f32", "bf16", "f16"])
         return (n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, rng.random() < 0.3, rng.randrange(len(KNOBS)), odt)
@@ -167,7 +170,10 @@ def main():
     ap.add_argument("--trace", action="store_true", help="print every case before running it")
     ap.add_argument("--threads", type=int, default=0, help="thread soak over a pool of plans instead")
     ap.add_argument("--plans", type=int, default=96)
+    ap.add_argument("--wide", action="store_true", help="also draw Cout 320-1024")
     args = ap.parse_args()
+    global args_wide
+    args_wide = args.wide
     if args.threads:
         return thread_soak(args.seconds, args.seed, args.threads, args.plans)
     rng = random.Random(args.seed)
