@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "kernels.hpp"
@@ -118,21 +119,24 @@ __device__ __forceinline__ void repitch_store_any(const RowChunks& rc, uint8_t* 
 // layout's rows in shared memory to store them contiguously measured slower
 // than these scattered 16-byte stores: AlexNet b512 73 vs 61 us.)
 __global__ void __launch_bounds__(256) repitch_kernel(const uint8_t* __restrict__ x, uint8_t* __restrict__ y,
-                                                      long long rows, int rb_in, int rb_out, int Q, int plane_bytes) {
+                                                      long long rows, int rb_in, int rb_out, int Q, int plane_bytes,
+                                                      int rev) {
   const int lane = threadIdx.x & 31;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const int cpr = rb_out >> 4;
   for (long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows;
        r += 2 * nwarps) {
-    const long long r2 = r + nwarps;
-    const bool has2 = r2 < rows;
-    const uintptr_t src = reinterpret_cast<uintptr_t>(x) + r * rb_in;
-    const uintptr_t src2 = reinterpret_cast<uintptr_t>(x) + (has2 ? r2 : r) * rb_in;
+    const bool has2 = r + nwarps < rows;
+    // rev: rows in descending order, so the rows written last (still in L2) are the first the conv reads
+    const long long ra = rev ? rows - 1 - r : r;
+    const long long r2 = has2 ? (rev ? rows - 1 - (r + nwarps) : r + nwarps) : ra;
+    const uintptr_t src = reinterpret_cast<uintptr_t>(x) + ra * rb_in;
+    const uintptr_t src2 = reinterpret_cast<uintptr_t>(x) + r2 * rb_in;
     const uint4* a0 = reinterpret_cast<const uint4*>(src & ~static_cast<uintptr_t>(15));
     const uint4* a2 = reinterpret_cast<const uint4*>(src2 & ~static_cast<uintptr_t>(15));
     const int sh = static_cast<int>(src & 15u), sh2 = static_cast<int>(src2 & 15u);
     const int nin = (sh + rb_in + 15) >> 4, nin2 = (sh2 + rb_in + 15) >> 4;  // aligned chunks holding the row
-    uint8_t* const d1 = y + r * rb_out;
+    uint8_t* const d1 = y + ra * rb_out;
     uint8_t* const d2 = y + r2 * rb_out;
     for (int s0 = 0; s0 < cpr; s0 += 32 * kRepitchRounds) {
       RowChunks c1, c2;
@@ -144,12 +148,20 @@ __global__ void __launch_bounds__(256) repitch_kernel(const uint8_t* __restrict_
   }
 }
 
+static int repitch_reverse() {
+  static const int rev = [] {
+    const char* e = std::getenv("WF_REPITCH_REV");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return rev;
+}
+
 wf_status launch_repitch(const void* x, void* ws, long long rows, int rb_in, int rb_out, int planes,
                          cudaStream_t st, std::string* err) {
   const int threads = 256;  // 8 warps, one row each at a time
   const int blocks = static_cast<int>(std::min<long long>((rows + 7) / 8, 148LL * 8));
   repitch_kernel<<<blocks, threads, 0, st>>>(static_cast<const uint8_t*>(x), static_cast<uint8_t*>(ws), rows, rb_in,
-                                             rb_out, planes, planes > 0 ? rb_out / planes : 0);
+                                             rb_out, planes, planes > 0 ? rb_out / planes : 0, repitch_reverse());
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("repitch_kernel: ") + cudaGetErrorString(e);
