@@ -14,7 +14,8 @@ count = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 ran = 0
 for case in CASES2[:count]:
     n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, relu, knob = case
-    for key in ("WF_KPAIR", "WF_TPS", "WF_MCAST", "WF_GATHER", "WF_RING", "WF_PLANES", "WF_NACC", "WF_EPI_PP", "WF_PDL"):
+    for key in ("WF_KPAIR", "WF_TPS", "WF_MCAST", "WF_GATHER", "WF_RING", "WF_PLANES", "WF_NACC", "WF_EPI_PP", "WF_PDL",
+                "WF_CTA_PAIR"):
         os.environ.pop(key, None)
     os.environ.update(KNOBS[knob])
     tdt = TDT[dt]
@@ -26,8 +27,9 @@ for case in CASES2[:count]:
     except wf.UnsupportedError:
         continue
     y = conv(x, relu=relu, out_dtype=torch.float32)
-    ref = torch.nn.functional.conv2d(x.double().permute(0, 3, 1, 2), wt.double().permute(3, 2, 0, 1), b.double(),
-                                     stride=(sh, sw), padding=(ph, pw)).permute(0, 2, 3, 1)
+    with torch.backends.cudnn.flags(enabled=False):  # exact float64 reference (cuDNN's is not for every shape)
+        ref = torch.nn.functional.conv2d(x.double().permute(0, 3, 1, 2), wt.double().permute(3, 2, 0, 1),
+                                         b.double(), stride=(sh, sw), padding=(ph, pw)).permute(0, 2, 3, 1)
     if relu:
         ref = torch.relu(ref)
     assert torch.equal(y.double(), ref), case
