@@ -28,6 +28,7 @@ KNOBS = [{}, {"WF_KPAIR": "0"}, {"WF_KPAIR": "1"}, {"WF_TPS": "1"}, {"WF_TPS": "
          {"WF_MCAST": "0"}, {"WF_GATHER": "1"}, {"WF_GATHER": "2"}, {"WF_RING": "1"}, {"WF_PLANES": "0"},
          {"WF_NACC": "2"}, {"WF_EPI_PP": "1"}, {"WF_PDL": "0"}, {"WF_CTA_PAIR": "1"}]
 args_wide = False  # --wide: also Cout 320-1024 (several N-tiles per plan)
+args_unfolded = False  # --unfolded: 30% of the 16-bit cases through the unfolded variant (the zero-pad/im2col baseline)
 PLAN_KEYS = ("f", "r", "group_size", "n_tiles", "producer", "kstep_mode", "stage_tiles", "wbox", "cta_pair")
 
 
@@ -52,11 +53,14 @@ def draw(rng):
         co = rng.choice([32, 64, 96, 128, 160, 192, 256] + ([320, 384, 512, 1024] if args_wide else []))
         dt = rng.choice(["bf16", "f16", "tf32"])
         odt = rng.choice(["f32", "f32", "bf16", "f16"])
-        return (n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, rng.random() < 0.3, rng.randrange(len(KNOBS)), odt)
+        case = (n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, rng.random() < 0.3, rng.randrange(len(KNOBS)), odt)
+        if args_unfolded and dt != "tf32" and rng.random() < 0.3:
+            case = case + ("unfolded",)
+        return case
 
 
 def f64_conv(x, w, b, case):
-    n, h, wd, c, kh, kw, sh, sw, ph, pw, co, dt, relu, knob, odt = case
+    n, h, wd, c, kh, kw, sh, sw, ph, pw, co, dt, relu, knob, odt = case[:15]
     with torch.backends.cudnn.flags(enabled=False):  # cuDNN's float64 algorithms are not exact for every shape
         y = torch.nn.functional.conv2d(x.double().permute(0, 3, 1, 2), w.double().permute(3, 2, 0, 1), b.double(),
                                        stride=(sh, sw), padding=(ph, pw)).permute(0, 2, 3, 1)
@@ -64,7 +68,8 @@ def f64_conv(x, w, b, case):
 
 
 def run_case(case):
-    n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, relu, knob, odt = case
+    n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, relu, knob, odt = case[:15]
+    variant = case[15] if len(case) > 15 else "fold"
     saved = {k: os.environ.get(k) for k in KNOBS[knob]}
     os.environ.update(KNOBS[knob])
     try:
@@ -74,7 +79,7 @@ def run_case(case):
         wi = torch.randint(-3, 4, (kh, kw, c, co), generator=g, device="cuda").to(tdt)
         bi = torch.randint(-8, 9, (co,), generator=g, device="cuda").float()
         try:
-            conv = wf.FoldedConv2d(wi, bi, xi.shape, stride=(sh, sw), padding=(ph, pw), dtype=tdt)
+            conv = wf.FoldedConv2d(wi, bi, xi.shape, stride=(sh, sw), padding=(ph, pw), dtype=tdt, variant=variant)
         except wf.UnsupportedError:
             return "skip", None, None
         plan = {k: conv.device_plan.get(k) for k in PLAN_KEYS}
@@ -86,7 +91,7 @@ def run_case(case):
         xr = (torch.rand((n, h, w, c), generator=g, device="cuda") * 2 - 1).to(tdt)
         wr = ((torch.rand((kh, kw, c, co), generator=g, device="cuda") * 2 - 1) / (kh * kw * c) ** 0.5).to(tdt)
         br = torch.rand((co,), generator=g, device="cuda") * 2 - 1
-        conv2 = wf.FoldedConv2d(wr, br, xr.shape, stride=(sh, sw), padding=(ph, pw), dtype=tdt)
+        conv2 = wf.FoldedConv2d(wr, br, xr.shape, stride=(sh, sw), padding=(ph, pw), dtype=tdt, variant=variant)
         out_t = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}[odt]
         if dt == "tf32" and out_t != torch.float32:
             out_t = torch.float32
@@ -116,7 +121,7 @@ def thread_soak(seconds, seed, n_threads, n_convs):
     pool = []
     while len(pool) < n_convs:
         case = draw(rng)
-        n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, relu, knob, odt = case
+        n, h, w, c, kh, kw, sh, sw, ph, pw, co, dt, relu, knob, odt = case[:15]
         if n * h * w * co > 40_000_000:
             continue
         tdt = TDT[dt]
@@ -171,9 +176,11 @@ def main():
     ap.add_argument("--threads", type=int, default=0, help="thread soak over a pool of plans instead")
     ap.add_argument("--plans", type=int, default=96)
     ap.add_argument("--wide", action="store_true", help="also draw Cout 320-1024")
+    ap.add_argument("--unfolded", action="store_true", help="also run the unfolded variant")
     args = ap.parse_args()
-    global args_wide
+    global args_wide, args_unfolded
     args_wide = args.wide
+    args_unfolded = args.unfolded
     if args.threads:
         return thread_soak(args.seconds, args.seed, args.threads, args.plans)
     rng = random.Random(args.seed)
@@ -192,7 +199,8 @@ def main():
             status, plan, msg = "fail", None, repr(e)[:300]
         counts[status] += 1
         if plan:
-            producers[plan["producer"]] = producers.get(plan["producer"], 0) + 1
+            key = plan["producer"] + ("/unfolded" if len(case) > 15 else "")
+            producers[key] = producers.get(key, 0) + 1
             kn = json.dumps(KNOBS[case[13]])
             knobs[kn] = knobs.get(kn, 0) + 1
         if i % 50 == 0:
