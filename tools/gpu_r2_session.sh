@@ -15,6 +15,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_fold -s 2 -c 1 -o gpurun_out/prof_vgg_b256 -f python tools/prof_conv.py vgg 256 0 0 3 > gpurun_out/ncu_full_vgg.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_fold -s 2 -c 1 -o gpurun_out/prof_alex_b512 -f \
    python tools/prof_conv.py alex 512 0 0 3 > gpurun_out/ncu_full_alex.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_fold -s 2 -c 1 -o gpurun_out/prof_mnv2_b1024 -f \
+   python tools/prof_conv.py mnv2 1024 0 0 3 > gpurun_out/ncu_full_mnv2.log 2>&1
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:conv_fold -s 1 -c 1 --csv --log-file gpurun_out/traffic_r50_n8192.csv \
    python tools/prof_conv.py r50 8192 0 0 1 > gpurun_out/ncu_traffic.log 2>&1
 bash tools/gpu_sanitize.sh > /dev/null 2>&1
