@@ -2,7 +2,7 @@
 # device soak (tools/fuzz_soak.py) with a host-memory watchdog on its exact PID
 mkdir -p gpurun_out
 SECS=${1:-1200}; SEED=${2:-1000}; EXTRA=${3:-}
-timeout $((SECS + 300)) python tools/fuzz_soak.py --seconds $SECS --seed $SEED --trace $EXTRA > gpurun_out/soak_$SEED.log 2>&1 &
+timeout $((SECS + 300)) python tools/fuzz_soak.py --seconds $SECS --seed $SEED $EXTRA > gpurun_out/soak_$SEED.log 2>&1 &
 P=$!
 while kill -0 $P 2>/dev/null; do
   avail=$(free -m | awk '/Mem/{print $7}')
